@@ -1,0 +1,175 @@
+/* include/dmoe.h — C ABI of the B200-native DMoE layer hot path (libdmoe.so).
+ *
+ * The calls follow the paper's statement of the layer (Ryabinin & Gusev,
+ * "Learning@home", arXiv 2002.04013; line numbers refer to PAPER.md):
+ *   - run the gating function to select k experts out of N       (§3.1)
+ *       dmoe_gate_scores  (Eq. 2)
+ *       dmoe_beam_topk    (Alg. 1 SelectExperts + FilterAlive)
+ *   - send inputs to those experts and collect outputs           (§3.1)
+ *       dmoe_dispatch     (renormalised Eq. 3 weights + per-expert batching)
+ *       dmoe_expert_ffn_fwd (runtime Forward request)
+ *   - aggregate expert outputs by weighted averaging             (Eq. 3)
+ *       dmoe_combine
+ *   - backward: runtime Backward request + gating gradient
+ *       dmoe_combine_bwd, dmoe_expert_ffn_bwd, dmoe_gate_bwd
+ *
+ * Readings where the paper is silent or garbled (X1..X19):
+ *   X1  expert uid (u_0..u_{d-1}) <-> flat index e = sum_i u_i M^(d-1-i), u_0 most significant.
+ *   X2  Eq. 3's denominator is the standard softmax over the beam (index typo read as f_j).
+ *   X3  beam width B >= k (B = k is the paper's Alg. 1); the last level keeps k.
+ *   X4  ties broken by the total order (score descending, flat index ascending);
+ *       -0.0 is treated as +0.0.
+ *   X5  a prefix is alive iff at least one alive expert lies below it; FilterAlive runs
+ *       before TopK at every level, including the last.
+ *   X6  fewer than k alive experts: sel padded with -1, sel_score with -inf.
+ *   X7  a token whose selected experts all failed is dropped: valid = 0, y = 0,
+ *       zero gradient; counted in n_dropped (PAPER.md:287 footnote).
+ *   X8  `responded` is known at dispatch time; non-responders are not dispatched.
+ *   X11 the linear gate is affine (x W_g + b_g); logits G are fp32.
+ *   X12 no gradient through the discrete selection.
+ *   X13 ReLU'(0) = 0.
+ *   X14 expert = 2-linear FFN D -> H -> D with bias and ReLU.
+ *   X15 bf16 storage with fp32 accumulation; G, w, dscore, biases and all bias/gate
+ *       gradients are fp32; H, Out, dW are stored in the parameter dtype.
+ *   X18 rows inside an expert segment are in increasing token order.
+ *
+ * Conventions for every call:
+ *   - All pointers are caller-owned DEVICE memory unless marked (host); row-major,
+ *     contiguous; 16-byte aligned (the caller's cudaMalloc / torch allocations are).
+ *   - Work is enqueued on `stream`; no call synchronises the host or allocates memory.
+ *     Scratch comes from the caller's workspace `ws` of at least
+ *     dmoe_workspace_bytes(...) bytes (re-usable across calls on one stream).
+ *   - Outputs are fully overwritten; callers never pre-zero (dW of an expert with no
+ *     rows is written as 0; y and dX of dropped tokens are 0).
+ *   - Argument/shape validation is synchronous and returns DMOE_ERR_* without
+ *     enqueueing anything; launch failures return DMOE_ERR_CUDA; asynchronous kernel
+ *     faults surface on a later CUDA call.  dmoe_last_error() gives a message.
+ *   - Deterministic: no floating-point atomics; results are bitwise reproducible.
+ *   - dtype DMOE_BF16 runs the tcgen05 tensor-core path for the contractions;
+ *     DMOE_F32 runs exact fp32 SIMT kernels (no TF32), for the fp32 parity config.
+ *   - "Batch dropped" is not an error (reported per token through valid/n_dropped).
+ */
+#ifndef DMOE_H
+#define DMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dmoe_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  DMOE_OK = 0,
+  DMOE_ERR_ARG = -1,         /* null pointer, negative size, bad enum */
+  DMOE_ERR_SHAPE = -2,       /* dimension outside the supported envelope or inconsistent */
+  DMOE_ERR_UNSUPPORTED = -3, /* valid request the library does not implement */
+  DMOE_ERR_CUDA = -4         /* a CUDA launch / driver call failed */
+} dmoe_status;
+
+typedef enum { DMOE_F32 = 0, DMOE_BF16 = 1 } dmoe_dtype;
+
+/* Expert grid of Eq. 1: E = M^d experts, k selected per token,
+ * beam width `beam` (0 means k).  Envelope: 1 <= d <= 4, 1 <= M <= 1024, d*M <= 256,
+ * M^d < 2^31, 1 <= k <= 16, k <= beam <= 32, beam*M <= 8192. */
+typedef struct {
+  int32_t d, M, k, beam;
+} dmoe_grid;
+
+const char* dmoe_last_error(void); /* thread-local text for the last non-OK status */
+int32_t dmoe_version(void);
+
+/* Scratch needed by any call below for T tokens, d_model D, hidden H, E_local experts
+ * on this rank and R_cap dispatched-row capacity (T*k on one GPU). */
+size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_t E_local,
+                            int64_t R_cap);
+
+/* S1 — gate scores, Eq. 2:
+ *   G[t, i*M + j] = g_i(x_t, j) = b_g[i*M + j] + sum_c x[t, c] * W_g[c, i*M + j]
+ * x [T, D] in dtype dt; W_g [D, d*M] in dt; b_g [d*M] fp32; G [T, d*M] fp32 (out). */
+dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg,
+                             const float* bg, dmoe_grid g, float* G, dmoe_stream_t stream);
+
+/* S2+S3 — SelectExperts, Alg. 1 with FilterAlive,
+ * per token: beam := [()]; for level i: expand every prefix p by j in [0,M) with score
+ * s_p + G[t, i*M+j]; drop candidates whose prefix has no alive expert (X5); keep the
+ * best B (k at the last level) under the order of X4.
+ * G [T, d*M] fp32; alive_bits [ceil(E/32)] uint32, bit e%32 of word e/32 = expert e alive.
+ * sel [T, k] int32 out: flat expert index per slot, best first, -1 pad (X6);
+ * sel_score [T, k] fp32 out: the Eq. 2 score sum of the slot, -inf pad. */
+dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive_bits,
+                           int32_t* sel, float* sel_score, void* ws, size_t ws_bytes,
+                           dmoe_stream_t stream);
+
+/* S4+S5 — renormalised Eq. 3 weights and per-expert dispatch:
+ *   ok[t,s]  = sel[t,s] >= 0 && responded(sel[t,s])                  (X8)
+ *   w[t,s]   = exp(sel_score[t,s] - m_t) / sum_{ok r} exp(sel_score[t,r] - m_t), 0 if !ok
+ *   valid[t] = any ok;  n_dropped = #tokens with !valid               (X7)
+ *   rows of expert e = ok pairs with sel == e in increasing t (X18), segments by e;
+ *   counts [E], offsets [E+1] (exclusive scan), row_of_slot [T,k] (-1 if !ok),
+ *   token_of_row [R] (capacity T*k), xd [R, D] = x[token_of_row[r]] (capacity T*k rows).
+ * x [T, D] in dt; responded_bits [ceil(E/32)] uint32; w [T,k] fp32; valid [T] uint8;
+ * n_dropped [1] int32 (device). */
+dmoe_status dmoe_dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, dmoe_grid g,
+                          const int32_t* sel, const float* sel_score,
+                          const uint32_t* responded_bits, float* w, uint8_t* valid,
+                          int32_t* n_dropped, int32_t* counts, int32_t* offsets,
+                          int32_t* row_of_slot, int32_t* token_of_row, void* xd, void* ws,
+                          size_t ws_bytes, dmoe_stream_t stream);
+
+/* S6 — grouped expert FFN forward, the runtime Forward request:
+ * for expert e < E_local, rows r in [offsets[e], offsets[e+1]):
+ *   h[r]   = relu(W1[e] xd[r] + b1[e])     (H outputs, stored in dt: saved for backward)
+ *   out[r] = W2[e] h[r] + b2[e]            (D outputs, dt)
+ * xd [R_cap, D] dt; offsets [E_local+1] int32 device, non-decreasing, offsets[E_local] <= R_cap;
+ * W1 [E_local, H, D] dt; b1 [E_local, H] fp32; W2 [E_local, D, H] dt; b2 [E_local, D] fp32;
+ * h [R_cap, H] dt (out); out [R_cap, D] dt (out).  bf16 needs D % 64 == 0, H % 64 == 0. */
+dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t E_local,
+                                int64_t R_cap, int32_t D, int32_t H, dmoe_dtype dt,
+                                const void* W1, const float* b1, const void* W2, const float* b2,
+                                void* h, void* out, void* ws, size_t ws_bytes,
+                                dmoe_stream_t stream);
+
+/* S7 — combine, Eq. 3: y[t] = sum_{ok s} w[t,s] out[row_of_slot[t,s]]
+ * (fp32 accumulate), y[t] = 0 if !valid[t].  out [R, D] dt; y [T, D] dt (out). */
+dmoe_status dmoe_combine(const void* out, const int32_t* row_of_slot, const float* w,
+                         const uint8_t* valid, int64_t T, int32_t D, int32_t k, dmoe_dtype dt,
+                         void* y, dmoe_stream_t stream);
+
+/* S8 — combine backward (softmax Jacobian of Eq. 3 over the ok slots):
+ *   a[t,s] = <dy[t], out[row]>;  dscore[t,s] = w[t,s] (a[t,s] - sum_{ok r} w[t,r] a[t,r]);
+ *   dout[row] = w[t,s] dy[t]  (the Backward request's output gradient).
+ * dy [T, D] dt; dout [R, D] dt (out); dscore [T, k] fp32 (out, 0 for !ok). */
+dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
+                             const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt,
+                             void* dout, float* dscore, dmoe_stream_t stream);
+
+/* S9 — grouped expert FFN backward, the runtime Backward request:
+ *   dh  = (dout W2[e]) * 1[h > 0]   (X13)
+ *   dxd = dh W1[e]
+ *   dW2[e] = sum_rows dout^T h;  db2[e] = sum_rows dout
+ *   dW1[e] = sum_rows dh^T xd;   db1[e] = sum_rows dh      (0 for experts without rows)
+ * dxd [R_cap, D] dt (out); dW1 [E_local, H, D] dt; dW2 [E_local, D, H] dt; db1 [E_local, H]
+ * and db2 [E_local, D] fp32 (out). */
+dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
+                                const int32_t* offsets, int32_t E_local, int64_t R_cap,
+                                int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
+                                const void* W2, void* dxd, void* dW1, float* db1, void* dW2,
+                                float* db2, void* ws, size_t ws_bytes, dmoe_stream_t stream);
+
+/* S10 — undispatch + gate backward (gradient of Eq. 2 through the Eq. 3 softmax):
+ *   dG[t, i*M + u_i(sel[t,s])] += dscore[t,s]            (u_i per X1)
+ *   dx[t]  = sum_{ok s} dxd[row_of_slot[t,s]] + sum_j dG[t,j] W_g[:, j]
+ *   dWg    = sum_t x[t]^T dG[t]  ([D, d*M] fp32);  dbg = sum_t dG[t]  ([d*M] fp32)
+ * x [T, D] dt; W_g [D, d*M] dt; dxd [R, D] dt; dx [T, D] dt (out). */
+dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, const float* dscore,
+                          const void* dxd, const int32_t* row_of_slot, int64_t T, int32_t D,
+                          dmoe_grid g, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
+                          size_t ws_bytes, dmoe_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DMOE_H */

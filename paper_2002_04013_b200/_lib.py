@@ -1,0 +1,144 @@
+"""Thin ctypes binding of libdmoe.so (include/dmoe.h).
+
+Argument marshalling only: every function takes torch CUDA tensors, reads shapes and
+data pointers, passes torch's current stream, and raises on a non-OK status.  No compute
+happens here and there is no fallback: importing fails loudly if the library is missing.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdmoe.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `make` or __graft_entry__.build() (no CPU fallback exists)")
+
+_L = ctypes.CDLL(LIB_PATH)
+
+DMOE_F32, DMOE_BF16 = 0, 1
+_STATUS = {0: "DMOE_OK", -1: "DMOE_ERR_ARG", -2: "DMOE_ERR_SHAPE", -3: "DMOE_ERR_UNSUPPORTED", -4: "DMOE_ERR_CUDA"}
+
+
+class dmoe_grid(ctypes.Structure):
+    _fields_ = [("d", ctypes.c_int32), ("M", ctypes.c_int32), ("k", ctypes.c_int32), ("beam", ctypes.c_int32)]
+
+
+class DMoEError(RuntimeError):
+    def __init__(self, fn, status):
+        msg = _L.dmoe_last_error().decode()
+        super().__init__(f"{fn}: {_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_P, _I64, _I32, _SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+_SIGS = {
+    "dmoe_last_error": ([], ctypes.c_char_p),
+    "dmoe_version": ([], ctypes.c_int32),
+    "dmoe_workspace_bytes": ([_I64, _I32, _I32, dmoe_grid, _I32, _I64], ctypes.c_size_t),
+    "dmoe_gate_scores": ([_P, _I32, _I64, _I32, _P, _P, dmoe_grid, _P, _P], ctypes.c_int),
+    "dmoe_beam_topk": ([_P, _I64, dmoe_grid, _P, _P, _P, _P, _SZ, _P], ctypes.c_int),
+    "dmoe_dispatch": ([_P, _I32, _I64, _I32, dmoe_grid, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
+                       _SZ, _P], ctypes.c_int),
+    "dmoe_expert_ffn_fwd": ([_P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
+                            ctypes.c_int),
+    "dmoe_combine": ([_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P], ctypes.c_int),
+    "dmoe_combine_bwd": ([_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P], ctypes.c_int),
+    "dmoe_expert_ffn_bwd": ([_P, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
+                             _SZ, _P], ctypes.c_int),
+    "dmoe_gate_bwd": ([_P, _P, _P, _P, _P, _P, _I64, _I32, dmoe_grid, _I32, _P, _P, _P, _P, _SZ, _P],
+                      ctypes.c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_L, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)
+
+
+def _check(fn, st):
+    if st != 0:
+        raise DMoEError(fn, st)
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _dt(t):
+    if t.dtype == torch.bfloat16:
+        return DMOE_BF16
+    if t.dtype == torch.float32:
+        return DMOE_F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def grid(d, M, k, beam=0):
+    return dmoe_grid(d, M, k, beam)
+
+
+def dmoe_version():
+    return _L.dmoe_version()
+
+
+def dmoe_workspace_bytes(T, D, H, g, E_local, R_cap):
+    return int(_L.dmoe_workspace_bytes(T, D, H, g, E_local, R_cap))
+
+
+def dmoe_gate_scores(x, Wg, bg, g, G):
+    T, D = x.shape
+    _check("dmoe_gate_scores", _L.dmoe_gate_scores(_p(x), _dt(x), T, D, _p(Wg), _p(bg), g, _p(G), _stream()))
+
+
+def dmoe_beam_topk(G, g, alive_bits, sel, sel_score, ws):
+    _check("dmoe_beam_topk", _L.dmoe_beam_topk(_p(G), G.shape[0], g, _p(alive_bits), _p(sel), _p(sel_score),
+                                               _p(ws), ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_dispatch(x, g, sel, sel_score, responded_bits, w, valid, n_dropped, counts, offsets,
+                  row_of_slot, token_of_row, xd, ws):
+    T, D = x.shape
+    _check("dmoe_dispatch", _L.dmoe_dispatch(
+        _p(x), _dt(x), T, D, g, _p(sel), _p(sel_score), _p(responded_bits), _p(w), _p(valid), _p(n_dropped),
+        _p(counts), _p(offsets), _p(row_of_slot), _p(token_of_row), _p(xd), _p(ws),
+        ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_expert_ffn_fwd(xd, offsets, W1, b1, W2, b2, h, out, ws):
+    E_local, H, D = W1.shape
+    _check("dmoe_expert_ffn_fwd", _L.dmoe_expert_ffn_fwd(
+        _p(xd), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd), _p(W1), _p(b1), _p(W2), _p(b2), _p(h),
+        _p(out), _p(ws), ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_combine(out, row_of_slot, w, valid, y):
+    T, D = y.shape
+    _check("dmoe_combine", _L.dmoe_combine(_p(out), _p(row_of_slot), _p(w), _p(valid), T, D,
+                                           row_of_slot.shape[1], _dt(y), _p(y), _stream()))
+
+
+def dmoe_combine_bwd(dy, out, row_of_slot, w, dout, dscore):
+    T, D = dy.shape
+    _check("dmoe_combine_bwd", _L.dmoe_combine_bwd(_p(dy), _p(out), _p(row_of_slot), _p(w), T, D,
+                                                   row_of_slot.shape[1], _dt(dy), _p(dout), _p(dscore),
+                                                   _stream()))
+
+
+def dmoe_expert_ffn_bwd(xd, h, dout, offsets, W1, W2, dxd, dW1, db1, dW2, db2, ws):
+    E_local, H, D = W1.shape
+    _check("dmoe_expert_ffn_bwd", _L.dmoe_expert_ffn_bwd(
+        _p(xd), _p(h), _p(dout), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd), _p(W1), _p(W2), _p(dxd),
+        _p(dW1), _p(db1), _p(dW2), _p(db2), _p(ws), ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, g, dx, dWg, dbg, ws):
+    T, D = x.shape
+    _check("dmoe_gate_bwd", _L.dmoe_gate_bwd(
+        _p(x), _p(Wg), _p(sel), _p(dscore), _p(dxd), _p(row_of_slot), T, D, g, _dt(x), _p(dx), _p(dWg),
+        _p(dbg), _p(ws), ws.numel() * ws.element_size(), _stream()))

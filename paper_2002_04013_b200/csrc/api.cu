@@ -1,0 +1,272 @@
+// api.cu — the C ABI of include/dmoe.h: argument validation, workspace carving and the
+// launch sequence of each call.  Every step of the hot path runs in this library's
+// kernels; there is no host compute and no fallback outside the GPU.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace dmoe {
+
+static thread_local char g_err[512] = "";
+
+dmoe_status set_error(dmoe_status st, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return st;
+}
+
+dmoe_status check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(DMOE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return DMOE_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = kNumSMs;
+  }
+  return n;
+}
+
+// declared in the kernel files
+dmoe_status beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive_bits,
+                      int32_t* sel, float* sel_score, uint32_t* PA, cudaStream_t s);
+size_t prefix_words(int d, int M);
+size_t dispatch_ws_bytes(int64_t T, int64_t E);
+dmoe_status dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, int64_t E, int32_t k,
+                     const int32_t* sel, const float* sel_score, const uint32_t* responded,
+                     float* w, uint8_t* valid, int32_t* n_dropped, int32_t* counts,
+                     int32_t* offsets, int32_t* row_of_slot, int32_t* token_of_row, void* xd,
+                     int32_t* plan128, int32_t* plan64, void* ws, size_t ws_bytes, cudaStream_t s);
+dmoe_status combine(const void* out, const int32_t* row_of_slot, const float* w,
+                    const uint8_t* valid, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* y,
+                    cudaStream_t s);
+dmoe_status combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
+                        const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout,
+                        float* dscore, cudaStream_t s);
+size_t gate_bwd_ws_bytes(int64_t T, int32_t D, int dM);
+dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const float* dscore,
+                     const void* dxd, const int32_t* row_of_slot, int64_t T, int32_t D, int d, int M,
+                     int k, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
+                     size_t ws_bytes, cudaStream_t s);
+
+static dmoe_status check_grid(dmoe_grid* g, int64_t* E) {
+  if (g->beam == 0) g->beam = g->k;
+  DMOE_REQUIRE(g->d >= 1 && g->d <= 4, DMOE_ERR_SHAPE, "grid: d=%d outside [1,4]", g->d);
+  DMOE_REQUIRE(g->M >= 1 && g->M <= 1024, DMOE_ERR_SHAPE, "grid: M=%d outside [1,1024]", g->M);
+  DMOE_REQUIRE(g->d * g->M <= 256, DMOE_ERR_SHAPE, "grid: d*M=%d > 256", g->d * g->M);
+  DMOE_REQUIRE(g->k >= 1 && g->k <= 16, DMOE_ERR_SHAPE, "grid: k=%d outside [1,16]", g->k);
+  DMOE_REQUIRE(g->beam >= g->k && g->beam <= 32, DMOE_ERR_SHAPE, "grid: beam=%d outside [k,32]", g->beam);
+  DMOE_REQUIRE((int64_t)g->beam * g->M <= 8192, DMOE_ERR_SHAPE, "grid: beam*M > 8192");
+  int64_t e = 1;
+  for (int i = 0; i < g->d; ++i) e *= g->M;
+  DMOE_REQUIRE(e < (1ll << 31), DMOE_ERR_SHAPE, "grid: M^d >= 2^31");
+  *E = e;
+  return DMOE_OK;
+}
+
+static dmoe_status check_dt(dmoe_dtype dt, int32_t D) {
+  DMOE_REQUIRE(dt == DMOE_F32 || dt == DMOE_BF16, DMOE_ERR_ARG, "dtype %d unknown", (int)dt);
+  const int v = dt == DMOE_BF16 ? 8 : 4;
+  DMOE_REQUIRE(D >= v && D % v == 0, DMOE_ERR_SHAPE, "D=%d must be a positive multiple of %d", D, v);
+  return DMOE_OK;
+}
+
+#define NN(p) DMOE_REQUIRE((p) != nullptr, DMOE_ERR_ARG, "%s: null pointer `%s`", __func__, #p)
+
+static dmoe_status rows_gemm(const GemmRows& g, dmoe_dtype dt, cudaStream_t s) {
+  if (dt == DMOE_BF16 && tc_rows_supported(g)) return tc_gemm_rows(g, s);
+  return simt_gemm_rows(g, dt, s);
+}
+static dmoe_status segk_gemm(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
+  if (dt == DMOE_BF16 && tc_segk_supported(g)) return tc_gemm_segk(g, s);
+  return simt_gemm_segk(g, dt, s);
+}
+constexpr int kPlanBM_TC = 128, kPlanBM_SIMT = 64;
+
+}  // namespace dmoe
+
+using namespace dmoe;
+
+extern "C" {
+
+const char* dmoe_last_error(void) { return g_err; }
+int32_t dmoe_version(void) { return 1; }
+
+size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_t E_local,
+                            int64_t R_cap) {
+  int64_t E = 1;
+  for (int i = 0; i < g.d; ++i) E *= g.M;
+  size_t beam = prefix_words(g.d, g.M) * 4 + 256;
+  size_t disp = dispatch_ws_bytes(T, E);
+  size_t ffn = 2 * align_up((size_t)(E_local + 1) * 4, 256) + align_up((size_t)R_cap * H * 4, 256) + 1024;
+  size_t gate = gate_bwd_ws_bytes(T, D, g.d * g.M);
+  size_t m = beam;
+  if (disp > m) m = disp;
+  if (ffn > m) m = ffn;
+  if (gate > m) m = gate;
+  return align_up(m, 4096);
+}
+
+dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg,
+                             const float* bg, dmoe_grid g, float* G, dmoe_stream_t stream) {
+  int64_t E = 0;
+  DMOE_TRY(check_grid(&g, &E));
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
+  if (T == 0) return DMOE_OK;
+  NN(x); NN(Wg); NN(bg); NN(G);
+  GemmRows r{};
+  r.A = x; r.B = Wg; r.C = G; r.bias = bg; r.aux = nullptr;
+  r.offsets = nullptr; r.plan = nullptr;
+  r.E = 1; r.N = g.d * g.M; r.K = D; r.rows_single = T;
+  r.b_mn = true; r.epi = EPI_F32_BIAS;
+  const bool tc = dt == DMOE_BF16 && tc_rows_supported(r);
+  r.max_tiles = ceil_div(T, tc ? kPlanBM_TC : kPlanBM_SIMT);
+  return rows_gemm(r, dt, (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive_bits,
+                           int32_t* sel, float* sel_score, void* ws, size_t ws_bytes,
+                           dmoe_stream_t stream) {
+  int64_t E = 0;
+  DMOE_TRY(check_grid(&g, &E));
+  DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
+  NN(alive_bits); NN(ws);
+  if (T > 0) { NN(G); NN(sel); NN(sel_score); }
+  DMOE_REQUIRE(ws_bytes >= prefix_words(g.d, g.M) * 4, DMOE_ERR_ARG, "beam_topk: workspace too small");
+  return beam_topk(G, T, g, alive_bits, sel, sel_score, (uint32_t*)ws, (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, dmoe_grid g,
+                          const int32_t* sel, const float* sel_score,
+                          const uint32_t* responded_bits, float* w, uint8_t* valid,
+                          int32_t* n_dropped, int32_t* counts, int32_t* offsets,
+                          int32_t* row_of_slot, int32_t* token_of_row, void* xd, void* ws,
+                          size_t ws_bytes, dmoe_stream_t stream) {
+  int64_t E = 0;
+  DMOE_TRY(check_grid(&g, &E));
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
+  NN(responded_bits); NN(n_dropped); NN(counts); NN(offsets); NN(ws);
+  if (T > 0) { NN(x); NN(sel); NN(sel_score); NN(w); NN(valid); NN(row_of_slot); NN(token_of_row); NN(xd); }
+  return dispatch(x, dt, T, D, E, g.k, sel, sel_score, responded_bits, w, valid, n_dropped, counts,
+                  offsets, row_of_slot, token_of_row, xd, nullptr, nullptr, ws, ws_bytes,
+                  (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t E_local,
+                                int64_t R_cap, int32_t D, int32_t H, dmoe_dtype dt,
+                                const void* W1, const float* b1, const void* W2, const float* b2,
+                                void* h, void* out, void* ws, size_t ws_bytes,
+                                dmoe_stream_t stream) {
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_TRY(check_dt(dt, H));
+  DMOE_REQUIRE(E_local >= 1 && R_cap >= 0, DMOE_ERR_SHAPE, "E_local=%d R_cap=%lld", E_local, (long long)R_cap);
+  NN(offsets); NN(W1); NN(b1); NN(W2); NN(b2); NN(ws);
+  if (R_cap > 0) { NN(xd); NN(h); NN(out); }
+  cudaStream_t s = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  int32_t* plan_tc = cv.take<int32_t>(E_local + 1);
+  int32_t* plan_simt = cv.take<int32_t>(E_local + 1);
+  DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "expert_ffn_fwd: workspace too small");
+  GemmRows g1{};
+  g1.A = xd; g1.B = W1; g1.C = h; g1.bias = b1; g1.offsets = offsets;
+  g1.E = E_local; g1.N = H; g1.K = D; g1.b_mn = false; g1.epi = EPI_BIAS_RELU;
+  GemmRows g2 = g1;
+  g2.A = h; g2.B = W2; g2.C = out; g2.bias = b2; g2.N = D; g2.K = H; g2.epi = EPI_BIAS;
+  for (GemmRows* g : {&g1, &g2}) {
+    const bool tc = dt == DMOE_BF16 && tc_rows_supported(*g);
+    const int bm = tc ? kPlanBM_TC : kPlanBM_SIMT;
+    g->plan = tc ? plan_tc : plan_simt;
+    g->max_tiles = ceil_div(R_cap, bm) + E_local;
+  }
+  DMOE_TRY(tile_plan(offsets, E_local, kPlanBM_TC, plan_tc, s));
+  DMOE_TRY(tile_plan(offsets, E_local, kPlanBM_SIMT, plan_simt, s));
+  DMOE_TRY(rows_gemm(g1, dt, s));
+  return rows_gemm(g2, dt, s);
+}
+
+dmoe_status dmoe_combine(const void* out, const int32_t* row_of_slot, const float* w,
+                         const uint8_t* valid, int64_t T, int32_t D, int32_t k, dmoe_dtype dt,
+                         void* y, dmoe_stream_t stream) {
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
+  if (T > 0) { NN(row_of_slot); NN(w); NN(valid); NN(y); }
+  return combine(out, row_of_slot, w, valid, T, D, k, dt, y, (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
+                             const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt,
+                             void* dout, float* dscore, dmoe_stream_t stream) {
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
+  if (T > 0) { NN(dy); NN(row_of_slot); NN(w); NN(dscore); }
+  return combine_bwd(dy, out, row_of_slot, w, T, D, k, dt, dout, dscore, (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
+                                const int32_t* offsets, int32_t E_local, int64_t R_cap,
+                                int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
+                                const void* W2, void* dxd, void* dW1, float* db1, void* dW2,
+                                float* db2, void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_TRY(check_dt(dt, H));
+  DMOE_REQUIRE(E_local >= 1 && R_cap >= 0, DMOE_ERR_SHAPE, "E_local=%d R_cap=%lld", E_local, (long long)R_cap);
+  NN(offsets); NN(W1); NN(W2); NN(dW1); NN(db1); NN(dW2); NN(db2); NN(ws);
+  if (R_cap > 0) { NN(xd); NN(h); NN(dout); NN(dxd); }
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t esz = dt == DMOE_BF16 ? 2 : 4;
+  Carver cv(ws, ws_bytes);
+  int32_t* plan_tc = cv.take<int32_t>(E_local + 1);
+  int32_t* plan_simt = cv.take<int32_t>(E_local + 1);
+  void* dh = cv.take<char>((size_t)(R_cap > 0 ? R_cap : 1) * H * esz);
+  DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "expert_ffn_bwd: workspace too small (%zu < %zu)", ws_bytes, cv.used);
+  // dh = (dout W2_e) * 1[h > 0];  dxd = dh W1_e
+  GemmRows g3{};
+  g3.A = dout; g3.B = W2; g3.C = dh; g3.aux = h; g3.offsets = offsets;
+  g3.E = E_local; g3.N = H; g3.K = D; g3.b_mn = true; g3.epi = EPI_RELU_MASK;
+  GemmRows g4 = g3;
+  g4.A = dh; g4.B = W1; g4.C = dxd; g4.aux = nullptr; g4.N = D; g4.K = H; g4.epi = EPI_PLAIN;
+  for (GemmRows* g : {&g3, &g4}) {
+    const bool tc = dt == DMOE_BF16 && tc_rows_supported(*g);
+    const int bm = tc ? kPlanBM_TC : kPlanBM_SIMT;
+    g->plan = tc ? plan_tc : plan_simt;
+    g->max_tiles = ceil_div(R_cap, bm) + E_local;
+  }
+  DMOE_TRY(tile_plan(offsets, E_local, kPlanBM_TC, plan_tc, s));
+  DMOE_TRY(tile_plan(offsets, E_local, kPlanBM_SIMT, plan_simt, s));
+  DMOE_TRY(rows_gemm(g3, dt, s));
+  DMOE_TRY(rows_gemm(g4, dt, s));
+  // dW2_e = dout^T h;  dW1_e = dh^T xd;  db2 / db1 = segment column sums
+  GemmSegK g5{dout, h, dW2, offsets, E_local, D, H};
+  GemmSegK g6{dh, xd, dW1, offsets, E_local, H, D};
+  DMOE_TRY(segk_gemm(g5, dt, s));
+  DMOE_TRY(segk_gemm(g6, dt, s));
+  DMOE_TRY(seg_colsum(dout, dt, offsets, E_local, D, db2, s));
+  return seg_colsum(dh, dt, offsets, E_local, H, db1, s);
+}
+
+dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, const float* dscore,
+                          const void* dxd, const int32_t* row_of_slot, int64_t T, int32_t D,
+                          dmoe_grid g, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
+                          size_t ws_bytes, dmoe_stream_t stream) {
+  int64_t E = 0;
+  DMOE_TRY(check_grid(&g, &E));
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
+  NN(Wg); NN(dWg); NN(dbg); NN(ws);
+  if (T > 0) { NN(x); NN(sel); NN(dscore); NN(row_of_slot); NN(dx); }
+  return gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, T, D, g.d, g.M, g.k, dt, dx, dWg, dbg, ws,
+                  ws_bytes, (cudaStream_t)stream);
+}
+
+}  // extern "C"

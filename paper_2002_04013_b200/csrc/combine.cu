@@ -1,0 +1,123 @@
+// combine.cu — S7 combine (Eq. 3 weighted average) and S8 combine backward.
+//
+// One warp per token; rows are read and written as 16-byte vectors (8 bf16 / 4 fp32
+// per lane), accumulation in fp32.  Eq. 3; backward = softmax
+// Jacobian over the ok slots (S8).
+#include "common.cuh"
+
+namespace dmoe {
+
+constexpr int kCombWarps = 8;
+constexpr int kMaxK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(kCombWarps * 32)
+k_combine(const T* __restrict__ out, const int32_t* __restrict__ row_of_slot,
+          const float* __restrict__ w, const uint8_t* __restrict__ valid, int64_t Tn, int32_t D,
+          int k, T* __restrict__ y) {
+  constexpr int V = Vec16<T>::N;
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = blockIdx.x * (int64_t)kCombWarps + (threadIdx.x >> 5); t < Tn;
+       t += (int64_t)gridDim.x * kCombWarps) {
+    int32_t rows[kMaxK];
+    float ws[kMaxK];
+    for (int s = 0; s < k; ++s) {
+      rows[s] = row_of_slot[t * k + s];
+      ws[s] = w[t * k + s];
+    }
+    const bool ok_tok = valid[t] != 0;
+    for (int c = lane * V; c < D; c += 32 * V) {
+      float acc[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] = 0.0f;
+      if (ok_tok) {
+        for (int s = 0; s < k; ++s) {
+          if (rows[s] < 0) continue;
+          float f[V];
+          unpack16(ld_nc_v4(out + (int64_t)rows[s] * D + c), f, (const T*)nullptr);
+#pragma unroll
+          for (int i = 0; i < V; ++i) acc[i] = fmaf(ws[s], f[i], acc[i]);
+        }
+      }
+      st_v4(y + t * D + c, pack16(acc, (const T*)nullptr));
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCombWarps * 32)
+k_combine_bwd(const T* __restrict__ dy, const T* __restrict__ out,
+              const int32_t* __restrict__ row_of_slot, const float* __restrict__ w, int64_t Tn,
+              int32_t D, int k, T* __restrict__ dout, float* __restrict__ dscore) {
+  constexpr int V = Vec16<T>::N;
+  const int lane = threadIdx.x & 31;
+  for (int64_t t = blockIdx.x * (int64_t)kCombWarps + (threadIdx.x >> 5); t < Tn;
+       t += (int64_t)gridDim.x * kCombWarps) {
+    int32_t rows[kMaxK];
+    float ws[kMaxK], a[kMaxK];
+    for (int s = 0; s < k; ++s) {
+      rows[s] = row_of_slot[t * k + s];
+      ws[s] = w[t * k + s];
+      a[s] = 0.0f;
+    }
+    // a_s = <dy_t, out_row>, and dout_row = w_s dy_t in the same pass over dy_t
+    for (int c = lane * V; c < D; c += 32 * V) {
+      float g[V];
+      unpack16(ld_nc_v4(dy + t * D + c), g, (const T*)nullptr);
+      for (int s = 0; s < k; ++s) {
+        if (rows[s] < 0) continue;
+        float f[V], o[V];
+        unpack16(ld_nc_v4(out + (int64_t)rows[s] * D + c), f, (const T*)nullptr);
+        float p = 0.0f;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          p = fmaf(g[i], f[i], p);
+          o[i] = ws[s] * g[i];
+        }
+        a[s] += p;
+        st_v4(dout + (int64_t)rows[s] * D + c, pack16(o, (const T*)nullptr));
+      }
+    }
+    float abar = 0.0f;
+    for (int s = 0; s < k; ++s) {
+      a[s] = warp_sum(a[s]);
+      if (rows[s] >= 0) abar = fmaf(ws[s], a[s], abar);
+    }
+    if (lane < k) dscore[t * k + lane] = rows[lane] >= 0 ? ws[lane] * (a[lane] - abar) : 0.0f;
+  }
+}
+
+static unsigned grid_tokens(int64_t T) {
+  int64_t b = ceil_div(T, kCombWarps);
+  int64_t cap = (int64_t)num_sms() * 16;
+  return (unsigned)(b < cap ? (b > 0 ? b : 1) : cap);
+}
+
+dmoe_status combine(const void* out, const int32_t* row_of_slot, const float* w,
+                    const uint8_t* valid, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* y,
+                    cudaStream_t s) {
+  if (T == 0) return DMOE_OK;
+  if (dt == DMOE_BF16)
+    k_combine<__nv_bfloat16><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(
+        (const __nv_bfloat16*)out, row_of_slot, w, valid, T, D, k, (__nv_bfloat16*)y);
+  else
+    k_combine<float><<<grid_tokens(T), kCombWarps * 32, 0, s>>>((const float*)out, row_of_slot, w,
+                                                                valid, T, D, k, (float*)y);
+  return check_launch("combine");
+}
+
+dmoe_status combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
+                        const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout,
+                        float* dscore, cudaStream_t s) {
+  if (T == 0) return DMOE_OK;
+  if (dt == DMOE_BF16)
+    k_combine_bwd<__nv_bfloat16><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(
+        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)out, row_of_slot, w, T, D, k,
+        (__nv_bfloat16*)dout, dscore);
+  else
+    k_combine_bwd<float><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(
+        (const float*)dy, (const float*)out, row_of_slot, w, T, D, k, (float*)dout, dscore);
+  return check_launch("combine_bwd");
+}
+
+}  // namespace dmoe

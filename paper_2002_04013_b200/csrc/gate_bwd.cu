@@ -1,0 +1,219 @@
+// gate_bwd.cu — S10: undispatch (sum the expert-path input gradients back per token)
+// and the gating gradient of Eq. 2 through the Eq. 3 softmax.
+//
+//   dG[t, i*M + u_i(sel_ts)] += dscore_ts            (sparse: <= k*d non-zeros per row)
+//   dX_t  = sum_{ok s} dXd[row_ts] + sum_s dscore_ts sum_i W_g[:, i*M + u_i(sel_ts)]
+//   dW_g  = X^T dG (fp32),  db_g = column sums of dG (fp32)
+//
+// W_g is transposed once into the workspace so the k*d gate columns a token touches are
+// contiguous rows (coalesced, L2-resident).  dW_g is a split-K SIMT reduction over
+// tokens with a fixed-order final sum (deterministic, no float atomics).
+#include "common.cuh"
+
+namespace dmoe {
+
+template <typename T>
+__global__ void k_transpose(const T* __restrict__ src, int64_t rows, int64_t cols,
+                            T* __restrict__ dst) {
+  __shared__ float tile[32][33];
+  const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = Elem<T>::load(src + r * cols + c);
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) Elem<T>::store(dst + c * rows + r, tile[threadIdx.x][i]);
+  }
+}
+
+constexpr int kGbWarps = 8;
+constexpr int kGbMaxK = 16;
+
+template <typename T>
+__global__ void __launch_bounds__(kGbWarps * 32)
+k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
+              const float* __restrict__ dscore, const T* __restrict__ dxd,
+              const int32_t* __restrict__ row_of_slot, int64_t Tn, int32_t D, int d, int M, int k,
+              T* __restrict__ dx, float* __restrict__ dG) {
+  constexpr int V = Vec16<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int dM = d * M;
+  for (int64_t t = blockIdx.x * (int64_t)kGbWarps + (threadIdx.x >> 5); t < Tn;
+       t += (int64_t)gridDim.x * kGbWarps) {
+    int32_t rows[kGbMaxK], es[kGbMaxK];
+    float ds[kGbMaxK];
+    for (int s = 0; s < k; ++s) {
+      rows[s] = row_of_slot[t * k + s];
+      es[s] = sel[t * k + s];
+      ds[s] = dscore[t * k + s];
+    }
+    // dense dG row (fp32) for dW_g / db_g
+    for (int col = lane; col < dM; col += 32) {
+      const int i = col / M, j = col - i * M;
+      int div = 1;
+      for (int q = i + 1; q < d; ++q) div *= M;
+      float v = 0.0f;
+      for (int s = 0; s < k; ++s)
+        if (es[s] >= 0 && (es[s] / div) % M == j) v += ds[s];
+      dG[t * dM + col] = v;
+    }
+    for (int c = lane * V; c < D; c += 32 * V) {
+      float acc[V];
+#pragma unroll
+      for (int q = 0; q < V; ++q) acc[q] = 0.0f;
+      for (int s = 0; s < k; ++s) {
+        if (rows[s] >= 0) {
+          float f[V];
+          unpack16(ld_nc_v4(dxd + (int64_t)rows[s] * D + c), f, (const T*)nullptr);
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] += f[q];
+        }
+      }
+      for (int s = 0; s < k; ++s) {
+        if (es[s] < 0 || ds[s] == 0.0f) continue;
+        int e = es[s];
+        for (int i = d - 1; i >= 0; --i) {
+          const int col = i * M + (e % M);
+          e /= M;
+          float f[V];
+          unpack16(ld_v4(WgT + (int64_t)col * D + c), f, (const T*)nullptr);
+#pragma unroll
+          for (int q = 0; q < V; ++q) acc[q] = fmaf(ds[s], f[q], acc[q]);
+        }
+      }
+      st_v4(dx + t * D + c, pack16(acc, (const T*)nullptr));
+    }
+  }
+}
+
+// partial[split][c][col] = sum_{t in split} X[t][c] dG[t][col]; pb[split][col] = sum dG[t][col]
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn, int32_t D, int dM,
+              int64_t tok_per_split, float* __restrict__ partial, float* __restrict__ pb) {
+  __shared__ float xs[32][65];
+  __shared__ float gs[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
+  const int c0 = blockIdx.x * 64, col0 = blockIdx.y * 32;
+  const int64_t split = blockIdx.z;
+  const int64_t t_begin = split * tok_per_split;
+  int64_t t_end = t_begin + tok_per_split;
+  if (t_end > Tn) t_end = Tn;
+  float acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+  float bsum = 0.0f;
+  for (int64_t tb = t_begin; tb < t_end; tb += 32) {
+    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
+      int r = i / 64, c = i % 64;
+      int64_t t = tb + r;
+      xs[r][c] = (t < t_end && c0 + c < D) ? Elem<T>::load(X + t * D + c0 + c) : 0.0f;
+    }
+    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
+      int r = i / 32, c = i % 32;
+      int64_t t = tb + r;
+      gs[r][c] = (t < t_end && col0 + c < dM) ? dG[t * dM + col0 + c] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const float g = gs[r][tx];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = fmaf(xs[r][ty * 8 + q], g, acc[q]);
+      if (ty == 0) bsum += g;
+    }
+    __syncthreads();
+  }
+  const int col = col0 + tx;
+  if (col < dM) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = c0 + ty * 8 + q;
+      if (c < D) partial[(split * D + c) * dM + col] = acc[q];
+    }
+    if (blockIdx.x == 0 && ty == 0) pb[split * dM + col] = bsum;
+  }
+}
+
+__global__ void k_dwg_reduce(const float* __restrict__ partial, const float* __restrict__ pb,
+                             int64_t nsplit, int32_t D, int dM, float* __restrict__ dWg,
+                             float* __restrict__ dbg) {
+  const int64_t n = (int64_t)D * dM;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n + dM;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v = 0.0f;
+    if (i < n) {
+      for (int64_t s = 0; s < nsplit; ++s) v += partial[s * n + i];
+      dWg[i] = v;
+    } else {
+      const int64_t col = i - n;
+      for (int64_t s = 0; s < nsplit; ++s) v += pb[s * dM + col];
+      dbg[col] = v;
+    }
+  }
+}
+
+constexpr int64_t kMaxSplits = 2 * kNumSMs;
+
+static int64_t dwg_splits(int64_t T, int32_t D, int dM) {
+  const int64_t tiles = ceil_div(D, 64) * ceil_div(dM, 32);
+  int64_t s = ceil_div(kMaxSplits, tiles);
+  const int64_t maxs = ceil_div(T, 256);
+  if (s > maxs) s = maxs;
+  return s < 1 ? 1 : s;
+}
+
+size_t gate_bwd_ws_bytes(int64_t T, int32_t D, int dM) {
+  int64_t S = ceil_div(T, 256);
+  if (S > kMaxSplits) S = kMaxSplits;
+  if (S < 1) S = 1;
+  return align_up((size_t)D * dM * 4, 256) + align_up((size_t)(T > 0 ? T : 1) * dM * 4, 256) +
+         align_up((size_t)S * D * dM * 4, 256) + align_up((size_t)S * dM * 4, 256) + 1024;
+}
+
+dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const float* dscore,
+                     const void* dxd, const int32_t* row_of_slot, int64_t T, int32_t D, int d, int M,
+                     int k, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
+                     size_t ws_bytes, cudaStream_t s) {
+  const int dM = d * M;
+  const int64_t S = dwg_splits(T, D, dM);
+  const size_t esz = dt == DMOE_BF16 ? 2 : 4;
+  Carver cv(ws, ws_bytes);
+  void* WgT = cv.take<char>((size_t)D * dM * esz);
+  float* dG = cv.take<float>((size_t)(T > 0 ? T : 1) * dM);
+  float* part = cv.take<float>((size_t)S * D * dM);
+  float* pb = cv.take<float>((size_t)S * dM);
+  DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "gate_bwd: workspace too small (%zu < %zu)", ws_bytes, cv.used);
+  dim3 tb(32, 8), tg((unsigned)ceil_div(dM, 32), (unsigned)ceil_div(D, 32));
+  if (dt == DMOE_BF16)
+    k_transpose<__nv_bfloat16><<<tg, tb, 0, s>>>((const __nv_bfloat16*)Wg, D, dM, (__nv_bfloat16*)WgT);
+  else
+    k_transpose<float><<<tg, tb, 0, s>>>((const float*)Wg, D, dM, (float*)WgT);
+  DMOE_TRY(check_launch("gate_bwd.transpose"));
+  if (T > 0) {
+    int64_t b = ceil_div(T, kGbWarps), cap = (int64_t)num_sms() * 16;
+    unsigned grid = (unsigned)(b < cap ? b : cap);
+    if (dt == DMOE_BF16)
+      k_gate_bwd_dx<__nv_bfloat16><<<grid, kGbWarps * 32, 0, s>>>(
+          (const __nv_bfloat16*)WgT, sel, dscore, (const __nv_bfloat16*)dxd, row_of_slot, T, D, d, M,
+          k, (__nv_bfloat16*)dx, dG);
+    else
+      k_gate_bwd_dx<float><<<grid, kGbWarps * 32, 0, s>>>((const float*)WgT, sel, dscore,
+                                                          (const float*)dxd, row_of_slot, T, D, d,
+                                                          M, k, (float*)dx, dG);
+    DMOE_TRY(check_launch("gate_bwd.dx"));
+  }
+  const int64_t tps = T > 0 ? ceil_div(T, S) : 1;
+  dim3 pg((unsigned)ceil_div(D, 64), (unsigned)ceil_div(dM, 32), (unsigned)S);
+  if (dt == DMOE_BF16)
+    k_dwg_partial<__nv_bfloat16><<<pg, 256, 0, s>>>((const __nv_bfloat16*)x, dG, T, D, dM, tps, part, pb);
+  else
+    k_dwg_partial<float><<<pg, 256, 0, s>>>((const float*)x, dG, T, D, dM, tps, part, pb);
+  DMOE_TRY(check_launch("gate_bwd.dwg_partial"));
+  k_dwg_reduce<<<(unsigned)ceil_div((int64_t)D * dM + dM, 256), 256, 0, s>>>(part, pb, S, D, dM, dWg, dbg);
+  return check_launch("gate_bwd.dwg_reduce");
+}
+
+}  // namespace dmoe

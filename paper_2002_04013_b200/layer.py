@@ -1,0 +1,92 @@
+"""DMoELayer: one Decentralized Mixture-of-Experts layer on one B200, driven through the C ABI.
+
+The forward pass is the paper's DMoE inference procedure (§3.1) with the
+structured gate of §3.2: gate scores (Eq. 2) -> SelectExperts (Alg. 1) -> renormalised Eq. 3
+weights + dispatch -> expert Forward (runtime, §3.3) -> weighted average (Eq. 3).  The
+backward pass is the runtime's Backward request plus the gating gradient.
+
+All buffers are allocated once for T_max tokens, so a step allocates nothing and can be
+captured in a CUDA graph.  Python only marshals arguments; every step runs in libdmoe.so.
+"""
+import torch
+
+from . import _lib as L
+
+
+class DMoELayer:
+    def __init__(self, d, M, k, D, H, dtype=torch.bfloat16, beam=0, T_max=4096, device="cuda",
+                 E_local=None, R_cap=None):
+        self.d, self.M, self.k, self.D, self.H = d, M, k, D, H
+        self.beam = beam or k
+        self.E = M ** d
+        self.E_local = E_local or self.E
+        self.dtype = dtype
+        self.T_max = T_max
+        self.R_cap = R_cap if R_cap is not None else T_max * k
+        self.g = L.grid(d, M, k, self.beam)
+        dev = torch.device(device)
+        f32 = torch.float32
+        dM = d * M
+        E, El = self.E, self.E_local
+        e = lambda *s, dt=dtype: torch.empty(*s, dtype=dt, device=dev)
+        # parameters (filled by the caller / generator)
+        self.Wg, self.bg = e(D, dM), e(dM, dt=f32)
+        self.W1, self.b1 = e(El, H, D), e(El, H, dt=f32)
+        self.W2, self.b2 = e(El, D, H), e(El, D, dt=f32)
+        # gradients
+        self.dWg, self.dbg = e(D, dM, dt=f32), e(dM, dt=f32)
+        self.dW1, self.db1 = e(El, H, D), e(El, H, dt=f32)
+        self.dW2, self.db2 = e(El, D, H), e(El, D, dt=f32)
+        # activations / routing records (forward) and backward buffers
+        T, R = T_max, self.R_cap
+        self.G = e(T, dM, dt=f32)
+        self.sel = e(T, k, dt=torch.int32)
+        self.sel_score = e(T, k, dt=f32)
+        self.w = e(T, k, dt=f32)
+        self.valid = e(T, dt=torch.uint8)
+        self.n_dropped = e(1, dt=torch.int32)
+        self.counts = e(E, dt=torch.int32)
+        self.offsets = e(E + 1, dt=torch.int32)
+        self.row_of_slot = e(T, k, dt=torch.int32)
+        self.token_of_row = e(max(T * k, 1), dt=torch.int32)
+        self.xd = e(max(R, 1), D)
+        self.h = e(max(R, 1), H)
+        self.out = e(max(R, 1), D)
+        self.y = e(T, D)
+        self.dout = e(max(R, 1), D)
+        self.dscore = e(T, k, dt=f32)
+        self.dxd = e(max(R, 1), D)
+        self.dx = e(T, D)
+        ws = L.dmoe_workspace_bytes(T, D, H, self.g, El, R)
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=dev)
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, x, alive_bits, responded_bits):
+        T = x.shape[0]
+        assert T <= self.T_max and x.dtype == self.dtype and x.shape[1] == self.D
+        self._x = x
+        L.dmoe_gate_scores(x, self.Wg, self.bg, self.g, self.G[:T])
+        L.dmoe_beam_topk(self.G[:T], self.g, alive_bits, self.sel[:T], self.sel_score[:T], self.ws)
+        L.dmoe_dispatch(x, self.g, self.sel[:T], self.sel_score[:T], responded_bits, self.w[:T], self.valid[:T],
+                        self.n_dropped, self.counts, self.offsets, self.row_of_slot[:T], self.token_of_row,
+                        self.xd, self.ws)
+        L.dmoe_expert_ffn_fwd(self.xd, self.offsets, self.W1, self.b1, self.W2, self.b2, self.h, self.out,
+                              self.ws)
+        L.dmoe_combine(self.out, self.row_of_slot[:T], self.w[:T], self.valid[:T], self.y[:T])
+        return self.y[:T]
+
+    # ----------------------------------------------------------------- backward
+    def backward(self, dy):
+        x = self._x
+        T = x.shape[0]
+        L.dmoe_combine_bwd(dy, self.out, self.row_of_slot[:T], self.w[:T], self.dout, self.dscore[:T])
+        L.dmoe_expert_ffn_bwd(self.xd, self.h, self.dout, self.offsets, self.W1, self.W2, self.dxd,
+                              self.dW1, self.db1, self.dW2, self.db2, self.ws)
+        L.dmoe_gate_bwd(x, self.Wg, self.sel[:T], self.dscore[:T], self.dxd, self.row_of_slot[:T], self.g,
+                        self.dx[:T], self.dWg, self.dbg, self.ws)
+        return self.dx[:T]
+
+    def step(self, x, dy, alive_bits, responded_bits):
+        """One layer step: forward + backward (the unit bench.py times)."""
+        self.forward(x, alive_bits, responded_bits)
+        return self.backward(dy)

@@ -1,0 +1,125 @@
+"""Shared test helpers: seeded inputs (gen/), the CUDA path through the C ABI, the oracle.
+
+Inputs come from the counter-based generator only; expected values only from oracle/.
+"""
+import numpy as np
+
+import gen
+from gen import CONFIGS  # noqa: F401
+
+TOL = {"bf16": 2e-2, "f32": 1e-4}   # north_star: max-abs error relative to max |oracle|
+GAP = 1e-3                          # north_star: routing compared where the oracle gap > 1e-3
+
+
+def make_inputs(cfg, seed=0, T=None, experts=None):
+    """Host arrays for one step of `cfg`.  Returns dict: for every tensor both the device form
+    (`dev_*`: uint16 bf16 bits or float32) and the exact float64 upcast the oracle sees."""
+    T = cfg.T if T is None else T
+    E, D, H, dM = cfg.E, cfg.D, cfg.H, cfg.dM
+    bf = cfg.dtype == "bf16"
+    out = {}
+
+    def param(name, tid, n, idx0=0, force_f32=False):
+        dist, scale = cfg.dist(tid)
+        if bf and not force_f32:
+            bits = gen.host_bf16_bits(seed, tid, dist, scale, n, idx0)
+            out["dev_" + name] = bits
+            return gen.bf16_bits_to_f64(bits)
+        v = gen.host_f32(seed, tid, dist, scale, n, idx0)
+        out["dev_" + name] = v
+        return v.astype(np.float64)
+
+    out["X"] = param("X", gen.X, T * D).reshape(T, D)
+    out["Wg"] = param("Wg", gen.WG, D * dM).reshape(D, dM)
+    out["bg"] = param("bg", gen.BG, dM, force_f32=True)
+    ex = range(E) if experts is None else experts
+    W1, b1, W2, b2 = [], [], [], []
+    dev = {k: [] for k in ("W1", "b1", "W2", "b2")}
+    for e in ex:
+        W1.append(param("_w1", gen.W1, H * D, e * H * D).reshape(H, D)); dev["W1"].append(out.pop("dev__w1"))
+        b1.append(param("_b1", gen.B1, H, e * H, force_f32=True)); dev["b1"].append(out.pop("dev__b1"))
+        W2.append(param("_w2", gen.W2, D * H, e * D * H).reshape(D, H)); dev["W2"].append(out.pop("dev__w2"))
+        b2.append(param("_b2", gen.B2, D, e * D, force_f32=True)); dev["b2"].append(out.pop("dev__b2"))
+    out["W1"], out["b1"], out["W2"], out["b2"] = (np.stack(v) for v in (W1, b1, W2, b2))
+    for k_, v in dev.items():
+        out["dev_" + k_] = np.concatenate(v)
+    out["dY"] = param("dY", gen.DY, T * D).reshape(T, D)
+    out["alive_bits"] = gen.host_mask(seed, gen.ALIVE, cfg.dead_frac, E)
+    out["responded_bits"] = gen.host_mask(seed, gen.RESPONDED, cfg.fail_frac, E)
+    out["alive"] = gen.unpack_mask(out["alive_bits"], E)
+    out["responded"] = gen.unpack_mask(out["responded_bits"], E)
+    return out
+
+
+def to_torch(arr, dtype, shape=None):
+    import torch
+    arr = np.ascontiguousarray(arr)
+    if dtype == "bf16":
+        t = torch.from_numpy(arr.view(np.int16)).view(torch.bfloat16)
+    else:
+        t = torch.from_numpy(arr)
+    t = t.cuda()
+    return t.reshape(shape) if shape is not None else t
+
+
+def gpu_layer(cfg, inp, T=None):
+    """Run one forward+backward through the C ABI; returns the DMoELayer (buffers hold everything)."""
+    import torch
+    from paper_2002_04013_b200 import DMoELayer
+    T = inp["X"].shape[0] if T is None else T
+    dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    lay = DMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=max(T, 1))
+    E, D, H, dM = cfg.E, cfg.D, cfg.H, cfg.dM
+    lay.Wg.copy_(to_torch(inp["dev_Wg"], cfg.dtype, (D, dM)))
+    lay.bg.copy_(torch.from_numpy(inp["dev_bg"]).cuda())
+    lay.W1.copy_(to_torch(inp["dev_W1"], cfg.dtype, (E, H, D)))
+    lay.b1.copy_(torch.from_numpy(inp["dev_b1"]).cuda().reshape(E, H))
+    lay.W2.copy_(to_torch(inp["dev_W2"], cfg.dtype, (E, D, H)))
+    lay.b2.copy_(torch.from_numpy(inp["dev_b2"]).cuda().reshape(E, D))
+    x = to_torch(inp["dev_X"], cfg.dtype, (T, D))
+    dy = to_torch(inp["dev_dY"], cfg.dtype, (T, D))
+    alive = torch.from_numpy(inp["alive_bits"].view(np.int32)).cuda()
+    resp = torch.from_numpy(inp["responded_bits"].view(np.int32)).cuda()
+    lay._inputs = (x, dy, alive, resp)
+    lay.step(x, dy, alive, resp)
+    torch.cuda.synchronize()
+    return lay
+
+
+def np64(t):
+    import torch
+    return t.detach().to(torch.float64).cpu().numpy() if t.dtype != torch.int32 else t.cpu().numpy()
+
+
+def rel_err(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    den = np.abs(want).max() if want.size else 0.0
+    num = np.abs(got - want).max() if want.size else 0.0
+    return num / den if den > 0 else num
+
+
+def oracle_step(cfg, inp, sel_override=None):
+    from oracle import oracle as O
+    return O.layer_step(inp["X"], inp["Wg"], inp["bg"], inp["W1"], inp["b1"], inp["W2"], inp["b2"],
+                        inp["dY"], inp["alive"], inp["responded"], cfg.d, cfg.M, cfg.k, cfg.B,
+                        sel_override=sel_override)
+
+
+def check_routing(cfg, gsel, ref, exact, alive):
+    """sel must equal the oracle's on every token (exact-grid) or where gap > GAP (continuous);
+    elsewhere the GPU's choice must be a valid alternative: alive experts whose oracle Eq. 2
+    scores are within GAP of the oracle's slot scores.  Returns the #tokens compared."""
+    from oracle import oracle as O
+    osel, gap = ref["sel"], ref["gap"]
+    mask = np.ones(len(gap), bool) if exact else gap > GAP
+    bad = np.nonzero((gsel != osel).any(1) & mask)[0]
+    assert len(bad) == 0, f"routing mismatch on tokens {bad[:10]}: gpu {gsel[bad[:3]]} oracle {osel[bad[:3]]}"
+    rest = np.nonzero(~mask & (gsel != osel).any(1))[0]
+    if len(rest):
+        s_gpu = O._scores_of(ref["G"][rest], gsel[rest], cfg.d, cfg.M)
+        assert np.all(np.abs(np.where(gsel[rest] >= 0, s_gpu, 0) - np.where(osel[rest] >= 0, ref["sel_score"][rest], 0)) <= 2 * GAP)
+        chosen = gsel[rest][gsel[rest] >= 0]
+        assert np.all(alive[chosen] == 1)
+        assert ((gsel[rest] >= 0).sum(1) == (osel[rest] >= 0).sum(1)).all()
+    return int(mask.sum())

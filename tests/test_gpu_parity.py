@@ -1,0 +1,109 @@
+"""GPU-vs-oracle parity through the C ABI (north_star bars: routing and dispatch permutations
+bit-exact; values within 2e-2 (bf16) / 1e-4 (fp32) max-abs error relative to max |oracle|)."""
+import numpy as np
+import pytest
+
+import gen
+from harness import CONFIGS, TOL, check_routing, gpu_layer, make_inputs, np64, oracle_step, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _compare_layer(cfg, inp, lay, exact=False):
+    T = inp["X"].shape[0]
+    ref = oracle_step(cfg, inp)
+    gsel = np64(lay.sel[:T])
+    ntok = check_routing(cfg, gsel, ref, exact, inp["alive"])
+    # values and permutations with forced routing: the oracle downstream of S3 uses the GPU's sel
+    r = oracle_step(cfg, inp, sel_override=gsel)
+    E = cfg.E
+    assert np.array_equal(np64(lay.counts), r["counts"])
+    assert np.array_equal(np64(lay.offsets), r["offsets"])
+    assert np.array_equal(np64(lay.row_of_slot[:T]), r["row_of_slot"])
+    R = int(r["offsets"][E])
+    assert np.array_equal(np64(lay.token_of_row[:R]), r["token_of_row"])
+    assert int(lay.n_dropped.item()) == r["n_dropped"]
+    assert np.array_equal(np64(lay.valid[:T]), r["valid"])
+    assert np.array_equal(np64(lay.xd[:R]), inp["X"][r["token_of_row"]])      # gather is a copy
+    tol = TOL[cfg.dtype]
+    errs = {
+        "w": rel_err(np64(lay.w[:T]), r["w"]),
+        "y": rel_err(np64(lay.y[:T]), r["y"]),
+        "h": rel_err(np64(lay.h[:R]), r["a"]),
+        "out": rel_err(np64(lay.out[:R]), r["out"]),
+        "dscore": rel_err(np64(lay.dscore[:T]), r["dscore"]),
+        "dX": rel_err(np64(lay.dx[:T]), r["dX"]),
+        "dWg": rel_err(np64(lay.dWg), r["dWg"]),
+        "dbg": rel_err(np64(lay.dbg), r["dbg"]),
+        "dW1": rel_err(np64(lay.dW1), r["dW1"]),
+        "db1": rel_err(np64(lay.db1), r["db1"]),
+        "dW2": rel_err(np64(lay.dW2), r["dW2"]),
+        "db2": rel_err(np64(lay.db2), r["db2"]),
+    }
+    bad = {k: v for k, v in errs.items() if not v <= tol}
+    assert not bad, f"tolerance {tol} exceeded: {bad} (all: {errs})"
+    return ntok, errs
+
+
+def test_tiny_fp32():
+    cfg = CONFIGS["tiny"]
+    inp = make_inputs(cfg, seed=1)
+    _compare_layer(cfg, inp, gpu_layer(cfg, inp))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_tiny_fp32_exact_grid(seed):
+    cfg = CONFIGS["tiny"].with_(exact_grid=True)
+    inp = make_inputs(cfg, seed=seed)
+    lay = gpu_layer(cfg, inp)
+    ref = oracle_step(cfg, inp)
+    assert np.array_equal(np64(lay.G[:cfg.T]), ref["G"])          # fp32 G exact in this mode
+    _compare_layer(cfg, inp, lay, exact=True)
+
+
+@pytest.mark.parametrize("T", [1, 333, 1024])
+def test_mnist_shape_bf16(T):
+    cfg = CONFIGS["mnist"]
+    inp = make_inputs(cfg, seed=2, T=T)
+    _compare_layer(cfg, inp, gpu_layer(cfg, inp))
+
+
+def test_mnist_shape_bf16_exact_grid_with_masks():
+    cfg = CONFIGS["mnist"].with_(exact_grid=True, dead_frac=0.3, fail_frac=0.3, beam=6)
+    inp = make_inputs(cfg, seed=3, T=700)
+    lay = gpu_layer(cfg, inp)
+    ref = oracle_step(cfg, inp)
+    assert np.array_equal(np64(lay.G[:700]), ref["G"])
+    _compare_layer(cfg, inp, lay, exact=True)
+
+
+def test_grid3d_shape_small_exact():
+    cfg = CONFIGS["grid3d"].with_(D=128, H=256, exact_grid=True, dead_frac=0.2)
+    inp = make_inputs(cfg, seed=4, T=300)
+    _compare_layer(cfg, inp, gpu_layer(cfg, inp), exact=True)
+
+
+def test_all_experts_failed_drops_every_token():
+    cfg = CONFIGS["tiny"].with_(fail_frac=1.0)
+    inp = make_inputs(cfg, seed=5)
+    lay = gpu_layer(cfg, inp)
+    assert int(lay.n_dropped.item()) == cfg.T
+    for t in (lay.y, lay.dx, lay.dW1, lay.dW2, lay.db1, lay.db2, lay.dWg, lay.dbg):
+        assert (np64(t) == 0).all()
+
+
+def test_no_alive_expert_gives_empty_selection():
+    cfg = CONFIGS["tiny"].with_(dead_frac=1.0)
+    inp = make_inputs(cfg, seed=6)
+    lay = gpu_layer(cfg, inp)
+    assert (np64(lay.sel[:cfg.T]) == -1).all()
+    assert np.isneginf(np64(lay.sel_score[:cfg.T])).all()
+    assert int(lay.n_dropped.item()) == cfg.T
+
+
+def test_deterministic_rerun():
+    cfg = CONFIGS["mnist"]
+    inp = make_inputs(cfg, seed=7, T=512)
+    a, b = gpu_layer(cfg, inp), gpu_layer(cfg, inp)
+    for n in ("y", "dx", "dW1", "dW2", "db1", "db2", "dWg", "dbg", "row_of_slot"):
+        assert np.array_equal(np64(getattr(a, n)), np64(getattr(b, n))), n
