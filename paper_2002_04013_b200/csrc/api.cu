@@ -127,7 +127,7 @@ dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D,
   GemmRows r{};
   r.A = x; r.B = Wg; r.C = G; r.bias = bg; r.aux = nullptr;
   r.offsets = nullptr; r.plan = nullptr;
-  r.E = 1; r.N = g.d * g.M; r.K = D; r.rows_single = T;
+  r.E = 1; r.N = g.d * g.M; r.K = D; r.rows_single = T; r.rows_cap = T;
   r.b_mn = true; r.epi = EPI_F32_BIAS;
   const bool tc = dt == DMOE_BF16 && tc_rows_supported(r);
   r.max_tiles = ceil_div(T, tc ? kPlanBM_TC : kPlanBM_SIMT);
@@ -180,7 +180,7 @@ dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t 
   DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "expert_ffn_fwd: workspace too small");
   GemmRows g1{};
   g1.A = xd; g1.B = W1; g1.C = h; g1.bias = b1; g1.offsets = offsets;
-  g1.E = E_local; g1.N = H; g1.K = D; g1.b_mn = false; g1.epi = EPI_BIAS_RELU;
+  g1.E = E_local; g1.N = H; g1.K = D; g1.rows_cap = R_cap; g1.b_mn = false; g1.epi = EPI_BIAS_RELU;
   GemmRows g2 = g1;
   g2.A = h; g2.B = W2; g2.C = out; g2.bias = b2; g2.N = D; g2.K = H; g2.epi = EPI_BIAS;
   for (GemmRows* g : {&g1, &g2}) {
@@ -233,7 +233,7 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
   // dh = (dout W2_e) * 1[h > 0];  dxd = dh W1_e
   GemmRows g3{};
   g3.A = dout; g3.B = W2; g3.C = dh; g3.aux = h; g3.offsets = offsets;
-  g3.E = E_local; g3.N = H; g3.K = D; g3.b_mn = true; g3.epi = EPI_RELU_MASK;
+  g3.E = E_local; g3.N = H; g3.K = D; g3.rows_cap = R_cap; g3.b_mn = true; g3.epi = EPI_RELU_MASK;
   GemmRows g4 = g3;
   g4.A = dh; g4.B = W1; g4.C = dxd; g4.aux = nullptr; g4.N = D; g4.K = H; g4.epi = EPI_PLAIN;
   for (GemmRows* g : {&g3, &g4}) {
@@ -247,8 +247,8 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
   DMOE_TRY(rows_gemm(g3, dt, s));
   DMOE_TRY(rows_gemm(g4, dt, s));
   // dW2_e = dout^T h;  dW1_e = dh^T xd;  db2 / db1 = segment column sums
-  GemmSegK g5{dout, h, dW2, offsets, E_local, D, H};
-  GemmSegK g6{dh, xd, dW1, offsets, E_local, H, D};
+  GemmSegK g5{dout, h, dW2, offsets, E_local, D, H, R_cap};
+  GemmSegK g6{dh, xd, dW1, offsets, E_local, H, D, R_cap};
   DMOE_TRY(segk_gemm(g5, dt, s));
   DMOE_TRY(segk_gemm(g6, dt, s));
   DMOE_TRY(seg_colsum(dout, dt, offsets, E_local, D, db2, s));

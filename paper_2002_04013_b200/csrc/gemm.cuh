@@ -23,6 +23,7 @@ struct GemmRows {
   const int32_t* plan;     // [E+1] device tile plan for this engine's row-tile size
   int E, N, K;
   int64_t rows_single;
+  int64_t rows_cap;        // allocated rows of A / C / aux (TMA tensor extent)
   int64_t max_tiles;       // host upper bound on plan[E] (grid size)
   bool b_mn;
   int epi;
@@ -35,6 +36,7 @@ struct GemmSegK {
   void* C;        // [E][Mdim][N]
   const int32_t* offsets;
   int E, Mdim, N;
+  int64_t R_cap;  // allocated rows of A and B
 };
 
 dmoe_status simt_gemm_rows(const GemmRows& g, dmoe_dtype dt, cudaStream_t s);

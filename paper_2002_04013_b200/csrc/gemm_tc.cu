@@ -1,8 +1,534 @@
-// gemm_tc.cu — tcgen05 grouped GEMM engine (placeholder: not yet enabled).
+// gemm_tc.cu — grouped bf16 GEMM engine on the 5th-generation tensor cores (sm_100a).
+//
+// The expert FFNs are the dense contraction of the DMoE layer: the runtime "aggregates
+// requests into batches for better GPU utilization" (§3.3); here every
+// expert's batch is one row segment [offsets[e], offsets[e+1]) of a dispatched matrix
+// and all experts run in ONE persistent launch.
+//
+// Structure (one CTA per SM, 256 threads, warp-specialised):
+//   warp 0   TMA producer: cp.async.bulk.tensor tiles (128B-swizzled) into a smem ring
+//   warp 1   MMA issuer: one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//            (M=128, N=BN, K=16) with fp32 accumulation in TMEM; tcgen05.commit frees
+//            smem slots and hands finished accumulators to the epilogue
+//   warp 2   TMEM allocator (2 accumulator buffers x BN columns)
+//   warps 4-7 epilogue: tcgen05.ld 32x32b -> registers -> bias / ReLU / ReLU-mask ->
+//            bf16 (or fp32) 16-byte global stores, rows masked to the segment
+// Tile scheduler: static round robin over a device-side tile count (no host sync):
+//   ROWS  tiles = (expert row tile from the plan) x (N tile); K = D or H (fixed)
+//   SEGK  tiles = expert x (M tile) x (N tile); K = the expert's rows (variable). The
+//         last K block's rows past the segment are zeroed in smem before the MMA.
+// Operands are K-major (rows of A in ROWS; torch Linear weights in the forward) or
+// MN-major (weights in the backward-dx GEMMs, both operands of the weight-gradient
+// GEMMs); the UMMA descriptors encode either, so no transposed copy is ever made.
+#include <cuda.h>
+
 #include "gemm.cuh"
+
 namespace dmoe {
-bool tc_rows_supported(const GemmRows&) { return false; }
-bool tc_segk_supported(const GemmSegK&) { return false; }
-dmoe_status tc_gemm_rows(const GemmRows&, cudaStream_t) { return DMOE_ERR_UNSUPPORTED; }
-dmoe_status tc_gemm_segk(const GemmSegK&, cudaStream_t) { return DMOE_ERR_UNSUPPORTED; }
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 64;  // one 128-byte swizzle atom of bf16
+constexpr int TC_THREADS = 256;
+
+// --------------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+#define TMEM_LD32(taddr, r)                                                                         \
+  asm volatile(                                                                                     \
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"               \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),        \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),    \
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), \
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), \
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                         \
+      : "r"(taddr))
+
+// UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), sm_100 version 1.
+//   K-major operand: rows of 128 B (64 bf16 of K), 8-row atoms 1024 B apart (SBO).
+//   MN-major operand: K rows of 128 B (64 bf16 of M/N), 8-row groups 1024 B apart (SBO),
+//                     64-element M/N chunks LBO bytes apart.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: kind::f16, A/B bf16, D fp32, M=128, N=BN, majors
+__host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
+  return (1u << 4)                       // D format f32
+         | (1u << 7)                     // A format bf16
+         | (1u << 10)                    // B format bf16
+         | ((a_mn ? 1u : 0u) << 15)      // A major
+         | ((b_mn ? 1u : 0u) << 16)      // B major
+         | ((uint32_t)(bn >> 3) << 17)   // N >> 3
+         | ((uint32_t)(TC_BM >> 4) << 24);  // M >> 4
+}
+
+// ------------------------------------------------------------------------- kernel
+struct TcParams {
+  const int32_t* offsets;  // [E+1] or nullptr (single group of rows_single rows)
+  const int32_t* plan;     // ROWS: [E+1] row-tile prefix (128-row tiles)
+  const float* bias;
+  const __nv_bfloat16* aux;  // ReLU mask source [rows, N]
+  void* C;
+  int E, N, K, Mdim;
+  int64_t rows_single;
+};
+
+template <int BN> struct TcCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
+  static constexpr int B_BYTES = BN * TC_BK * 2;      // 16/32 KB
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;            // two accumulators
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool SEGK, bool B_MN, int EPI>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+          const TcParams p) {
+  using Cfg = TcCfg<BN>;
+  constexpr int S = Cfg::STAGES;
+  constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + S * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- tile space (identical walk in every role)
+  const int NT = p.N / BN;
+  const int MT = SEGK ? p.Mdim / TC_BM : 0;
+  int total;
+  if (SEGK) total = p.E * MT * NT;
+  else if (p.offsets) total = p.plan[p.E] * NT;
+  else total = (int)((p.rows_single + TC_BM - 1) / TC_BM) * NT;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // decode a tile -> (group e, row0 / m0, n0, row_end, number of K blocks)
+  auto decode = [&](int tile, int& e, int64_t& row0, int64_t& row_end, int& m0, int& n0, int& nkb) {
+    if (SEGK) {
+      e = tile / (MT * NT);
+      const int rem = tile - e * MT * NT;
+      m0 = (rem / NT) * TC_BM;
+      n0 = (rem % NT) * BN;
+      row0 = p.offsets[e];
+      row_end = p.offsets[e + 1];
+      nkb = (int)((row_end - row0 + TC_BK - 1) / TC_BK);
+    } else {
+      const int rt = tile / NT;
+      n0 = (tile - rt * NT) * BN;
+      m0 = 0;
+      if (p.offsets) {
+        int lo = 0, hi = p.E;
+        while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (p.plan[mid] <= rt) lo = mid; else hi = mid; }
+        e = lo;
+        row0 = p.offsets[e] + (int64_t)(rt - p.plan[e]) * TC_BM;
+        row_end = p.offsets[e + 1];
+      } else {
+        e = 0;
+        row0 = (int64_t)rt * TC_BM;
+        row_end = p.rows_single;
+      }
+      nkb = p.K / TC_BK;
+    }
+  };
+
+  if (warp == 0) {
+    // ======================= TMA producer =======================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        int e, m0, n0, nkb;
+        int64_t row0, row_end;
+        decode(tile, e, row0, row_end, m0, n0, nkb);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          if (SEGK) {
+            const int kr = (int)(row0 + kb * TC_BK);
+            tma_load_2d(sa, &tmA, &full[stage], m0, kr);
+            tma_load_2d(sa + 8192, &tmA, &full[stage], m0 + 64, kr);
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(sb + c * 8192, &tmB, &full[stage], n0 + 64 * c, kr);
+          } else {
+            tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, (int)row0);
+            if (B_MN) {
+#pragma unroll
+              for (int c = 0; c < BN / 64; ++c)
+                tma_load_3d(sb + c * 8192, &tmB, &full[stage], n0 + 64 * c, kb * TC_BK, e);
+            } else {
+              tma_load_3d(sb, &tmB, &full[stage], kb * TC_BK, n0, e);
+            }
+          }
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ======================= MMA issuer =======================
+    constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int e, m0, n0, nkb;
+      int64_t row0, row_end;
+      decode(tile, e, row0, row_end, m0, n0, nkb);
+      if (nkb == 0) continue;  // empty segment: the epilogue writes zeros without TMEM
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+        uint8_t* sb = sa + Cfg::A_BYTES;
+        if (SEGK && kb == nkb - 1) {
+          // zero the K rows past the segment end in both operands (they hold other
+          // experts' rows or uninitialised capacity rows)
+          const int valid = (int)(row_end - row0 - (int64_t)kb * TC_BK);
+          if (valid < TC_BK) {
+            const int lines = (TC_BK - valid);
+            const int nchunk = 2 + BN / 64;  // 128-byte lines per K row across A and B chunks
+            for (int i = lane; i < lines * nchunk * 8; i += 32) {
+              const int piece = i & 7, rest = i >> 3;
+              const int c = rest % nchunk, r = valid + rest / nchunk;
+              uint8_t* base = c < 2 ? sa + c * 8192 : sb + (c - 2) * 8192;
+              *reinterpret_cast<uint4*>(base + r * 128 + piece * 16) = make_uint4(0, 0, 0, 0);
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          }
+          __syncwarp();
+        }
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            const uint64_t ad = A_MN ? make_desc(a0 + k * 2048, 8192, 1024) : make_desc(a0 + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(b0 + k * 2048, 8192, 1024) : make_desc(b0 + k * 32, 16, 1024);
+            tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (kb == nkb - 1) tc_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 4) {
+    // ======================= epilogue =======================
+    const int q = warp & 3;  // TMEM lanes 32q .. 32q+31
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int e, m0, n0, nkb;
+      int64_t row0, row_end;
+      decode(tile, e, row0, row_end, m0, n0, nkb);
+      const int rloc = q * 32 + lane;
+      if (SEGK) {
+        __nv_bfloat16* C = (__nv_bfloat16*)p.C + ((int64_t)e * p.Mdim + m0 + rloc) * p.N + n0;
+        if (nkb == 0) {
+          for (int c = 0; c < BN; c += 8) *reinterpret_cast<uint4*>(C + c) = make_uint4(0, 0, 0, 0);
+          continue;
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          TMEM_LD32(taddr + c, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            uint4 v = make_uint4(pack_bf16x2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])),
+                                 pack_bf16x2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])),
+                                 pack_bf16x2(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5])),
+                                 pack_bf16x2(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7])));
+            *reinterpret_cast<uint4*>(C + c + j) = v;
+          }
+        }
+      } else {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const int64_t row = row0 + rloc;
+        const bool live = row < row_end;
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+        const float* bias = p.bias ? p.bias + (int64_t)e * p.N + n0 : nullptr;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          TMEM_LD32(taddr + c, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (!live) continue;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c + j));
+              v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
+            }
+          }
+          if (EPI == EPI_BIAS_RELU) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+          }
+          if (EPI == EPI_RELU_MASK) {
+            const __nv_bfloat16* hrow = p.aux + row * p.N + n0 + c;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              const uint4 hv = *reinterpret_cast<const uint4*>(hrow + j);
+              const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                // bf16 h > 0  <=>  sign bit clear and not +0
+                const uint32_t lo = hw[i] & 0xFFFFu, hi = hw[i] >> 16;
+                if (!(lo != 0 && !(lo & 0x8000u))) v[j + 2 * i] = 0.0f;
+                if (!(hi != 0 && !(hi & 0x8000u))) v[j + 2 * i + 1] = 0.0f;
+              }
+            }
+          }
+          if (EPI == EPI_F32_BIAS) {
+            float* C = (float*)p.C + row * p.N + n0 + c;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(C + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          } else {
+            __nv_bfloat16* C = (__nv_bfloat16*)p.C + row * p.N + n0 + c;
+#pragma unroll
+            for (int j = 0; j < 32; j += 8)
+              *reinterpret_cast<uint4*>(C + j) =
+                  make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                             pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+  }
+}
+
+// ----------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+
+// bf16 tensor map, dims innermost first; box {64, box1, 1...}; 128-byte swizzle
+static dmoe_status make_map(CUtensorMap* m, const void* ptr, int rank, const uint64_t* dims,
+                            uint32_t box1) {
+  EncodeTiledFn fn = encode_fn();
+  DMOE_REQUIRE(fn != nullptr, DMOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[3], gstride[2];
+  cuuint32_t box[3] = {64, box1, 1}, estr[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) gdim[i] = dims[i];
+  gstride[0] = dims[0] * 2;
+  if (rank == 3) gstride[1] = dims[0] * dims[1] * 2;
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), gdim, gstride, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DMOE_REQUIRE(r == CUDA_SUCCESS, DMOE_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DMOE_OK;
+}
+
+static int pick_bn(int N) { return (N % 256 == 0) ? 256 : 128; }
+
+bool tc_rows_supported(const GemmRows& g) {
+  if (g.K % TC_BK != 0 || g.K <= 0) return false;
+  if (g.N % 128 != 0) return false;
+  if (g.epi == EPI_F32_BIAS && g.offsets != nullptr) return false;
+  if (encode_fn() == nullptr) return false;
+  return true;
+}
+bool tc_segk_supported(const GemmSegK& g) {
+  return g.Mdim % TC_BM == 0 && g.N % 128 == 0 && encode_fn() != nullptr;
+}
+
+template <int BN, bool SEGK, bool B_MN, int EPI>
+static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int64_t max_tiles,
+                          cudaStream_t s) {
+  auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
+  const int smem = TcCfg<BN>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  int64_t grid = max_tiles < num_sms() ? max_tiles : num_sms();
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, TC_THREADS, smem, s>>>(a, b, p);
+  return check_launch("tc_gemm");
+}
+
+template <int BN>
+static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtensorMap& b, const TcParams& p,
+                           int64_t tiles, cudaStream_t s) {
+#define DMOE_TC_ROWS(BMN, E_) return launch<BN, false, BMN, E_>(a, b, p, tiles, s)
+#define DMOE_TC_EPI(BMN)                                   \
+  switch (g.epi) {                                         \
+    case EPI_F32_BIAS: DMOE_TC_ROWS(BMN, EPI_F32_BIAS);    \
+    case EPI_BIAS_RELU: DMOE_TC_ROWS(BMN, EPI_BIAS_RELU);  \
+    case EPI_BIAS: DMOE_TC_ROWS(BMN, EPI_BIAS);            \
+    case EPI_RELU_MASK: DMOE_TC_ROWS(BMN, EPI_RELU_MASK);  \
+    default: DMOE_TC_ROWS(BMN, EPI_PLAIN);                 \
+  }
+  if (g.b_mn) { DMOE_TC_EPI(true) } else { DMOE_TC_EPI(false) }
+#undef DMOE_TC_EPI
+#undef DMOE_TC_ROWS
+}
+
+dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
+  if (g.max_tiles <= 0) return DMOE_OK;
+  const int BN = pick_bn(g.N);
+  // A: [rows_cap, K] K-major; rows past the extent are zero-filled by TMA, rows past a
+  // segment produce accumulator rows the epilogue never stores.
+  CUtensorMap ta, tb;
+  uint64_t adims[2] = {(uint64_t)g.K, (uint64_t)(g.rows_cap > 0 ? g.rows_cap : 1)};
+  DMOE_TRY(make_map(&ta, g.A, 2, adims, TC_BM));
+  if (g.b_mn) {
+    uint64_t bdims[3] = {(uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.E};
+    DMOE_TRY(make_map(&tb, g.B, 3, bdims, 64));
+  } else {
+    uint64_t bdims[3] = {(uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.E};
+    DMOE_TRY(make_map(&tb, g.B, 3, bdims, (uint32_t)BN));
+  }
+  TcParams p{};
+  p.offsets = g.offsets; p.plan = g.plan; p.bias = g.bias; p.aux = (const __nv_bfloat16*)g.aux;
+  p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
+  const int64_t tiles = g.max_tiles * (g.N / BN);
+  if (BN == 256) return rows_bn<256>(g, ta, tb, p, tiles, s);
+  return rows_bn<128>(g, ta, tb, p, tiles, s);
+}
+
+dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
+  const int BN = pick_bn(g.N);
+  CUtensorMap ta, tb;
+  // K rows past a segment end (other experts' rows, or capacity rows past R) are zeroed
+  // in smem before the MMA; rows past R_cap are zero-filled by TMA.
+  const uint64_t rc = (uint64_t)(g.R_cap > 0 ? g.R_cap : 1);
+  uint64_t adims[2] = {(uint64_t)g.Mdim, rc};
+  uint64_t bdims[2] = {(uint64_t)g.N, rc};
+  DMOE_TRY(make_map(&ta, g.A, 2, adims, 64));
+  DMOE_TRY(make_map(&tb, g.B, 2, bdims, 64));
+  TcParams p{};
+  p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim;
+  const int64_t tiles = (int64_t)g.E * (g.Mdim / TC_BM) * (g.N / BN);
+  if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, p, tiles, s);
+  return launch<128, true, true, EPI_PLAIN>(ta, tb, p, tiles, s);
+}
+
 }  // namespace dmoe
