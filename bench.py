@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""DMoE layer step benchmark (forward + backward), BASELINE.json metric:
+"DMoE layer tokens/sec fwd+bwd at 1/2/4/8 B200; % HBM / bf16 tensor peak".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config mnist] [--impl ours|reference]
+
+One step = the whole hot path (gate -> beam top-k -> dispatch -> expert FFN fwd -> combine ->
+combine bwd -> expert FFN bwd -> gate bwd) over one batch of synthetic tokens generated on the
+device by the seeded counter generator (gen/).  `value` = tokens/s of the whole job with inputs
+resident in HBM, timed with CUDA events around a CUDA-graph replay of the step (max over ranks);
+L2 is flushed (untimed 256 MiB write) before every timed step.  `e2e` = the same metric through
+the public API with host buffers: pinned-host x, dy -> device, step, y, dx -> pinned host, all
+inside the timed region.  `--impl reference` times the float64 CPU oracle (oracle/) on a bounded
+token sample of the same workload (the only reference this paper has).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import gen  # noqa: E402
+from gen import CONFIGS  # noqa: E402
+
+METRIC = "DMoE layer tokens/sec fwd+bwd"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+
+
+def load_peaks():
+    try:
+        with open(PEAKS) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+# ------------------------------------------------------------------ algorithmic work
+def step_work(cfg, R):
+    """Algorithmic FLOPs and HBM bytes of one layer step, R = dispatched rows."""
+    T, D, H, k, dM, E = cfg.T, cfg.D, cfg.H, cfg.k, cfg.dM, cfg.E
+    es = 2 if cfg.dtype == "bf16" else 4
+    flops = 12.0 * R * D * H + 6.0 * T * D * dM
+    wbytes = E * 2 * D * H * es
+    return flops, wbytes
+
+
+def call_bytes(cfg, name, R, E_act):
+    """Algorithmic bytes moved by one ABI call (inputs read once + outputs written once)."""
+    T, D, H, k, dM, E = cfg.T, cfg.D, cfg.H, cfg.k, cfg.dM, cfg.E
+    es = 2 if cfg.dtype == "bf16" else 4
+    W = E * D * H * es  # one weight matrix of all experts
+    return {
+        "gate_scores": T * D * es + D * dM * es + T * dM * 4,
+        "beam_topk": T * dM * 4 + T * k * 8,
+        "dispatch": T * k * 8 + T * k * 9 + R * 4 + T * D * es + R * D * es,
+        # read xd, W1, W2; write h, out (experts with no rows read no weights)
+        "expert_ffn_fwd": R * D * es + 2 * W * E_act / E + R * H * es + R * D * es,
+        "combine": R * D * es + T * k * 8 + T + T * D * es,
+        "combine_bwd": T * D * es + R * D * es + T * k * 8 + R * D * es + T * k * 4,
+        # read xd, h, dout, W1, W2; write dxd, dW1, dW2 (all experts), db; dh written+read twice
+        "expert_ffn_bwd": R * D * es * 2 + R * H * es + 2 * W * E_act / E + R * D * es + 2 * W
+        + E * (D + H) * 4 + 3 * R * H * es,
+        "gate_bwd": T * D * es * 2 + R * D * es + T * k * 8 + T * D * es + D * dM * 4,
+    }[name]
+
+
+def call_flops(cfg, name, R):
+    T, D, H, dM = cfg.T, cfg.D, cfg.H, cfg.dM
+    return {"gate_scores": 2.0 * T * D * dM, "expert_ffn_fwd": 4.0 * R * D * H,
+            "expert_ffn_bwd": 8.0 * R * D * H, "gate_bwd": 4.0 * T * D * dM}.get(name, 0.0)
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.p is None:
+            return
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                self.rows.append(f)
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        loaded = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ our implementation
+def build_layer(cfg, seed, device, T):
+    import torch
+    from paper_2002_04013_b200 import DMoELayer
+    dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    lay = DMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=T, device=device)
+    for t, tid in ((lay.Wg, gen.WG), (lay.bg, gen.BG), (lay.W1, gen.W1), (lay.b1, gen.B1), (lay.W2, gen.W2),
+                   (lay.b2, gen.B2)):
+        dist, scale = cfg.dist(tid)
+        gen.dev_fill(t, seed, tid, dist, scale)
+    x = torch.empty(T, cfg.D, dtype=dt, device=device)
+    dy = torch.empty(T, cfg.D, dtype=dt, device=device)
+    gen.dev_fill(x, seed, gen.X, *cfg.dist(gen.X))
+    gen.dev_fill(dy, seed, gen.DY, *cfg.dist(gen.DY))
+    nw = (cfg.E + 31) // 32
+    alive = gen.dev_mask(torch.empty(nw, dtype=torch.int32, device=device), seed, gen.ALIVE, cfg.dead_frac, cfg.E)
+    resp = gen.dev_mask(torch.empty(nw, dtype=torch.int32, device=device), seed, gen.RESPONDED, cfg.fail_frac,
+                        cfg.E)
+    return lay, x, dy, alive, resp
+
+
+CALLS = ["gate_scores", "beam_topk", "dispatch", "expert_ffn_fwd", "combine", "combine_bwd", "expert_ffn_bwd",
+         "gate_bwd"]
+
+
+def run_calls(lay, x, dy, alive, resp, ev=None):
+    """The step as its 8 ABI calls (same as DMoELayer.step), optionally bracketed by events."""
+    from paper_2002_04013_b200 import _lib as L
+    T = x.shape[0]
+    g = lay.g
+    seq = [
+        lambda: L.dmoe_gate_scores(x, lay.Wg, lay.bg, g, lay.G[:T]),
+        lambda: L.dmoe_beam_topk(lay.G[:T], g, alive, lay.sel[:T], lay.sel_score[:T], lay.ws),
+        lambda: L.dmoe_dispatch(x, g, lay.sel[:T], lay.sel_score[:T], resp, lay.w[:T], lay.valid[:T], lay.n_dropped,
+                                lay.counts, lay.offsets, lay.row_of_slot[:T], lay.token_of_row, lay.xd, lay.ws),
+        lambda: L.dmoe_expert_ffn_fwd(lay.xd, lay.offsets, lay.W1, lay.b1, lay.W2, lay.b2, lay.h, lay.out, lay.ws),
+        lambda: L.dmoe_combine(lay.out, lay.row_of_slot[:T], lay.w[:T], lay.valid[:T], lay.y[:T]),
+        lambda: L.dmoe_combine_bwd(dy, lay.out, lay.row_of_slot[:T], lay.w[:T], lay.dout, lay.dscore[:T]),
+        lambda: L.dmoe_expert_ffn_bwd(lay.xd, lay.h, lay.dout, lay.offsets, lay.W1, lay.W2, lay.dxd, lay.dW1,
+                                      lay.db1, lay.dW2, lay.db2, lay.ws),
+        lambda: L.dmoe_gate_bwd(x, lay.Wg, lay.sel[:T], lay.dscore[:T], lay.dxd, lay.row_of_slot[:T], g,
+                                lay.dx[:T], lay.dWg, lay.dbg, lay.ws),
+    ]
+    for i, f in enumerate(seq):
+        if ev is not None:
+            ev[i][0].record()
+        f()
+        if ev is not None:
+            ev[i][1].record()
+
+
+def bench_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2002_04013_b200 import _lib as L
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    T = cfg.T
+    seed = args.seed + rank  # each rank: its own tokens (weak scaling over independent batches)
+    lay, x, dy, alive, resp = build_layer(cfg, seed, device, T)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    stream = torch.cuda.Stream(device)
+    torch.cuda.synchronize()
+
+    # warm-up through the eager ABI path, then capture one step in a CUDA graph
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 1)):
+            run_calls(lay, x, dy, alive, resp)
+    stream.synchronize()
+    c0 = L.dmoe_launch_counters()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        run_calls(lay, x, dy, alive, resp)
+    c1 = L.dmoe_launch_counters()
+    launches_per_step = c1[0] - c0[0]
+    tc_per_step = c1[1] - c0[1]
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K graph replays, L2 flushed (untimed) before each
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local_rank) as clk:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)
+                starts[i].record(stream)
+                graph.replay()
+                ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- per-call timing (eager calls bracketed by events on the launch stream)
+    ev = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)] for _ in CALLS]
+    per_call = {c: [] for c in CALLS}
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            run_calls(lay, x, dy, alive, resp, ev)
+            stream.synchronize()
+            for c, (a, b) in zip(CALLS, ev):
+                per_call[c].append(a.elapsed_time(b))
+    per_call_ms = {c: sum(v) / len(v) for c, v in per_call.items()}
+
+    # ---- e2e through the public API with pinned host buffers
+    hx = torch.empty(T, cfg.D, dtype=x.dtype, pin_memory=True)
+    hdy = torch.empty_like(hx, pin_memory=True)
+    hx.copy_(x)
+    hdy.copy_(dy)
+    hy = torch.empty_like(hx, pin_memory=True)
+    hdx = torch.empty_like(hx, pin_memory=True)
+    dx_in = torch.empty_like(x)
+    dy_in = torch.empty_like(dy)
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        dx_in.copy_(hx, non_blocking=True)
+        dy_in.copy_(hdy, non_blocking=True)
+        lay.forward(dx_in, alive, resp)
+        gx = lay.backward(dy_in)
+        hy.copy_(lay.y[:T], non_blocking=True)
+        hdx.copy_(gx, non_blocking=True)
+        b.record()
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e = sum(e2e_ms) / len(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+    R = int(lay.offsets[cfg.E].item())
+    E_act = int((lay.counts[: cfg.E] > 0).sum().item())
+    n_dropped = int(lay.n_dropped.item())
+    return dict(ms=ms, step_ms=step_ms, per_call_ms=per_call_ms, e2e_ms=e2e, R=R, E_act=E_act,
+                n_dropped=n_dropped, launches=launches_per_step, tc_launches=tc_per_step, clocks=clk.summary(),
+                h2d=2 * T * cfg.D * x.element_size(), d2h=2 * T * cfg.D * x.element_size())
+
+
+# ------------------------------------------------------------------ oracle (CPU)
+def oracle_sample_tokens(cfg):
+    """Bounded CPU sample: ~10-30 s of float64 oracle work for one step's worth of tokens."""
+    per_tok = cfg.k * 6.0 * cfg.D * cfg.H + 2.0 * cfg.D * cfg.dM   # multiply-adds per token, fwd+bwd
+    return int(max(16, min(cfg.T, 4e10 / per_tok)))
+
+
+def oracle_inputs(cfg, seed, Ts):
+    from gen.inputs import make_inputs  # generator only (no method arithmetic)
+    return make_inputs(cfg, seed=seed, T=Ts)
+
+
+def time_oracle(cfg, seed, steps=1):
+    from oracle import oracle as O
+    Ts = oracle_sample_tokens(cfg)
+    inp = oracle_inputs(cfg, seed, Ts)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.layer_step(inp["X"], inp["Wg"], inp["bg"], inp["W1"], inp["b1"], inp["W2"], inp["b2"], inp["dY"],
+                     inp["alive"], inp["responded"], cfg.d, cfg.M, cfg.k, cfg.B)
+        times.append(time.perf_counter() - t0)
+    cores = len(os.sched_getaffinity(0))
+    sample = (f"first {Ts} of {cfg.T} tokens of the '{cfg.name}' step (same seed/recipe), all {cfg.E} experts' "
+              f"weights; float64 oracle forward+backward; value = sample tokens / wall seconds")
+    return Ts, times, cores, sample
+
+
+def bench_reference(args, cfg):
+    os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
+    steps = max(1, min(args.steps, 3))
+    for _ in range(min(args.warmup, 1)):
+        time_oracle(cfg, args.seed, 1)
+    Ts, times, cores, sample = time_oracle(cfg, args.seed, steps)
+    sec = sum(times) / len(times)
+    v = Ts / sec
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "tokens": Ts, "grid": f"{cfg.M}^{cfg.d}", "D": cfg.D, "H": cfg.H,
+                       "k": cfg.k, "fail_frac": cfg.fail_frac},
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="mnist", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))  # oracle baseline threads
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(bench_reference(args, cfg)), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    r = bench_ours(args, cfg, rank, world, local_rank)
+    hbm, tf_burst, tf_sus, peak_src = load_peaks()
+    tokens = cfg.T * world
+    value = tokens / (r["ms"] / 1e3)
+    e2e_v = tokens / (r["e2e_ms"] / 1e3)
+    # dominant call and its roofline
+    dom = max(r["per_call_ms"], key=r["per_call_ms"].get)
+    dms = r["per_call_ms"][dom]
+    fl = call_flops(cfg, dom, r["R"])
+    by = call_bytes(cfg, dom, r["R"], r["E_act"])
+    ai = fl / by if by else 0.0
+    ridge = tf_sus * 1e12 / (hbm * 1e9)
+    if fl > 0 and ai > ridge:
+        roof = {"bound": "tensor", "achieved": fl / (dms / 1e3) / 1e12, "peak": tf_sus, "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": by / (dms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": None, "kernel": f"dmoe_{dom}",
+                 "algorithmic_bytes": by, "algorithmic_flops": fl, "ms": dms, "peak_source": peak_src})
+    out = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (counter-based generator, seeded)",
+        "config": {"workload": cfg.name, "tokens_per_gpu": cfg.T, "grid": f"{cfg.M}^{cfg.d}", "E": cfg.E, "D": cfg.D,
+                   "H": cfg.H, "k": cfg.k, "beam": cfg.B, "fail_frac": cfg.fail_frac,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed before every timed step (256 MiB write, untimed)", "graph": "cuda graph replay"},
+        "e2e": {"value": e2e_v, "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
+        "gpu_launches": r["launches"] * args.steps,
+        "roofline": roof,
+        "clocks": r["clocks"],
+        "detail": {"per_call_ms": r["per_call_ms"], "dispatched_rows": r["R"], "experts_with_rows": r["E_act"],
+                   "dropped_tokens": r["n_dropped"], "launches_per_step": r["launches"],
+                   "tcgen05_gemm_launches_per_step": r["tc_launches"],
+                   "step_flops": step_work(cfg, r["R"])[0]},
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Ts, times, cores, sample = time_oracle(cfg, args.seed, 1)
+        out["cpu_baseline"] = {"value": Ts / times[0], "unit": "tokens/s", "cores": cores, "kind": "oracle",
+                               "sample": sample}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -81,6 +81,11 @@ typedef struct {
 const char* dmoe_last_error(void); /* thread-local text for the last non-OK status */
 int32_t dmoe_version(void);
 
+/* Host-side launch counters of this process (for tests and the bench's gpu_launches):
+ * out[0] = all kernel launches, out[1] = tcgen05 GEMM launches, out[2] = SIMT GEMM
+ * launches, out[3] reserved.  Writes min(n, 4) entries (host memory); returns 4. */
+int32_t dmoe_launch_counters(int64_t* out, int32_t n);
+
 /* Scratch needed by any call below for T tokens, d_model D, hidden H, E_local experts
  * on this rank and R_cap dispatched-row capacity (T*k on one GPU). */
 size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_t E_local,

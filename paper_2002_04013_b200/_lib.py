@@ -36,6 +36,7 @@ _P, _I64, _I32, _SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_
 _SIGS = {
     "dmoe_last_error": ([], ctypes.c_char_p),
     "dmoe_version": ([], ctypes.c_int32),
+    "dmoe_launch_counters": ([_P, _I32], ctypes.c_int32),
     "dmoe_workspace_bytes": ([_I64, _I32, _I32, dmoe_grid, _I32, _I64], ctypes.c_size_t),
     "dmoe_gate_scores": ([_P, _I32, _I64, _I32, _P, _P, dmoe_grid, _P, _P], ctypes.c_int),
     "dmoe_beam_topk": ([_P, _I64, dmoe_grid, _P, _P, _P, _P, _SZ, _P], ctypes.c_int),
@@ -85,6 +86,13 @@ def grid(d, M, k, beam=0):
 
 def dmoe_version():
     return _L.dmoe_version()
+
+
+def dmoe_launch_counters():
+    """(all launches, tcgen05 GEMM launches, SIMT GEMM launches) issued by this process."""
+    buf = (ctypes.c_int64 * 4)()
+    _L.dmoe_launch_counters(buf, 4)
+    return tuple(buf[:3])
 
 
 def dmoe_workspace_bytes(T, D, H, g, E_local, R_cap):

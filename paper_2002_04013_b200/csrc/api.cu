@@ -19,7 +19,10 @@ dmoe_status set_error(dmoe_status st, const char* fmt, ...) {
   return st;
 }
 
+int64_t g_counters[4] = {0, 0, 0, 0};  // launches: all kernels, tcgen05 GEMMs, SIMT GEMMs, -
+
 dmoe_status check_launch(const char* what) {
+  __atomic_fetch_add(&g_counters[0], 1, __ATOMIC_RELAXED);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(DMOE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
   return DMOE_OK;
@@ -99,6 +102,11 @@ using namespace dmoe;
 extern "C" {
 
 const char* dmoe_last_error(void) { return g_err; }
+
+int32_t dmoe_launch_counters(int64_t* out, int32_t n) {
+  for (int i = 0; i < n && i < 4; ++i) out[i] = __atomic_load_n(&g_counters[i], __ATOMIC_RELAXED);
+  return 4;
+}
 int32_t dmoe_version(void) { return 1; }
 
 size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_t E_local,

@@ -12,6 +12,7 @@ constexpr int kNumSMs = 148;  // B200 (sm_100a); launch code queries the device,
 
 dmoe_status set_error(dmoe_status st, const char* fmt, ...);
 dmoe_status check_launch(const char* what);
+extern int64_t g_counters[4];
 int num_sms();
 
 #define DMOE_REQUIRE(cond, st, ...)                          \

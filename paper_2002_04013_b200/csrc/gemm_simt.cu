@@ -177,6 +177,7 @@ dmoe_status simt_gemm_rows(const GemmRows& g, dmoe_dtype dt, cudaStream_t s) {
   } else {
     launch_rows<float, float>(g, s);
   }
+  __atomic_fetch_add(&g_counters[2], 1, __ATOMIC_RELAXED);
   return check_launch("simt_gemm_rows");
 }
 
@@ -188,6 +189,7 @@ dmoe_status simt_gemm_segk(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
   else
     k_simt_segk<float><<<grid, 256, 0, s>>>((const float*)g.A, (const float*)g.B, (float*)g.C,
                                             g.offsets, g.Mdim, g.N);
+  __atomic_fetch_add(&g_counters[2], 1, __ATOMIC_RELAXED);
   return check_launch("simt_gemm_segk");
 }
 

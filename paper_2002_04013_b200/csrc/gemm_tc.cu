@@ -471,6 +471,7 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcPa
   int64_t grid = max_tiles < num_sms() ? max_tiles : num_sms();
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, TC_THREADS, smem, s>>>(a, b, p);
+  __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
 }
 
