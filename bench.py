@@ -157,7 +157,7 @@ def run_calls(lay, x, dy, alive, resp, ev=None):
     T = x.shape[0]
     g = lay.g
     seq = [
-        lambda: L.dmoe_gate_scores(x, lay.Wg, lay.bg, g, lay.G[:T]),
+        lambda: L.dmoe_gate_scores(x, lay.Wg, lay.bg, g, lay.G[:T], lay.ws),
         lambda: L.dmoe_beam_topk(lay.G[:T], g, alive, lay.sel[:T], lay.sel_score[:T], lay.ws),
         lambda: L.dmoe_dispatch(x, g, lay.sel[:T], lay.sel_score[:T], resp, lay.w[:T], lay.valid[:T], lay.n_dropped,
                                 lay.counts, lay.offsets, lay.row_of_slot[:T], lay.token_of_row, lay.xd, lay.ws),

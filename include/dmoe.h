@@ -93,9 +93,11 @@ size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_
 
 /* S1 — gate scores, Eq. 2:
  *   G[t, i*M + j] = g_i(x_t, j) = b_g[i*M + j] + sum_c x[t, c] * W_g[c, i*M + j]
- * x [T, D] in dtype dt; W_g [D, d*M] in dt; b_g [d*M] fp32; G [T, d*M] fp32 (out). */
+ * x [T, D] in dtype dt; W_g [D, d*M] in dt; b_g [d*M] fp32; G [T, d*M] fp32 (out).
+ * bf16 with d*M % 16 == 0 runs on the tensor cores (W_g^T staged in `ws`). */
 dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg,
-                             const float* bg, dmoe_grid g, float* G, dmoe_stream_t stream);
+                             const float* bg, dmoe_grid g, float* G, void* ws, size_t ws_bytes,
+                             dmoe_stream_t stream);
 
 /* S2+S3 — SelectExperts, Alg. 1 with FilterAlive,
  * per token: beam := [()]; for level i: expand every prefix p by j in [0,M) with score

@@ -38,7 +38,7 @@ _SIGS = {
     "dmoe_version": ([], ctypes.c_int32),
     "dmoe_launch_counters": ([_P, _I32], ctypes.c_int32),
     "dmoe_workspace_bytes": ([_I64, _I32, _I32, dmoe_grid, _I32, _I64], ctypes.c_size_t),
-    "dmoe_gate_scores": ([_P, _I32, _I64, _I32, _P, _P, dmoe_grid, _P, _P], ctypes.c_int),
+    "dmoe_gate_scores": ([_P, _I32, _I64, _I32, _P, _P, dmoe_grid, _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_beam_topk": ([_P, _I64, dmoe_grid, _P, _P, _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_dispatch": ([_P, _I32, _I64, _I32, dmoe_grid, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                        _SZ, _P], ctypes.c_int),
@@ -99,9 +99,10 @@ def dmoe_workspace_bytes(T, D, H, g, E_local, R_cap):
     return int(_L.dmoe_workspace_bytes(T, D, H, g, E_local, R_cap))
 
 
-def dmoe_gate_scores(x, Wg, bg, g, G):
+def dmoe_gate_scores(x, Wg, bg, g, G, ws):
     T, D = x.shape
-    _check("dmoe_gate_scores", _L.dmoe_gate_scores(_p(x), _dt(x), T, D, _p(Wg), _p(bg), g, _p(G), _stream()))
+    _check("dmoe_gate_scores", _L.dmoe_gate_scores(_p(x), _dt(x), T, D, _p(Wg), _p(bg), g, _p(G), _p(ws),
+                                                   ws.numel() * ws.element_size(), _stream()))
 
 
 def dmoe_beam_topk(G, g, alive_bits, sel, sel_score, ws):

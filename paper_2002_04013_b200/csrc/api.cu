@@ -56,6 +56,8 @@ dmoe_status combine_bwd(const void* dy, const void* out, const int32_t* row_of_s
                         const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout,
                         float* dscore, cudaStream_t s);
 size_t gate_bwd_ws_bytes(int64_t T, int32_t D, int dM);
+dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt, void* dst,
+                      cudaStream_t s);
 dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const float* dscore,
                      const void* dxd, const int32_t* row_of_slot, int64_t T, int32_t D, int d, int M,
                      int k, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
@@ -113,7 +115,7 @@ size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_
                             int64_t R_cap) {
   int64_t E = 1;
   for (int i = 0; i < g.d; ++i) E *= g.M;
-  size_t beam = prefix_words(g.d, g.M) * 4 + 256;
+  size_t beam = prefix_words(g.d, g.M) * 4 + (size_t)g.d * g.M * D * 2 + 256;
   size_t disp = dispatch_ws_bytes(T, E);
   size_t ffn = 2 * align_up((size_t)(E_local + 1) * 4, 256) + align_up((size_t)R_cap * H * 4, 256) + 1024;
   size_t gate = gate_bwd_ws_bytes(T, D, g.d * g.M);
@@ -125,21 +127,32 @@ size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_
 }
 
 dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg,
-                             const float* bg, dmoe_grid g, float* G, dmoe_stream_t stream) {
+                             const float* bg, dmoe_grid g, float* G, void* ws, size_t ws_bytes,
+                             dmoe_stream_t stream) {
   int64_t E = 0;
   DMOE_TRY(check_grid(&g, &E));
   DMOE_TRY(check_dt(dt, D));
   DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
   if (T == 0) return DMOE_OK;
-  NN(x); NN(Wg); NN(bg); NN(G);
+  NN(x); NN(Wg); NN(bg); NN(G); NN(ws);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int dM = g.d * g.M;
   GemmRows r{};
   r.A = x; r.B = Wg; r.C = G; r.bias = bg; r.aux = nullptr;
   r.offsets = nullptr; r.plan = nullptr;
-  r.E = 1; r.N = g.d * g.M; r.K = D; r.rows_single = T; r.rows_cap = T;
-  r.b_mn = true; r.epi = EPI_F32_BIAS;
-  const bool tc = dt == DMOE_BF16 && tc_rows_supported(r);
-  r.max_tiles = ceil_div(T, tc ? kPlanBM_TC : kPlanBM_SIMT);
-  return rows_gemm(r, dt, (cudaStream_t)stream);
+  r.E = 1; r.N = dM; r.K = D; r.rows_single = T; r.rows_cap = T;
+  r.b_mn = false; r.epi = EPI_F32_BIAS;
+  if (dt == DMOE_BF16 && tc_rows_supported(r)) {
+    // tensor-core path: W_g^T [d*M, D] (K-major B operand) staged in the workspace
+    DMOE_REQUIRE(ws_bytes >= (size_t)dM * D * 2, DMOE_ERR_ARG, "gate_scores: workspace too small");
+    DMOE_TRY(transpose(Wg, D, dM, dt, ws, s));
+    r.B = ws;
+    r.max_tiles = ceil_div(T, kPlanBM_TC);
+    return tc_gemm_rows(r, s);
+  }
+  r.b_mn = true;
+  r.max_tiles = ceil_div(T, kPlanBM_SIMT);
+  return simt_gemm_rows(r, dt, s);
 }
 
 dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive_bits,

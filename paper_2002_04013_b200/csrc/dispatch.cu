@@ -18,14 +18,23 @@
 
 namespace dmoe {
 
-constexpr int kChunkTok = 64;   // tokens per chunk (one warp)
 constexpr int kDispWarps = 4;   // warps per CTA
+
+// tokens per chunk (one warp per chunk): small enough for >= ~16 warps per SM on the
+// rank/histogram passes, large enough that the per-chunk histograms stay <= 4M ints.
+int64_t chunk_tokens(int64_t T, int64_t E) {
+  int64_t nc = ceil_div(T, 16);
+  const int64_t cap = (int64_t)(4 << 20) / (E > 0 ? E : 1);
+  if (nc > cap) nc = cap;
+  if (nc < 1) nc = 1;
+  return ceil_div(T > 0 ? T : 1, nc);
+}
 
 __global__ void __launch_bounds__(kDispWarps * 32)
 k_weights_hist(const int32_t* __restrict__ sel, const float* __restrict__ sel_score,
                const uint32_t* __restrict__ responded, int64_t T, int k, int64_t E,
                float* __restrict__ w, uint8_t* __restrict__ valid, int32_t* __restrict__ hist,
-               int32_t* __restrict__ chunk_dropped, int64_t n_chunks) {
+               int32_t* __restrict__ chunk_dropped, int64_t n_chunks, int64_t kChunkTok) {
   const int lane = threadIdx.x & 31;
   const int64_t c = blockIdx.x * (int64_t)kDispWarps + (threadIdx.x >> 5);
   if (c >= n_chunks) return;
@@ -67,19 +76,26 @@ k_weights_hist(const int32_t* __restrict__ sel, const float* __restrict__ sel_sc
   if (lane == 0) chunk_dropped[c] = dropped;
 }
 
-// per expert: exclusive prefix of hist[:, e] over chunks (in place), total -> counts[e]
+// per expert (one warp): exclusive prefix of hist[:, e] over chunks (in place) -> counts[e]
 __global__ void k_scan_chunks(int32_t* __restrict__ hist, int64_t n_chunks, int64_t E,
                               int32_t* __restrict__ counts) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int32_t run = 0;
-    for (int64_t c = 0; c < n_chunks; ++c) {
-      int32_t v = hist[c * E + e];
-      hist[c * E + e] = run;
-      run += v;
+  const int lane = threadIdx.x & 31;
+  const int64_t e = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (e >= E) return;
+  int32_t carry = 0;
+  for (int64_t c0 = 0; c0 < n_chunks; c0 += 32) {
+    const int64_t c = c0 + lane;
+    const int32_t v = c < n_chunks ? hist[c * E + e] : 0;
+    int32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    counts[e] = run;
+    if (c < n_chunks) hist[c * E + e] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
   }
+  if (lane == 0) counts[e] = carry;
 }
 
 // block-wide exclusive scan helper (1024 threads), returns exclusive prefix and total
@@ -152,7 +168,8 @@ k_scan_experts(const int32_t* __restrict__ counts, int64_t E, int32_t* __restric
 __global__ void __launch_bounds__(kDispWarps * 32)
 k_rank(const int32_t* __restrict__ sel, const uint32_t* __restrict__ responded, int64_t T, int k,
        int64_t E, int32_t* __restrict__ hist, const int32_t* __restrict__ offsets,
-       int32_t* __restrict__ row_of_slot, int32_t* __restrict__ token_of_row, int64_t n_chunks) {
+       int32_t* __restrict__ row_of_slot, int32_t* __restrict__ token_of_row, int64_t n_chunks,
+       int64_t kChunkTok) {
   const int lane = threadIdx.x & 31;
   const int64_t c = blockIdx.x * (int64_t)kDispWarps + (threadIdx.x >> 5);
   if (c >= n_chunks) return;
@@ -203,7 +220,7 @@ __global__ void k_gather(const T* __restrict__ x, const int32_t* __restrict__ to
 }
 
 size_t dispatch_ws_bytes(int64_t T, int64_t E) {
-  int64_t nc = ceil_div(T, kChunkTok);
+  int64_t nc = ceil_div(T, chunk_tokens(T, E));
   return align_up((size_t)nc * E * 4, 256) + align_up((size_t)nc * 4, 256) + 1024;
 }
 
@@ -213,6 +230,7 @@ dmoe_status dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, int64_t
                      int32_t* offsets, int32_t* row_of_slot, int32_t* token_of_row, void* xd,
                      int32_t* plan128, int32_t* plan64, void* ws, size_t ws_bytes,
                      cudaStream_t s) {
+  const int64_t kChunkTok = chunk_tokens(T, E);
   const int64_t nc = ceil_div(T, kChunkTok);
   Carver cv(ws, ws_bytes);
   int32_t* hist = cv.take<int32_t>((size_t)(nc > 0 ? nc : 1) * E);
@@ -221,16 +239,16 @@ dmoe_status dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, int64_t
   const unsigned blocks = (unsigned)ceil_div(nc, kDispWarps);
   if (nc > 0) {
     k_weights_hist<<<blocks, kDispWarps * 32, 0, s>>>(sel, sel_score, responded, T, k, E, w, valid,
-                                                       hist, cdrop, nc);
+                                                       hist, cdrop, nc, kChunkTok);
     DMOE_TRY(check_launch("dispatch.weights_hist"));
   }
-  k_scan_chunks<<<(unsigned)ceil_div(E, 256), 256, 0, s>>>(hist, nc, E, counts);
+  k_scan_chunks<<<(unsigned)ceil_div(E, 8), 256, 0, s>>>(hist, nc, E, counts);
   DMOE_TRY(check_launch("dispatch.scan_chunks"));
   k_scan_experts<<<1, 1024, 0, s>>>(counts, E, offsets, plan128, plan64, cdrop, nc, n_dropped);
   DMOE_TRY(check_launch("dispatch.scan_experts"));
   if (nc > 0) {
     k_rank<<<blocks, kDispWarps * 32, 0, s>>>(sel, responded, T, k, E, hist, offsets, row_of_slot,
-                                              token_of_row, nc);
+                                              token_of_row, nc, kChunkTok);
     DMOE_TRY(check_launch("dispatch.rank"));
     const int grid = num_sms() * 8;
     if (dt == DMOE_BF16)

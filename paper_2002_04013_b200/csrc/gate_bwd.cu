@@ -28,6 +28,16 @@ __global__ void k_transpose(const T* __restrict__ src, int64_t rows, int64_t col
   }
 }
 
+dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt, void* dst,
+                      cudaStream_t s) {
+  dim3 tb(32, 8), tg((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
+  if (dt == DMOE_BF16)
+    k_transpose<__nv_bfloat16><<<tg, tb, 0, s>>>((const __nv_bfloat16*)src, rows, cols, (__nv_bfloat16*)dst);
+  else
+    k_transpose<float><<<tg, tb, 0, s>>>((const float*)src, rows, cols, (float*)dst);
+  return check_launch("transpose");
+}
+
 constexpr int kGbWarps = 8;
 constexpr int kGbMaxK = 16;
 
@@ -155,20 +165,17 @@ __global__ void k_dwg_reduce(const float* __restrict__ partial, const float* __r
   }
 }
 
-constexpr int64_t kMaxSplits = 2 * kNumSMs;
-
+// split-K over tokens: >= 64 tokens per split, partial sums capped at 8M floats
 static int64_t dwg_splits(int64_t T, int32_t D, int dM) {
-  const int64_t tiles = ceil_div(D, 64) * ceil_div(dM, 32);
-  int64_t s = ceil_div(kMaxSplits, tiles);
-  const int64_t maxs = ceil_div(T, 256);
-  if (s > maxs) s = maxs;
+  int64_t smax = ((int64_t)8 << 20) / ((int64_t)D * dM);
+  if (smax < 1) smax = 1;
+  int64_t s = ceil_div(T, 64);
+  if (s > smax) s = smax;
   return s < 1 ? 1 : s;
 }
 
 size_t gate_bwd_ws_bytes(int64_t T, int32_t D, int dM) {
-  int64_t S = ceil_div(T, 256);
-  if (S > kMaxSplits) S = kMaxSplits;
-  if (S < 1) S = 1;
+  const int64_t S = dwg_splits(T, D, dM);
   return align_up((size_t)D * dM * 4, 256) + align_up((size_t)(T > 0 ? T : 1) * dM * 4, 256) +
          align_up((size_t)S * D * dM * 4, 256) + align_up((size_t)S * dM * 4, 256) + 1024;
 }

@@ -138,15 +138,41 @@ k_simt_segk(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
 }
 
 // segment column sums: out[e][n] = sum_{r in seg e} X[r][n] (fp32, row order) — db1 / db2
+// Each thread owns one 16-byte column vector; rows are walked in order with 4 loads in
+// flight (the sum order is fixed: row order, so the result is deterministic).
 template <typename T>
 __global__ void k_seg_colsum(const T* __restrict__ X, const int32_t* __restrict__ offsets, int N,
                              float* __restrict__ out) {
+  constexpr int V = Vec16<T>::N;
   const int e = blockIdx.y;
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * V;
   if (n >= N) return;
-  float v = 0.0f;
-  for (int64_t r = offsets[e]; r < offsets[e + 1]; ++r) v += Elem<T>::load(X + r * N + n);
-  out[(int64_t)e * N + n] = v;
+  float acc[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) acc[i] = 0.0f;
+  const int64_t r0 = offsets[e], r1 = offsets[e + 1];
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    uint4 u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) u[j] = ld_nc_v4(X + (r + j) * N + n);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float f[V];
+      unpack16(u[j], f, (const T*)nullptr);
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc[i] += f[i];
+    }
+  }
+  for (; r < r1; ++r) {
+    float f[V];
+    unpack16(ld_nc_v4(X + r * N + n), f, (const T*)nullptr);
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] += f[i];
+  }
+  float* o = out + (int64_t)e * N + n;
+#pragma unroll
+  for (int i = 0; i < V; ++i) o[i] = acc[i];
 }
 
 template <typename T, typename TC>
@@ -195,11 +221,13 @@ dmoe_status simt_gemm_segk(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
 
 dmoe_status seg_colsum(const void* X, dmoe_dtype dt, const int32_t* offsets, int E, int N,
                        float* out, cudaStream_t s) {
-  dim3 grid((unsigned)ceil_div(N, 256), (unsigned)E);
+  const int V = dt == DMOE_BF16 ? 8 : 4;  // N % V == 0 is validated by the caller
+  const int threads = (int)(N / V < 128 ? N / V : 128);
+  dim3 grid((unsigned)ceil_div(N / V, threads), (unsigned)E);
   if (dt == DMOE_BF16)
-    k_seg_colsum<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, offsets, N, out);
+    k_seg_colsum<__nv_bfloat16><<<grid, threads, 0, s>>>((const __nv_bfloat16*)X, offsets, N, out);
   else
-    k_seg_colsum<float><<<grid, 256, 0, s>>>((const float*)X, offsets, N, out);
+    k_seg_colsum<float><<<grid, threads, 0, s>>>((const float*)X, offsets, N, out);
   return check_launch("seg_colsum");
 }
 

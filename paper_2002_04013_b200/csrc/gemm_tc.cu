@@ -28,7 +28,7 @@ namespace dmoe {
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 64;  // one 128-byte swizzle atom of bf16
-constexpr int TC_THREADS = 256;
+
 
 // --------------------------------------------------------------------- PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -126,6 +126,15 @@ __host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn) 
          | ((uint32_t)(TC_BM >> 4) << 24);  // M >> 4
 }
 
+#define TMEM_LD16(taddr, r)                                                                     \
+  asm volatile(                                                                                 \
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13," \
+      "%14,%15}, [%16];"                                                                        \
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),    \
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), \
+        "=r"(r[14]), "=r"(r[15])                                                               \
+      : "r"(taddr))
+
 // ------------------------------------------------------------------------- kernel
 struct TcParams {
   const int32_t* offsets;  // [E+1] or nullptr (single group of rows_single rows)
@@ -137,22 +146,38 @@ struct TcParams {
   int64_t rows_single;
 };
 
+constexpr int TC_SMEM_MAX = 227 * 1024;
+constexpr int TC_STAGE_ROW = 144;              // staging row pitch: 128 B of data + 16 B pad
+constexpr int TC_STAGE_WARP = 32 * TC_STAGE_ROW;  // one warp's 32-row staging tile
+
 template <int BN> struct TcCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : 6;
-  static constexpr int A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
-  static constexpr int B_BYTES = BN * TC_BK * 2;      // 16/32 KB
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = 2 * BN;            // two accumulators
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
+  static constexpr int EPI_WARPS = (BN >= 128) ? 8 : 4;   // 2 column halves when wide
+  static constexpr int EPI_COLS = BN / (EPI_WARPS / 4);   // columns per epilogue warp
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int A_BYTES = TC_BM * TC_BK * 2;       // 16 KB
+  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
+  static constexpr int FIXED = 1024 /*align*/ + 512 /*barriers*/ + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2;
+  static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
+  static constexpr int STAGES = ST > 8 ? 8 : ST;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
 };
 
+// bf16 h > 0  <=>  sign bit clear and not +0
+__device__ __forceinline__ bool bf16_pos(uint32_t b) { return b != 0 && !(b & 0x8000u); }
+
 template <int BN, bool SEGK, bool B_MN, int EPI>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TcCfg<BN>::THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const TcParams p) {
   using Cfg = TcCfg<BN>;
   constexpr int S = Cfg::STAGES;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
+  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
+  constexpr int OUT_ES = OUT_F32 ? 4 : 2;
+  constexpr int SUB = 128 / OUT_ES;  // columns per staged sub-tile (128 bytes per row)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + S * Cfg::STAGE_BYTES);
@@ -160,11 +185,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 512;
+  float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * TC_STAGE_WARP);  // [2][BN]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // ---- tile space (identical walk in every role)
-  const int NT = p.N / BN;
+  const int NT = (p.N + BN - 1) / BN;
   const int MT = SEGK ? p.Mdim / TC_BM : 0;
   int total;
   if (SEGK) total = p.E * MT * NT;
@@ -177,7 +204,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
   if (warp == 1 && lane == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], Cfg::EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -190,7 +217,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // decode a tile -> (group e, row0 / m0, n0, row_end, number of K blocks)
+  // decode a tile -> (group e, row0, row_end, m0, n0, number of K blocks)
   auto decode = [&](int tile, int& e, int64_t& row0, int64_t& row_end, int& m0, int& n0, int& nkb) {
     if (SEGK) {
       e = tile / (MT * NT);
@@ -308,98 +335,138 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
   } else if (warp >= 4) {
     // ======================= epilogue =======================
-    const int q = warp & 3;  // TMEM lanes 32q .. 32q+31
+    // warp -> TMEM lane quadrant q (rows 32q..32q+31) and column range [c_beg, c_beg+EPI_COLS).
+    // Each 128-byte-wide sub-tile goes TMEM -> registers -> (bias/ReLU/mask) -> padded smem
+    // staging -> coalesced 16-byte stores, 4 full rows (512 B) per warp instruction.
+    const int ew = warp - 4;
+    const int q = warp & 3;
+    const int c_beg = (ew >> 2) * Cfg::EPI_COLS;
+    uint8_t* stg = stage_base + ew * TC_STAGE_WARP;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int bias_buf = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       int e, m0, n0, nkb;
       int64_t row0, row_end;
       decode(tile, e, row0, row_end, m0, n0, nkb);
-      const int rloc = q * 32 + lane;
-      if (SEGK) {
-        __nv_bfloat16* C = (__nv_bfloat16*)p.C + ((int64_t)e * p.Mdim + m0 + rloc) * p.N + n0;
-        if (nkb == 0) {
-          for (int c = 0; c < BN; c += 8) *reinterpret_cast<uint4*>(C + c) = make_uint4(0, 0, 0, 0);
-          continue;
-        }
+      const bool has_acc = !(SEGK && nkb == 0);
+      // stage this tile's bias slice (double-buffered across tiles; one named barrier)
+      constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
+      float* bias_t = bias_s + bias_buf * BN;
+      if (HAS_BIAS) {
+        for (int c = threadIdx.x - 128; c < BN; c += 32 * Cfg::EPI_WARPS)
+          bias_t[c] = (n0 + c < p.N) ? p.bias[(int64_t)e * p.N + n0 + c] : 0.0f;
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * Cfg::EPI_WARPS) : "memory");
+        bias_buf ^= 1;
+      }
+      if (has_acc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          TMEM_LD32(taddr + c, r);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      }
+      // rows of this warp's quadrant: global row (ROWS) or output row m (SEGK)
+      const int64_t qrow0 = SEGK ? (int64_t)(m0 + q * 32) : row0 + q * 32;
+      int64_t live_rows;
+      if (SEGK) live_rows = 32;
+      else {
+        const int64_t left = row_end - qrow0;
+        live_rows = left < 0 ? 0 : (left > 32 ? 32 : left);
+      }
+      const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      for (int cs = c_beg; cs < c_beg + Cfg::EPI_COLS; cs += SUB) {
+        const int ncols = (c_beg + Cfg::EPI_COLS - cs) < SUB ? (c_beg + Cfg::EPI_COLS - cs) : SUB;  // multiple of 16
+        // (optional) ReLU-mask source rows -> staging, coalesced
+        uint32_t hmask[SUB / 32 + 1];
+        if (EPI == EPI_RELU_MASK) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 8) {
-            uint4 v = make_uint4(pack_bf16x2(__uint_as_float(r[j]), __uint_as_float(r[j + 1])),
-                                 pack_bf16x2(__uint_as_float(r[j + 2]), __uint_as_float(r[j + 3])),
-                                 pack_bf16x2(__uint_as_float(r[j + 4]), __uint_as_float(r[j + 5])),
-                                 pack_bf16x2(__uint_as_float(r[j + 6]), __uint_as_float(r[j + 7])));
-            *reinterpret_cast<uint4*>(C + c + j) = v;
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + (lane >> 3), piece = lane & 7;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (r < live_rows && piece * 8 < ncols)
+              v = *reinterpret_cast<const uint4*>(p.aux + (qrow0 + r) * p.N + n0 + cs + piece * 8);
+            *reinterpret_cast<uint4*>(stg + r * TC_STAGE_ROW + piece * 16) = v;
           }
-        }
-      } else {
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        const int64_t row = row0 + rloc;
-        const bool live = row < row_end;
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-        const float* bias = p.bias ? p.bias + (int64_t)e * p.N + n0 : nullptr;
-#pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t r[32];
-          TMEM_LD32(taddr + c, r);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (!live) continue;
-          float v[32];
+          __syncwarp();
+          // this lane's row: one bit per column, 1 = h > 0
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-          if (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU) {
+          for (int j = 0; j < SUB / 32 + 1; ++j) hmask[j] = 0;
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              const float4 b = __ldg(reinterpret_cast<const float4*>(bias + c + j));
-              v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
+          for (int piece = 0; piece < 8; ++piece) {
+            const uint4 hv = *reinterpret_cast<const uint4*>(stg + lane * TC_STAGE_ROW + piece * 16);
+            const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int col = piece * 8 + 2 * i;
+              if (bf16_pos(hw[i] & 0xFFFFu)) hmask[col >> 5] |= 1u << (col & 31);
+              if (bf16_pos(hw[i] >> 16)) hmask[(col + 1) >> 5] |= 1u << ((col + 1) & 31);
             }
+          }
+          __syncwarp();
+        }
+        // TMEM -> registers -> epilogue math -> staging (row = lane)
+        for (int c16 = 0; c16 < ncols; c16 += 16) {
+          float v[16];
+          if (has_acc) {
+            uint32_t r[16];
+            TMEM_LD16(tq + cs + c16, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = 0.0f;
+          }
+          if (HAS_BIAS) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] += bias_t[cs + c16 + j];
           }
           if (EPI == EPI_BIAS_RELU) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.0f);
+            for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.0f);
           }
           if (EPI == EPI_RELU_MASK) {
-            const __nv_bfloat16* hrow = p.aux + row * p.N + n0 + c;
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              const uint4 hv = *reinterpret_cast<const uint4*>(hrow + j);
-              const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                // bf16 h > 0  <=>  sign bit clear and not +0
-                const uint32_t lo = hw[i] & 0xFFFFu, hi = hw[i] >> 16;
-                if (!(lo != 0 && !(lo & 0x8000u))) v[j + 2 * i] = 0.0f;
-                if (!(hi != 0 && !(hi & 0x8000u))) v[j + 2 * i + 1] = 0.0f;
-              }
+            for (int j = 0; j < 16; ++j) {
+              const int col = c16 + j;
+              if (!((hmask[col >> 5] >> (col & 31)) & 1u)) v[j] = 0.0f;
             }
           }
-          if (EPI == EPI_F32_BIAS) {
-            float* C = (float*)p.C + row * p.N + n0 + c;
+          uint8_t* dst = stg + lane * TC_STAGE_ROW + c16 * OUT_ES;
+          if (OUT_F32) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4)
-              *reinterpret_cast<float4*>(C + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            for (int j = 0; j < 16; j += 4)
+              *reinterpret_cast<float4*>(dst + j * 4) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
           } else {
-            __nv_bfloat16* C = (__nv_bfloat16*)p.C + row * p.N + n0 + c;
 #pragma unroll
-            for (int j = 0; j < 32; j += 8)
-              *reinterpret_cast<uint4*>(C + j) =
+            for (int j = 0; j < 16; j += 8)
+              *reinterpret_cast<uint4*>(dst + j * 2) =
                   make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
                              pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
           }
         }
+        __syncwarp();
+        // staging -> global: lane (r = i*4 + lane/8, piece = lane%8) -> 4 full rows per instruction
+        const int row_bytes = ncols * OUT_ES;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 4 + (lane >> 3), piece = lane & 7;
+          if (r < live_rows && piece * 16 < row_bytes) {
+            const uint4 v = *reinterpret_cast<const uint4*>(stg + r * TC_STAGE_ROW + piece * 16);
+            uint8_t* gdst;
+            if (SEGK)
+              gdst = (uint8_t*)p.C + (((int64_t)e * p.Mdim + qrow0 + r) * p.N + n0 + cs) * OUT_ES + piece * 16;
+            else
+              gdst = (uint8_t*)p.C + ((qrow0 + r) * p.N + n0 + cs) * OUT_ES + piece * 16;
+            *reinterpret_cast<uint4*>(gdst) = v;
+          }
+        }
+        __syncwarp();
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (has_acc) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
     }
   }
 
@@ -445,11 +512,18 @@ static dmoe_status make_map(CUtensorMap* m, const void* ptr, int rank, const uin
   return DMOE_OK;
 }
 
-static int pick_bn(int N) { return (N % 256 == 0) ? 256 : 128; }
+// N tile: 256 when it divides N, else 128; K-major B also takes any N = 16..256 in one tile
+// (the gate, N = d*M) and MN-major B any multiple of 64 up to 256.
+static int pick_bn(int N, bool b_mn) {
+  if (N % 256 == 0) return 256;
+  if (N % 128 == 0) return 128;
+  if (N <= 256 && (b_mn ? N % 64 == 0 : N % 16 == 0)) return N;
+  return 0;
+}
 
 bool tc_rows_supported(const GemmRows& g) {
   if (g.K % TC_BK != 0 || g.K <= 0) return false;
-  if (g.N % 128 != 0) return false;
+  if (pick_bn(g.N, g.b_mn) == 0) return false;
   if (g.epi == EPI_F32_BIAS && g.offsets != nullptr) return false;
   if (encode_fn() == nullptr) return false;
   return true;
@@ -470,7 +544,7 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcPa
   }
   int64_t grid = max_tiles < num_sms() ? max_tiles : num_sms();
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, TC_THREADS, smem, s>>>(a, b, p);
+  kern<<<(unsigned)grid, TcCfg<BN>::THREADS, smem, s>>>(a, b, p);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
 }
@@ -487,14 +561,17 @@ static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtens
     case EPI_RELU_MASK: DMOE_TC_ROWS(BMN, EPI_RELU_MASK);  \
     default: DMOE_TC_ROWS(BMN, EPI_PLAIN);                 \
   }
-  if (g.b_mn) { DMOE_TC_EPI(true) } else { DMOE_TC_EPI(false) }
+  if constexpr (BN % 64 == 0) {
+    if (g.b_mn) { DMOE_TC_EPI(true) }
+  }
+  DMOE_TC_EPI(false)
 #undef DMOE_TC_EPI
 #undef DMOE_TC_ROWS
 }
 
 dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
   if (g.max_tiles <= 0) return DMOE_OK;
-  const int BN = pick_bn(g.N);
+  const int BN = pick_bn(g.N, g.b_mn);
   // A: [rows_cap, K] K-major; rows past the extent are zero-filled by TMA, rows past a
   // segment produce accumulator rows the epilogue never stores.
   CUtensorMap ta, tb;
@@ -510,13 +587,22 @@ dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
   TcParams p{};
   p.offsets = g.offsets; p.plan = g.plan; p.bias = g.bias; p.aux = (const __nv_bfloat16*)g.aux;
   p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
-  const int64_t tiles = g.max_tiles * (g.N / BN);
-  if (BN == 256) return rows_bn<256>(g, ta, tb, p, tiles, s);
-  return rows_bn<128>(g, ta, tb, p, tiles, s);
+  const int64_t tiles = g.max_tiles * ((g.N + BN - 1) / BN);
+  switch (BN) {
+    case 256: return rows_bn<256>(g, ta, tb, p, tiles, s);
+    case 128: return rows_bn<128>(g, ta, tb, p, tiles, s);
+    case 64: return rows_bn<64>(g, ta, tb, p, tiles, s);
+    case 192: return rows_bn<192>(g, ta, tb, p, tiles, s);
+    case 32: return rows_bn<32>(g, ta, tb, p, tiles, s);
+    case 48: return rows_bn<48>(g, ta, tb, p, tiles, s);
+    case 96: return rows_bn<96>(g, ta, tb, p, tiles, s);
+    case 16: return rows_bn<16>(g, ta, tb, p, tiles, s);
+    default: return set_error(DMOE_ERR_UNSUPPORTED, "tc_gemm_rows: N=%d", g.N);
+  }
 }
 
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
-  const int BN = pick_bn(g.N);
+  const int BN = pick_bn(g.N, true);
   CUtensorMap ta, tb;
   // K rows past a segment end (other experts' rows, or capacity rows past R) are zeroed
   // in smem before the MMA; rows past R_cap are zero-filled by TMA.

@@ -65,7 +65,7 @@ class DMoELayer:
         T = x.shape[0]
         assert T <= self.T_max and x.dtype == self.dtype and x.shape[1] == self.D
         self._x = x
-        L.dmoe_gate_scores(x, self.Wg, self.bg, self.g, self.G[:T])
+        L.dmoe_gate_scores(x, self.Wg, self.bg, self.g, self.G[:T], self.ws)
         L.dmoe_beam_topk(self.G[:T], self.g, alive_bits, self.sel[:T], self.sel_score[:T], self.ws)
         L.dmoe_dispatch(x, self.g, self.sel[:T], self.sel_score[:T], responded_bits, self.w[:T], self.valid[:T],
                         self.n_dropped, self.counts, self.offsets, self.row_of_slot[:T], self.token_of_row,

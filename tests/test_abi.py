@@ -37,10 +37,10 @@ def test_validation_errors_without_gpu():
     import paper_2002_04013_b200 as P
     from paper_2002_04013_b200 import _lib as L
     g = P.grid(2, 4, 4)
-    assert L._L.dmoe_gate_scores(None, 1, 8, 64, None, None, L.grid(5, 4, 4), None, None) == -2   # d > 4
-    assert L._L.dmoe_gate_scores(None, 1, 8, 64, None, None, L.grid(2, 4, 17), None, None) == -2  # k > 16
-    assert L._L.dmoe_gate_scores(None, 1, 8, 60, None, None, g, None, None) == -2                  # D % 8
-    assert L._L.dmoe_gate_scores(None, 7, 8, 64, None, None, g, None, None) == -1                  # dtype
-    assert L._L.dmoe_gate_scores(None, 1, 8, 64, None, None, g, None, None) == -1                  # null
+    assert L._L.dmoe_gate_scores(None, 1, 8, 64, None, None, L.grid(5, 4, 4), None, None, 0, None) == -2   # d > 4
+    assert L._L.dmoe_gate_scores(None, 1, 8, 64, None, None, L.grid(2, 4, 17), None, None, 0, None) == -2  # k > 16
+    assert L._L.dmoe_gate_scores(None, 1, 8, 60, None, None, g, None, None, 0, None) == -2                  # D % 8
+    assert L._L.dmoe_gate_scores(None, 7, 8, 64, None, None, g, None, None, 0, None) == -1                  # dtype
+    assert L._L.dmoe_gate_scores(None, 1, 8, 64, None, None, g, None, None, 0, None) == -1                  # null
     assert b"null pointer" in L._L.dmoe_last_error()
     assert P.dmoe_workspace_bytes(4096, 256, 1024, g, 16, 16384) > 16384 * 1024 * 2

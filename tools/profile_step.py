@@ -1,0 +1,24 @@
+"""Run W eager layer steps of a workload (for ncu captures: the last step's kernels are the
+ones to profile; every kernel of a step launches once per step)."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from gen import CONFIGS  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="mnist")
+ap.add_argument("--steps", type=int, default=3)
+a = ap.parse_args()
+cfg = CONFIGS[a.config]
+lay, x, dy, alive, resp = bench.build_layer(cfg, 0, torch.device("cuda", 0), cfg.T)
+for _ in range(a.steps):
+    bench.run_calls(lay, x, dy, alive, resp)
+torch.cuda.synchronize()
+print("ok")
