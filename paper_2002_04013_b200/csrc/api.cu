@@ -97,6 +97,16 @@ static dmoe_status segk_gemm(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
 }
 constexpr int kPlanBM_TC = 128, kPlanBM_SIMT = 64;
 
+// row-tile plans only for the engines the two GEMMs of a call will use
+static dmoe_status plans_for(const GemmRows& a, const GemmRows& b, const int32_t* offsets, int E,
+                             int32_t* plan_tc, int32_t* plan_simt, cudaStream_t s) {
+  const bool need_tc = a.plan == plan_tc || b.plan == plan_tc;
+  const bool need_simt = a.plan == plan_simt || b.plan == plan_simt;
+  if (need_tc) DMOE_TRY(tile_plan(offsets, E, kPlanBM_TC, plan_tc, s));
+  if (need_simt) DMOE_TRY(tile_plan(offsets, E, kPlanBM_SIMT, plan_simt, s));
+  return DMOE_OK;
+}
+
 }  // namespace dmoe
 
 using namespace dmoe;
@@ -210,8 +220,7 @@ dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t 
     g->plan = tc ? plan_tc : plan_simt;
     g->max_tiles = ceil_div(R_cap, bm) + E_local;
   }
-  DMOE_TRY(tile_plan(offsets, E_local, kPlanBM_TC, plan_tc, s));
-  DMOE_TRY(tile_plan(offsets, E_local, kPlanBM_SIMT, plan_simt, s));
+  DMOE_TRY(plans_for(g1, g2, offsets, E_local, plan_tc, plan_simt, s));
   DMOE_TRY(rows_gemm(g1, dt, s));
   return rows_gemm(g2, dt, s);
 }
@@ -263,8 +272,7 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
     g->plan = tc ? plan_tc : plan_simt;
     g->max_tiles = ceil_div(R_cap, bm) + E_local;
   }
-  DMOE_TRY(tile_plan(offsets, E_local, kPlanBM_TC, plan_tc, s));
-  DMOE_TRY(tile_plan(offsets, E_local, kPlanBM_SIMT, plan_simt, s));
+  DMOE_TRY(plans_for(g3, g4, offsets, E_local, plan_tc, plan_simt, s));
   DMOE_TRY(rows_gemm(g3, dt, s));
   DMOE_TRY(rows_gemm(g4, dt, s));
   // dW2_e = dout^T h;  dW1_e = dh^T xd;  db2 / db1 = segment column sums

@@ -138,41 +138,52 @@ k_simt_segk(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
 }
 
 // segment column sums: out[e][n] = sum_{r in seg e} X[r][n] (fp32, row order) — db1 / db2
-// Each thread owns one 16-byte column vector; rows are walked in order with 4 loads in
-// flight (the sum order is fixed: row order, so the result is deterministic).
+// Block = 8 warps over one expert and a 32-vector column strip; warp w sums rows
+// r0+w, r0+w+8, ... (2 loads in flight), then the 8 partials are added in warp order
+// (fixed order -> deterministic).
+constexpr int kCsWarps = 8;
 template <typename T>
-__global__ void k_seg_colsum(const T* __restrict__ X, const int32_t* __restrict__ offsets, int N,
-                             float* __restrict__ out) {
+__global__ void __launch_bounds__(kCsWarps * 32)
+k_seg_colsum(const T* __restrict__ X, const int32_t* __restrict__ offsets, int N,
+             float* __restrict__ out) {
   constexpr int V = Vec16<T>::N;
+  __shared__ float part[kCsWarps][32 * V + 1];
   const int e = blockIdx.y;
-  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * V;
-  if (n >= N) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = (blockIdx.x * 32 + lane) * V;
   float acc[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) acc[i] = 0.0f;
   const int64_t r0 = offsets[e], r1 = offsets[e + 1];
-  int64_t r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    uint4 u[4];
+  if (n < N) {
+    int64_t r = r0 + warp;
+    for (; r + kCsWarps < r1; r += 2 * kCsWarps) {
+      const uint4 u0 = ld_nc_v4(X + r * N + n);
+      const uint4 u1 = ld_nc_v4(X + (r + kCsWarps) * N + n);
+      float f0[V], f1[V];
+      unpack16(u0, f0, (const T*)nullptr);
+      unpack16(u1, f1, (const T*)nullptr);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) u[j] = ld_nc_v4(X + (r + j) * N + n);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
+      for (int i = 0; i < V; ++i) acc[i] += f0[i] + f1[i];
+    }
+    if (r < r1) {
       float f[V];
-      unpack16(u[j], f, (const T*)nullptr);
+      unpack16(ld_nc_v4(X + r * N + n), f, (const T*)nullptr);
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[i] += f[i];
     }
   }
-  for (; r < r1; ++r) {
-    float f[V];
-    unpack16(ld_nc_v4(X + r * N + n), f, (const T*)nullptr);
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc[i] += f[i];
+  for (int i = 0; i < V; ++i) part[warp][lane * V + i] = acc[i];
+  __syncthreads();
+  for (int c = threadIdx.x; c < 32 * V; c += kCsWarps * 32) {
+    const int col = blockIdx.x * 32 * V + c;
+    if (col >= N) continue;
+    float v = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kCsWarps; ++w) v += part[w][c];
+    out[(int64_t)e * N + col] = v;
   }
-  float* o = out + (int64_t)e * N + n;
-#pragma unroll
-  for (int i = 0; i < V; ++i) o[i] = acc[i];
 }
 
 template <typename T, typename TC>
@@ -222,12 +233,11 @@ dmoe_status simt_gemm_segk(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
 dmoe_status seg_colsum(const void* X, dmoe_dtype dt, const int32_t* offsets, int E, int N,
                        float* out, cudaStream_t s) {
   const int V = dt == DMOE_BF16 ? 8 : 4;  // N % V == 0 is validated by the caller
-  const int threads = (int)(N / V < 128 ? N / V : 128);
-  dim3 grid((unsigned)ceil_div(N / V, threads), (unsigned)E);
+  dim3 grid((unsigned)ceil_div(N, 32 * V), (unsigned)E);
   if (dt == DMOE_BF16)
-    k_seg_colsum<__nv_bfloat16><<<grid, threads, 0, s>>>((const __nv_bfloat16*)X, offsets, N, out);
+    k_seg_colsum<__nv_bfloat16><<<grid, kCsWarps * 32, 0, s>>>((const __nv_bfloat16*)X, offsets, N, out);
   else
-    k_seg_colsum<float><<<grid, threads, 0, s>>>((const float*)X, offsets, N, out);
+    k_seg_colsum<float><<<grid, kCsWarps * 32, 0, s>>>((const float*)X, offsets, N, out);
   return check_launch("seg_colsum");
 }
 

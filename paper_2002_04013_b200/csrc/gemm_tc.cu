@@ -359,10 +359,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         asm volatile("bar.sync 1, %0;" ::"n"(32 * Cfg::EPI_WARPS) : "memory");
         bias_buf ^= 1;
       }
-      if (has_acc) {
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-      }
       // rows of this warp's quadrant: global row (ROWS) or output row m (SEGK)
       const int64_t qrow0 = SEGK ? (int64_t)(m0 + q * 32) : row0 + q * 32;
       int64_t live_rows;
@@ -372,23 +368,39 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         live_rows = left < 0 ? 0 : (left > 32 ? 32 : left);
       }
       const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-      for (int cs = c_beg; cs < c_beg + Cfg::EPI_COLS; cs += SUB) {
+      // ReLU-mask source (h) for this warp's 32 rows x EPI_COLS columns: issue the coalesced
+      // loads before waiting for the accumulator so their latency hides behind the MMA
+      constexpr int NSUB = (Cfg::EPI_COLS + SUB - 1) / SUB;
+      uint4 hreg[EPI == EPI_RELU_MASK ? NSUB : 1][8];
+      if (EPI == EPI_RELU_MASK) {
+#pragma unroll
+        for (int sb = 0; sb < NSUB; ++sb)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + (lane >> 3), piece = lane & 7;
+            const int cs = c_beg + sb * SUB;
+            hreg[sb][i] = make_uint4(0, 0, 0, 0);
+            if (r < live_rows && cs + piece * 8 < c_beg + Cfg::EPI_COLS)
+              hreg[sb][i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (qrow0 + r) * p.N + n0 + cs + piece * 8));
+          }
+      }
+      if (has_acc) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+      }
+#pragma unroll
+      for (int sb = 0; sb < NSUB; ++sb) {
+        const int cs = c_beg + sb * SUB;
         const int ncols = (c_beg + Cfg::EPI_COLS - cs) < SUB ? (c_beg + Cfg::EPI_COLS - cs) : SUB;  // multiple of 16
-        // (optional) ReLU-mask source rows -> staging, coalesced
-        uint32_t hmask[SUB / 32 + 1];
+        uint32_t hmask[SUB / 32] = {};
         if (EPI == EPI_RELU_MASK) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), piece = lane & 7;
-            uint4 v = make_uint4(0, 0, 0, 0);
-            if (r < live_rows && piece * 8 < ncols)
-              v = *reinterpret_cast<const uint4*>(p.aux + (qrow0 + r) * p.N + n0 + cs + piece * 8);
-            *reinterpret_cast<uint4*>(stg + r * TC_STAGE_ROW + piece * 16) = v;
+            *reinterpret_cast<uint4*>(stg + r * TC_STAGE_ROW + piece * 16) = hreg[sb][i];
           }
           __syncwarp();
           // this lane's row: one bit per column, 1 = h > 0
-#pragma unroll
-          for (int j = 0; j < SUB / 32 + 1; ++j) hmask[j] = 0;
 #pragma unroll
           for (int piece = 0; piece < 8; ++piece) {
             const uint4 hv = *reinterpret_cast<const uint4*>(stg + lane * TC_STAGE_ROW + piece * 16);
@@ -403,7 +415,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           __syncwarp();
         }
         // TMEM -> registers -> epilogue math -> staging (row = lane)
-        for (int c16 = 0; c16 < ncols; c16 += 16) {
+#pragma unroll
+        for (int c16 = 0; c16 < SUB; c16 += 16) {
+          if (c16 >= ncols) break;
           float v[16];
           if (has_acc) {
             uint32_t r[16];
