@@ -21,6 +21,7 @@
 // MN-major (weights in the backward-dx GEMMs, both operands of the weight-gradient
 // GEMMs); the UMMA descriptors encode either, so no transposed copy is ever made.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "gemm.cuh"
 
@@ -144,11 +145,13 @@ struct TcParams {
   void* C;
   int E, N, K, Mdim;
   int64_t rows_single;
+  int dbg;  // experiment switches (env DMOE_TC_DEBUG): 1 skip stores, 2 skip TMEM loads, 4 skip MMAs
 };
 
 constexpr int TC_SMEM_MAX = 227 * 1024;
 constexpr int TC_STAGE_ROW = 144;              // staging row pitch: 128 B of data + 16 B pad
 constexpr int TC_STAGE_WARP = 32 * TC_STAGE_ROW;  // one warp's 32-row staging tile
+constexpr int TC_TABLE_E = 4096;                  // experts whose offsets/plan live in smem
 
 template <int BN> struct TcCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
@@ -158,7 +161,8 @@ template <int BN> struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;       // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
-  static constexpr int FIXED = 1024 /*align*/ + 512 /*barriers*/ + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2;
+  static constexpr int FIXED = 1024 /*align*/ + 512 /*barriers*/ + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2 +
+                               2 * (TC_TABLE_E + 1) * 4 /*offsets + plan tables*/;
   static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = ST > 8 ? 8 : ST;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -187,15 +191,29 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 512;
   float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * TC_STAGE_WARP);  // [2][BN]
+  int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [E+1]
+  int32_t* plan_s = off_s + (TC_TABLE_E + 1);                               // [E+1]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- per-expert tables in smem (every role decodes every tile: keep it off the L2 path)
+  const int32_t* offs = p.offsets;
+  const int32_t* plan = p.plan;
+  if (p.offsets && p.E <= TC_TABLE_E) {
+    for (int i = threadIdx.x; i <= p.E; i += blockDim.x) {
+      off_s[i] = p.offsets[i];
+      if (!SEGK) plan_s[i] = p.plan[i];
+    }
+    offs = off_s;
+    plan = plan_s;
+  }
 
   // ---- tile space (identical walk in every role)
   const int NT = (p.N + BN - 1) / BN;
   const int MT = SEGK ? p.Mdim / TC_BM : 0;
   int total;
   if (SEGK) total = p.E * MT * NT;
-  else if (p.offsets) total = p.plan[p.E] * NT;
+  else if (p.offsets) total = p.plan[p.E] * NT;  // (global read: tables are not yet visible)
   else total = (int)((p.rows_single + TC_BM - 1) / TC_BM) * NT;
 
   if (warp == 0 && lane == 0) {
@@ -224,8 +242,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       const int rem = tile - e * MT * NT;
       m0 = (rem / NT) * TC_BM;
       n0 = (rem % NT) * BN;
-      row0 = p.offsets[e];
-      row_end = p.offsets[e + 1];
+      row0 = offs[e];
+      row_end = offs[e + 1];
       nkb = (int)((row_end - row0 + TC_BK - 1) / TC_BK);
     } else {
       const int rt = tile / NT;
@@ -233,10 +251,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       m0 = 0;
       if (p.offsets) {
         int lo = 0, hi = p.E;
-        while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (p.plan[mid] <= rt) lo = mid; else hi = mid; }
+        while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (plan[mid] <= rt) lo = mid; else hi = mid; }
         e = lo;
-        row0 = p.offsets[e] + (int64_t)(rt - p.plan[e]) * TC_BM;
-        row_end = p.offsets[e + 1];
+        row0 = offs[e] + (int64_t)(rt - plan[e]) * TC_BM;
+        row_end = offs[e + 1];
       } else {
         e = 0;
         row0 = (int64_t)rt * TC_BM;
@@ -321,6 +339,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k) {
+            if (p.dbg & 4) break;
             const uint64_t ad = A_MN ? make_desc(a0 + k * 2048, 8192, 1024) : make_desc(a0 + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(b0 + k * 2048, 8192, 1024) : make_desc(b0 + k * 32, 16, 1024);
             tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
@@ -419,7 +438,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         for (int c16 = 0; c16 < SUB; c16 += 16) {
           if (c16 >= ncols) break;
           float v[16];
-          if (has_acc) {
+          if (has_acc && !(p.dbg & 2)) {
             uint32_t r[16];
             TMEM_LD16(tq + cs + c16, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -463,7 +482,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + (lane >> 3), piece = lane & 7;
-          if (r < live_rows && piece * 16 < row_bytes) {
+          if (r < live_rows && piece * 16 < row_bytes && !(p.dbg & 1)) {
             const uint4 v = *reinterpret_cast<const uint4*>(stg + r * TC_STAGE_ROW + piece * 16);
             uint8_t* gdst;
             if (SEGK)
@@ -546,6 +565,15 @@ bool tc_segk_supported(const GemmSegK& g) {
   return g.Mdim % TC_BM == 0 && g.N % 128 == 0 && encode_fn() != nullptr;
 }
 
+static int debug_flags() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("DMOE_TC_DEBUG");
+    f = e ? atoi(e) : 0;
+  }
+  return f;
+}
+
 template <int BN, bool SEGK, bool B_MN, int EPI>
 static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int64_t max_tiles,
                           cudaStream_t s) {
@@ -558,7 +586,9 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcPa
   }
   int64_t grid = max_tiles < num_sms() ? max_tiles : num_sms();
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, TcCfg<BN>::THREADS, smem, s>>>(a, b, p);
+  TcParams pp = p;
+  pp.dbg = debug_flags();
+  kern<<<(unsigned)grid, TcCfg<BN>::THREADS, smem, s>>>(a, b, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
 }
