@@ -136,6 +136,19 @@ __host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn) 
         "=r"(r[14]), "=r"(r[15])                                                               \
       : "r"(taddr))
 
+// pipeline timeline probe (dbg & 8): CTA 0 records %globaltimer at role events of its
+// first 32 tiles: [role][tile] with role 0 = producer first TMA issued, 1 = producer last TMA
+// issued, 2 = MMA got first stage, 3 = MMA committed last stage, 4 = epilogue got the
+// accumulator, 5 = epilogue done
+__device__ unsigned long long g_tc_probe[6][32];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROBE(role, i) \
+  do { if ((p.dbg & 8) && blockIdx.x == 0 && (i) < 32) g_tc_probe[role][i] = gtimer(); } while (0)
+
 // ------------------------------------------------------------------------- kernel
 struct TcParams {
   const int32_t* offsets;  // [E+1] or nullptr (single group of rows_single rows)
@@ -269,12 +282,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
         int e, m0, n0, nkb;
         int64_t row0, row_end;
         decode(tile, e, row0, row_end, m0, n0, nkb);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (kb == 0) PROBE(0, it);
+          if (kb == nkb - 1) PROBE(1, it);
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
@@ -305,7 +321,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
       int e, m0, n0, nkb;
       int64_t row0, row_end;
       decode(tile, e, row0, row_end, m0, n0, nkb);
@@ -316,6 +333,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (kb == 0 && lane == 0) PROBE(2, it);
         uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
         if (SEGK && kb == nkb - 1) {
@@ -345,7 +363,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
           }
           tc_commit(&empty[stage]);
-          if (kb == nkb - 1) tc_commit(&tfull[acc]);
+          if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
         }
         __syncwarp();
         if (++stage == S) { stage = 0; phase ^= 1; }
@@ -364,7 +382,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int acc = 0;
     uint32_t acc_phase = 0;
     int bias_buf = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
       int e, m0, n0, nkb;
       int64_t row0, row_end;
       decode(tile, e, row0, row_end, m0, n0, nkb);
@@ -407,6 +426,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
       }
+      if (ew == 0 && lane == 0) PROBE(4, it);
 #pragma unroll
       for (int sb = 0; sb < NSUB; ++sb) {
         const int cs = c_beg + sb * SUB;
@@ -494,6 +514,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
       }
+      if (ew == 0 && lane == 0) PROBE(5, it);
       if (has_acc) {
         tc_fence_before();
         __syncwarp();
@@ -663,3 +684,9 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
 }
 
 }  // namespace dmoe
+
+extern "C" int dmoe_debug_tc_probe(unsigned long long* host, int n) {
+  if (n > 6 * 32) n = 6 * 32;
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(host, dmoe::g_tc_probe, n * sizeof(unsigned long long));
+}
