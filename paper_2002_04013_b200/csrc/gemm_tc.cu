@@ -140,14 +140,14 @@ __host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn) 
 // first 32 tiles: [role][tile] with role 0 = producer first TMA issued, 1 = producer last TMA
 // issued, 2 = MMA got first stage, 3 = MMA committed last stage, 4 = epilogue got the
 // accumulator, 5 = epilogue done
-__device__ unsigned long long g_tc_probe[6][32];
+__device__ unsigned long long g_tc_probe[8][6][32];  // [launch % 8][role][tile]
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 #define PROBE(role, i) \
-  do { if ((p.dbg & 8) && blockIdx.x == 0 && (i) < 32) g_tc_probe[role][i] = gtimer(); } while (0)
+  do { if ((p.dbg & 8) && blockIdx.x == 0 && (i) < 32) g_tc_probe[p.slot][role][i] = gtimer(); } while (0)
 
 // ------------------------------------------------------------------------- kernel
 struct TcParams {
@@ -158,6 +158,7 @@ struct TcParams {
   void* C;
   int E, N, K, Mdim;
   int64_t rows_single;
+  int slot;  // probe slot (launch ordinal % 8)
   int dbg;  // experiment switches (env DMOE_TC_DEBUG): 1 skip stores, 2 skip TMEM loads, 4 skip MMAs
 };
 
@@ -609,6 +610,7 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcPa
   if (grid < 1) grid = 1;
   TcParams pp = p;
   pp.dbg = debug_flags();
+  pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
   kern<<<(unsigned)grid, TcCfg<BN>::THREADS, smem, s>>>(a, b, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
@@ -686,7 +688,7 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
 }  // namespace dmoe
 
 extern "C" int dmoe_debug_tc_probe(unsigned long long* host, int n) {
-  if (n > 6 * 32) n = 6 * 32;
+  if (n > 8 * 6 * 32) n = 8 * 6 * 32;
   cudaDeviceSynchronize();
   return (int)cudaMemcpyFromSymbol(host, dmoe::g_tc_probe, n * sizeof(unsigned long long));
 }

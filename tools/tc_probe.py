@@ -17,19 +17,24 @@ lay, x, dy, alive, resp = bench.build_layer(cfg, 0, torch.device("cuda", 0), cfg
 for _ in range(2):
     bench.run_calls(lay, x, dy, alive, resp)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * 192)()
+buf = (ctypes.c_ulonglong * (8 * 192))()
 f = L._L.dmoe_debug_tc_probe
 names = ["prod0", "prodN", "mma0", "mmaC", "epi0", "epiD"]
-calls = [
-    ("fwd (GEMM2: out)", lambda: L.dmoe_expert_ffn_fwd(lay.xd, lay.offsets, lay.W1, lay.b1, lay.W2, lay.b2, lay.h, lay.out, lay.ws)),
-    ("bwd (GEMM6: dW1)", lambda: L.dmoe_expert_ffn_bwd(lay.xd, lay.h, lay.dout, lay.offsets, lay.W1, lay.W2, lay.dxd, lay.dW1, lay.db1, lay.dW2, lay.db2, lay.ws)),
-]
-for name, fn in calls:
-    fn()
-    torch.cuda.synchronize()
-    f(buf, 192)
-    t = [[buf[r * 32 + i] for i in range(32)] for r in range(6)]
-    t0 = min(v for row in t for v in row if v)
-    print("==", name, "us since first event of CTA 0")
-    for i in range(16):
-        print(f"tile {i:2d} " + " ".join(f"{names[r]}={(t[r][i] - t0) / 1e3:7.2f}" if t[r][i] else f"{names[r]}=    -  " for r in range(6)))
+c0 = L.dmoe_launch_counters()[1]
+bench.run_calls(lay, x, dy, alive, resp)
+torch.cuda.synchronize()
+c1 = L.dmoe_launch_counters()[1]
+f(buf, 8 * 192)
+labels = ["gate", "GEMM1 h", "GEMM2 out", "GEMM3 dh", "GEMM4 dxd", "GEMM5 dW2", "GEMM6 dW1"]
+for j, launch in enumerate(range(c0, c1)):
+    slot = launch % 8
+    t = [[buf[slot * 192 + r * 32 + i] for i in range(32)] for r in range(6)]
+    vals = [v for row in t for v in row if v]
+    if not vals:
+        continue
+    t0 = min(vals)
+    print("==", labels[j] if j < len(labels) else j, "CTA 0, us since its first event")
+    for i in range(12):
+        if not any(t[r][i] for r in range(6)):
+            continue
+        print(f"tile {i:2d} " + " ".join(f"{names[r]}={(t[r][i] - t0) / 1e3:6.2f}" if t[r][i] else f"{names[r]}=   -  " for r in range(6)))
