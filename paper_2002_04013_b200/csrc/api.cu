@@ -95,14 +95,14 @@ static dmoe_status segk_gemm(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
   if (dt == DMOE_BF16 && tc_segk_supported(g)) return tc_gemm_segk(g, s);
   return simt_gemm_segk(g, dt, s);
 }
-constexpr int kPlanBM_TC = 128, kPlanBM_SIMT = 64;
+constexpr int kPlanBM_SIMT = 64;
 
 // row-tile plans only for the engines the two GEMMs of a call will use
 static dmoe_status plans_for(const GemmRows& a, const GemmRows& b, const int32_t* offsets, int E,
                              int32_t* plan_tc, int32_t* plan_simt, cudaStream_t s) {
   const bool need_tc = a.plan == plan_tc || b.plan == plan_tc;
   const bool need_simt = a.plan == plan_simt || b.plan == plan_simt;
-  if (need_tc) DMOE_TRY(tile_plan(offsets, E, kPlanBM_TC, plan_tc, s));
+  if (need_tc) DMOE_TRY(tile_plan(offsets, E, tc_rows_tile(a.plan == plan_tc ? a : b), plan_tc, s));
   if (need_simt) DMOE_TRY(tile_plan(offsets, E, kPlanBM_SIMT, plan_simt, s));
   return DMOE_OK;
 }
@@ -157,7 +157,7 @@ dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D,
     DMOE_REQUIRE(ws_bytes >= (size_t)dM * D * 2, DMOE_ERR_ARG, "gate_scores: workspace too small");
     DMOE_TRY(transpose(Wg, D, dM, dt, ws, s));
     r.B = ws;
-    r.max_tiles = ceil_div(T, kPlanBM_TC);
+    r.max_tiles = ceil_div(T, tc_rows_tile(r));
     return tc_gemm_rows(r, s);
   }
   r.b_mn = true;
@@ -216,7 +216,7 @@ dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t 
   g2.A = h; g2.B = W2; g2.C = out; g2.bias = b2; g2.N = D; g2.K = H; g2.epi = EPI_BIAS;
   for (GemmRows* g : {&g1, &g2}) {
     const bool tc = dt == DMOE_BF16 && tc_rows_supported(*g);
-    const int bm = tc ? kPlanBM_TC : kPlanBM_SIMT;
+    const int bm = tc ? tc_rows_tile(*g) : kPlanBM_SIMT;
     g->plan = tc ? plan_tc : plan_simt;
     g->max_tiles = ceil_div(R_cap, bm) + E_local;
   }
@@ -268,7 +268,7 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
   g4.A = dh; g4.B = W1; g4.C = dxd; g4.aux = nullptr; g4.N = D; g4.K = H; g4.epi = EPI_PLAIN;
   for (GemmRows* g : {&g3, &g4}) {
     const bool tc = dt == DMOE_BF16 && tc_rows_supported(*g);
-    const int bm = tc ? kPlanBM_TC : kPlanBM_SIMT;
+    const int bm = tc ? tc_rows_tile(*g) : kPlanBM_SIMT;
     g->plan = tc ? plan_tc : plan_simt;
     g->max_tiles = ceil_div(R_cap, bm) + E_local;
   }

@@ -533,6 +533,229 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
 }
 
+// --------------------------------------------------------- ROWS engine (swap-AB form)
+// For the row GEMMs C[r, n] = epi(sum_k X[r, k] W_e(n, k)) the expert weights are the MMA
+// M operand (128 output features per tile) and the dispatched tokens the N operand
+// (NT = 64/128/256 token rows per tile).  Each expert's rows are padded only to NT, a
+// stage is 16 KB of weights + NT*128 B of tokens, so 8+ stages keep >= 128 KB of weights in
+// flight per SM: the weight-streaming regime of small expert batches (rows/expert ~ 64)
+// needs that depth.  TMEM lane = output feature, column = token: the epilogue thread owns
+// one feature, so bias is one register and every store instruction writes 32 consecutive
+// features of one token row (coalesced) with rows masked to the expert's segment.
+constexpr int SW_FEAT = 128;  // MMA M (output features per tile)
+
+template <int NT> struct SwCfg {
+  static_assert(NT == 64 || NT == 128 || NT == 256, "token tile");
+  static constexpr int EPI_WARPS = 8;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int W_BYTES = SW_FEAT * TC_BK * 2;   // 16 KB
+  static constexpr int X_BYTES = NT * TC_BK * 2;
+  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
+  static constexpr int FIXED = 1024 + 512 + 2 * (TC_TABLE_E + 1) * 4;
+  static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
+  static constexpr int STAGES = ST > 12 ? 12 : ST;
+  static constexpr int ACC = NT == 256 ? 2 : 4;         // accumulator buffers in TMEM
+  static constexpr int TMEM_COLS = ACC * NT <= 256 ? 256 : 512;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
+};
+
+template <int NT, bool W_MN, int EPI>
+__global__ void __launch_bounds__(SwCfg<NT>::THREADS, 1)
+k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+          const TcParams p) {
+  using Cfg = SwCfg<NT>;
+  constexpr int S = Cfg::STAGES;
+  constexpr int ACC = Cfg::ACC;
+  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
+  constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + S * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + ACC;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + ACC);
+  int32_t* off_s = (int32_t*)(smem + S * Cfg::STAGE_BYTES + 512);
+  int32_t* plan_s = off_s + (TC_TABLE_E + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int32_t* offs = p.offsets;
+  const int32_t* plan = p.plan;
+  if (p.offsets && p.E <= TC_TABLE_E) {
+    for (int i = threadIdx.x; i <= p.E; i += blockDim.x) {
+      off_s[i] = p.offsets[i];
+      plan_s[i] = p.plan[i];
+    }
+    offs = off_s;
+    plan = plan_s;
+  }
+  const int NFB = (p.N + SW_FEAT - 1) / SW_FEAT;
+  const int total = (p.offsets ? p.plan[p.E] : (int)((p.rows_single + NT - 1) / NT)) * NFB;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], Cfg::EPI_WARPS); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // tile -> (expert e, token rows [row0, row_end), feature block f0)
+  auto decode = [&](int tile, int& e, int64_t& row0, int64_t& row_end, int& f0) {
+    const int rt = tile / NFB;
+    f0 = (tile - rt * NFB) * SW_FEAT;
+    if (p.offsets) {
+      int lo = 0, hi = p.E;
+      while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (plan[mid] <= rt) lo = mid; else hi = mid; }
+      e = lo;
+      row0 = offs[e] + (int64_t)(rt - plan[e]) * NT;
+      row_end = offs[e + 1];
+    } else {
+      e = 0;
+      row0 = (int64_t)rt * NT;
+      row_end = p.rows_single;
+    }
+  };
+  const int nkb = p.K / TC_BK;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+        int e, f0;
+        int64_t row0, row_end;
+        decode(tile, e, row0, row_end, f0);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (kb == 0) PROBE(0, it);
+          uint8_t* sw = smem + stage * Cfg::STAGE_BYTES;
+          uint8_t* sx = sw + Cfg::W_BYTES;
+          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          if (W_MN) {
+            tma_load_3d(sw, &tmW, &full[stage], f0, kb * TC_BK, e);
+            tma_load_3d(sw + 8192, &tmW, &full[stage], f0 + 64, kb * TC_BK, e);
+          } else {
+            tma_load_3d(sw, &tmW, &full[stage], kb * TC_BK, f0, e);
+          }
+          tma_load_2d(sx, &tmX, &full[stage], kb * TC_BK, (int)row0);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {  // ---------------- MMA issuer
+    constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((W_MN ? 1u : 0u) << 15) |
+                               ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(SW_FEAT >> 4) << 24);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * NT;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (kb == 0 && lane == 0) PROBE(2, it);
+        if (lane == 0) {
+          const uint32_t w0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
+          const uint32_t x0 = w0 + Cfg::W_BYTES;
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k) {
+            if (p.dbg & 4) break;
+            const uint64_t ad = W_MN ? make_desc(w0 + k * 2048, 8192, 1024) : make_desc(w0 + k * 32, 16, 1024);
+            const uint64_t bd = make_desc(x0 + k * 32, 16, 1024);
+            tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
+        }
+        __syncwarp();
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp >= 4) {  // ---------------- epilogue
+    const int ew = warp - 4;
+    const int q = warp & 3;                  // TMEM lanes 32q..32q+31 = features f0+32q+lane
+    constexpr int TH = NT / 2;               // tokens per warp
+    const int t_beg = (ew >> 2) * TH;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      int e, f0;
+      int64_t row0, row_end;
+      decode(tile, e, row0, row_end, f0);
+      const int f = f0 + q * 32 + lane;
+      const bool fvalid = f < p.N;
+      int64_t nrows = row_end - (row0 + t_beg);
+      nrows = nrows < 0 ? 0 : (nrows > TH ? TH : nrows);
+      float b = 0.0f;
+      if (HAS_BIAS && fvalid) b = __ldg(p.bias + (int64_t)e * p.N + f);
+      // ReLU-mask source h[row][f], 16 tokens at a time; the first chunk is loaded before
+      // the accumulator wait so its latency hides behind the MMA
+      uint16_t hb[16];
+      auto load_h = [&](int c) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          hb[j] = (c + j < nrows && fvalid)
+                      ? __ldg(reinterpret_cast<const unsigned short*>(p.aux) + (row0 + t_beg + c + j) * p.N + f)
+                      : (uint16_t)0;
+      };
+      if (EPI == EPI_RELU_MASK) load_h(0);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      if (ew == 0 && lane == 0) PROBE(4, it);
+      const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * NT + t_beg;
+#pragma unroll 1
+      for (int c = 0; c < TH; c += 16) {
+        if (EPI == EPI_RELU_MASK && c > 0) load_h(c);
+        uint32_t r[16];
+        TMEM_LD16(tq + c, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (p.dbg & 1) continue;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          if (c + j >= nrows || !fvalid) continue;
+          float v = __uint_as_float(r[j]);
+          if (HAS_BIAS) v += b;
+          if (EPI == EPI_BIAS_RELU) v = fmaxf(v, 0.0f);
+          if (EPI == EPI_RELU_MASK) v = bf16_pos(hb[j]) ? v : 0.0f;
+          const int64_t row = row0 + t_beg + c + j;
+          if (OUT_F32) reinterpret_cast<float*>(p.C)[row * p.N + f] = v;
+          else reinterpret_cast<__nv_bfloat16*>(p.C)[row * p.N + f] = __float2bfloat16_rn(v);
+        }
+      }
+      if (ew == 0 && lane == 0) PROBE(5, it);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+  }
+}
+
 // ----------------------------------------------------------------- host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -576,9 +799,16 @@ static int pick_bn(int N, bool b_mn) {
   return 0;
 }
 
+// token tile of the row GEMMs from the expected rows per expert (capacity / experts)
+int tc_rows_tile(const GemmRows& g) {
+  if (!g.offsets) return 64;
+  const int64_t avg = g.rows_cap / (g.E > 0 ? g.E : 1);
+  return avg <= 64 ? 64 : (avg <= 160 ? 128 : 256);
+}
+
 bool tc_rows_supported(const GemmRows& g) {
-  if (g.K % TC_BK != 0 || g.K <= 0) return false;
-  if (pick_bn(g.N, g.b_mn) == 0) return false;
+  if (g.K % TC_BK != 0 || g.K <= 0 || g.N % 16 != 0) return false;
+  if (g.b_mn && g.N % 64 != 0) return false;
   if (g.epi == EPI_F32_BIAS && g.offsets != nullptr) return false;
   if (encode_fn() == nullptr) return false;
   return true;
@@ -616,21 +846,39 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcPa
   return check_launch("tc_gemm");
 }
 
-template <int BN>
-static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtensorMap& b, const TcParams& p,
+template <int NT, bool W_MN, int EPI>
+static dmoe_status launch_rows(const CUtensorMap& w, const CUtensorMap& x, const TcParams& p, int64_t max_tiles,
+                               cudaStream_t s) {
+  auto kern = k_tc_rows<NT, W_MN, EPI>;
+  const int smem = SwCfg<NT>::SMEM;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  int64_t grid = max_tiles < num_sms() ? max_tiles : num_sms();
+  if (grid < 1) grid = 1;
+  TcParams pp = p;
+  pp.dbg = debug_flags();
+  pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
+  kern<<<(unsigned)grid, SwCfg<NT>::THREADS, smem, s>>>(w, x, pp);
+  __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
+  return check_launch("tc_gemm_rows");
+}
+
+template <int NT>
+static dmoe_status rows_nt(const GemmRows& g, const CUtensorMap& w, const CUtensorMap& x, const TcParams& p,
                            int64_t tiles, cudaStream_t s) {
-#define DMOE_TC_ROWS(BMN, E_) return launch<BN, false, BMN, E_>(a, b, p, tiles, s)
-#define DMOE_TC_EPI(BMN)                                   \
+#define DMOE_TC_ROWS(WMN, E_) return launch_rows<NT, WMN, E_>(w, x, p, tiles, s)
+#define DMOE_TC_EPI(WMN)                                   \
   switch (g.epi) {                                         \
-    case EPI_F32_BIAS: DMOE_TC_ROWS(BMN, EPI_F32_BIAS);    \
-    case EPI_BIAS_RELU: DMOE_TC_ROWS(BMN, EPI_BIAS_RELU);  \
-    case EPI_BIAS: DMOE_TC_ROWS(BMN, EPI_BIAS);            \
-    case EPI_RELU_MASK: DMOE_TC_ROWS(BMN, EPI_RELU_MASK);  \
-    default: DMOE_TC_ROWS(BMN, EPI_PLAIN);                 \
+    case EPI_F32_BIAS: DMOE_TC_ROWS(WMN, EPI_F32_BIAS);    \
+    case EPI_BIAS_RELU: DMOE_TC_ROWS(WMN, EPI_BIAS_RELU);  \
+    case EPI_BIAS: DMOE_TC_ROWS(WMN, EPI_BIAS);            \
+    case EPI_RELU_MASK: DMOE_TC_ROWS(WMN, EPI_RELU_MASK);  \
+    default: DMOE_TC_ROWS(WMN, EPI_PLAIN);                 \
   }
-  if constexpr (BN % 64 == 0) {
-    if (g.b_mn) { DMOE_TC_EPI(true) }
-  }
+  if (g.b_mn) { DMOE_TC_EPI(true) }
   DMOE_TC_EPI(false)
 #undef DMOE_TC_EPI
 #undef DMOE_TC_ROWS
@@ -638,34 +886,27 @@ static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtens
 
 dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
   if (g.max_tiles <= 0) return DMOE_OK;
-  const int BN = pick_bn(g.N, g.b_mn);
-  // A: [rows_cap, K] K-major; rows past the extent are zero-filled by TMA, rows past a
-  // segment produce accumulator rows the epilogue never stores.
-  CUtensorMap ta, tb;
-  uint64_t adims[2] = {(uint64_t)g.K, (uint64_t)(g.rows_cap > 0 ? g.rows_cap : 1)};
-  DMOE_TRY(make_map(&ta, g.A, 2, adims, TC_BM));
+  const int NT = tc_rows_tile(g);
+  // W (MMA A): K-major [E][N][K] boxes {64 K, 128 features}, or MN-major [E][K][N] boxes
+  // {64 features, 64 K} x 2.  X (MMA B): tokens [rows_cap][K], boxes {64 K, NT rows};
+  // rows past rows_cap are zero-filled by TMA, rows past a segment are never stored.
+  CUtensorMap tw, tx;
   if (g.b_mn) {
-    uint64_t bdims[3] = {(uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.E};
-    DMOE_TRY(make_map(&tb, g.B, 3, bdims, 64));
+    uint64_t d[3] = {(uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.E};
+    DMOE_TRY(make_map(&tw, g.B, 3, d, 64));
   } else {
-    uint64_t bdims[3] = {(uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.E};
-    DMOE_TRY(make_map(&tb, g.B, 3, bdims, (uint32_t)BN));
+    uint64_t d[3] = {(uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.E};
+    DMOE_TRY(make_map(&tw, g.B, 3, d, SW_FEAT));
   }
+  uint64_t xd[2] = {(uint64_t)g.K, (uint64_t)(g.rows_cap > 0 ? g.rows_cap : 1)};
+  DMOE_TRY(make_map(&tx, g.A, 2, xd, (uint32_t)NT));
   TcParams p{};
   p.offsets = g.offsets; p.plan = g.plan; p.bias = g.bias; p.aux = (const __nv_bfloat16*)g.aux;
   p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
-  const int64_t tiles = g.max_tiles * ((g.N + BN - 1) / BN);
-  switch (BN) {
-    case 256: return rows_bn<256>(g, ta, tb, p, tiles, s);
-    case 128: return rows_bn<128>(g, ta, tb, p, tiles, s);
-    case 64: return rows_bn<64>(g, ta, tb, p, tiles, s);
-    case 192: return rows_bn<192>(g, ta, tb, p, tiles, s);
-    case 32: return rows_bn<32>(g, ta, tb, p, tiles, s);
-    case 48: return rows_bn<48>(g, ta, tb, p, tiles, s);
-    case 96: return rows_bn<96>(g, ta, tb, p, tiles, s);
-    case 16: return rows_bn<16>(g, ta, tb, p, tiles, s);
-    default: return set_error(DMOE_ERR_UNSUPPORTED, "tc_gemm_rows: N=%d", g.N);
-  }
+  const int64_t tiles = g.max_tiles * ((g.N + SW_FEAT - 1) / SW_FEAT);
+  if (NT == 64) return rows_nt<64>(g, tw, tx, p, tiles, s);
+  if (NT == 128) return rows_nt<128>(g, tw, tx, p, tiles, s);
+  return rows_nt<256>(g, tw, tx, p, tiles, s);
 }
 
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
