@@ -551,7 +551,9 @@ template <int NT> struct SwCfg {
   static constexpr int W_BYTES = SW_FEAT * TC_BK * 2;   // 16 KB
   static constexpr int X_BYTES = NT * TC_BK * 2;
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  static constexpr int FIXED = 1024 + 512 + 2 * (TC_TABLE_E + 1) * 4;
+  static constexpr int STG_PITCH = SW_FEAT * 4 + 16;   // one token row of 128 features (fp32 worst case)
+  static constexpr int STG_BYTES = 2 * 32 * STG_PITCH;   // [token half][32 tokens][128 features]
+  static constexpr int FIXED = 1024 + 512 + 2 * (TC_TABLE_E + 1) * 4 + STG_BYTES;
   static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = ST > 12 ? 12 : ST;
   static constexpr int ACC = NT == 256 ? 2 : 4;         // accumulator buffers in TMEM
@@ -577,6 +579,7 @@ k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUten
   uint32_t* tmem_slot = (uint32_t*)(tempty + ACC);
   int32_t* off_s = (int32_t*)(smem + S * Cfg::STAGE_BYTES + 512);
   int32_t* plan_s = off_s + (TC_TABLE_E + 1);
+  uint8_t* stg_all = (uint8_t*)(plan_s + (TC_TABLE_E + 1));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int32_t* offs = p.offsets;
@@ -690,10 +693,19 @@ k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUten
       if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {  // ---------------- epilogue
+    // warp (q = warp % 4) owns TMEM lanes 32q..32q+31 = features f0+32q+lane; the two warp
+    // quartets split the tile's tokens.  Per 32-token chunk the quartet stages a
+    // [32 tokens][128 features] block in smem (lane -> one feature column), then each warp
+    // stores 8 token rows as 256-/512-byte contiguous runs, rows masked to the segment.
+    constexpr int OUT_ES = OUT_F32 ? 4 : 2;
+    constexpr int ROWB = SW_FEAT * OUT_ES;     // bytes of one staged token row
+    constexpr int TH = NT / 2;                 // tokens per quartet
     const int ew = warp - 4;
-    const int q = warp & 3;                  // TMEM lanes 32q..32q+31 = features f0+32q+lane
-    constexpr int TH = NT / 2;               // tokens per warp
-    const int t_beg = (ew >> 2) * TH;
+    const int q = warp & 3;
+    const int half = ew >> 2;
+    const int t_beg = half * TH;
+    uint8_t* stg = stg_all + half * 32 * Cfg::STG_PITCH;
+    const uint32_t bar_id = 1 + half;
     int acc = 0;
     uint32_t acc_phase = 0;
     int it = 0;
@@ -703,19 +715,21 @@ k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUten
       decode(tile, e, row0, row_end, f0);
       const int f = f0 + q * 32 + lane;
       const bool fvalid = f < p.N;
+      const int nf = p.N - f0 < SW_FEAT ? p.N - f0 : SW_FEAT;   // valid features in the tile
       int64_t nrows = row_end - (row0 + t_beg);
       nrows = nrows < 0 ? 0 : (nrows > TH ? TH : nrows);
       float b = 0.0f;
       if (HAS_BIAS && fvalid) b = __ldg(p.bias + (int64_t)e * p.N + f);
-      // ReLU-mask source h[row][f], 16 tokens at a time; the first chunk is loaded before
-      // the accumulator wait so its latency hides behind the MMA
-      uint16_t hb[16];
+      // ReLU-mask source rows h[row][f0 .. f0+127] of the first chunk, prefetched (coalesced)
+      uint4 hreg[4];
       auto load_h = [&](int c) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          hb[j] = (c + j < nrows && fvalid)
-                      ? __ldg(reinterpret_cast<const unsigned short*>(p.aux) + (row0 + t_beg + c + j) * p.N + f)
-                      : (uint16_t)0;
+        for (int i = 0; i < 4; ++i) {
+          const int r = q * 8 + i * 2 + (lane >> 4), piece = lane & 15;
+          hreg[i] = make_uint4(0, 0, 0, 0);
+          if (c + r < nrows && piece * 8 < nf)
+            hreg[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (row0 + t_beg + c + r) * p.N + f0) + piece);
+        }
       };
       if (EPI == EPI_RELU_MASK) load_h(0);
       mbar_wait(&tfull[acc], acc_phase);
@@ -723,23 +737,58 @@ k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUten
       if (ew == 0 && lane == 0) PROBE(4, it);
       const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * NT + t_beg;
 #pragma unroll 1
-      for (int c = 0; c < TH; c += 16) {
-        if (EPI == EPI_RELU_MASK && c > 0) load_h(c);
-        uint32_t r[16];
-        TMEM_LD16(tq + c, r);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (p.dbg & 1) continue;
+      for (int c = 0; c < TH; c += 32) {
+        if (c >= nrows) break;  // uniform across the quartet (same nrows)
+        uint32_t hm = 0xffffffffu;  // bit j: h[row c+j][f] > 0
+        if (EPI == EPI_RELU_MASK) {
+          if (c > 0) load_h(c);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (c + j >= nrows || !fvalid) continue;
-          float v = __uint_as_float(r[j]);
-          if (HAS_BIAS) v += b;
-          if (EPI == EPI_BIAS_RELU) v = fmaxf(v, 0.0f);
-          if (EPI == EPI_RELU_MASK) v = bf16_pos(hb[j]) ? v : 0.0f;
-          const int64_t row = row0 + t_beg + c + j;
-          if (OUT_F32) reinterpret_cast<float*>(p.C)[row * p.N + f] = v;
-          else reinterpret_cast<__nv_bfloat16*>(p.C)[row * p.N + f] = __float2bfloat16_rn(v);
+          for (int i = 0; i < 4; ++i) {
+            const int r = q * 8 + i * 2 + (lane >> 4), piece = lane & 15;
+            *reinterpret_cast<uint4*>(stg + r * Cfg::STG_PITCH + piece * 16) = hreg[i];
+          }
+          asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+          hm = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const uint16_t hv = *reinterpret_cast<const uint16_t*>(stg + j * Cfg::STG_PITCH + (q * 32 + lane) * 2);
+            hm |= (bf16_pos(hv) ? 1u : 0u) << j;
+          }
+          asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
         }
+        // TMEM -> registers -> epilogue math -> staging column (this lane's feature)
+#pragma unroll
+        for (int c16 = 0; c16 < 32; c16 += 16) {
+          uint32_t r[16];
+          TMEM_LD16(tq + c + c16, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float v = __uint_as_float(r[j]);
+            if (HAS_BIAS) v += b;
+            if (EPI == EPI_BIAS_RELU) v = fmaxf(v, 0.0f);
+            if (EPI == EPI_RELU_MASK) v = ((hm >> (c16 + j)) & 1u) ? v : 0.0f;
+            uint8_t* dst = stg + (c16 + j) * Cfg::STG_PITCH + (q * 32 + lane) * OUT_ES;
+            if (OUT_F32) *reinterpret_cast<float*>(dst) = v;
+            else *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(v);
+          }
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+        // staging -> global: warp q stores token rows 8q .. 8q+7
+        if (!(p.dbg & 1)) {
+          constexpr int LPR = ROWB / 16;           // 16-byte pieces per row (16 or 32)
+          constexpr int RPI = 32 / LPR;            // rows per instruction (2 or 1)
+#pragma unroll
+          for (int i = 0; i < 8 / RPI; ++i) {
+            const int r = q * 8 + i * RPI + lane / LPR, piece = lane % LPR;
+            if (c + r < nrows && piece * 16 < nf * OUT_ES) {
+              const uint4 v = *reinterpret_cast<const uint4*>(stg + r * Cfg::STG_PITCH + piece * 16);
+              uint8_t* g = (uint8_t*)p.C + ((row0 + t_beg + c + r) * p.N + f0) * OUT_ES + piece * 16;
+              *reinterpret_cast<uint4*>(g) = v;
+            }
+          }
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
       }
       if (ew == 0 && lane == 0) PROBE(5, it);
       tc_fence_before();
