@@ -166,6 +166,7 @@ constexpr int TC_SMEM_MAX = 227 * 1024;
 constexpr int TC_STAGE_ROW = 144;              // staging row pitch: 128 B of data + 16 B pad
 constexpr int TC_STAGE_WARP = 32 * TC_STAGE_ROW;  // one warp's 32-row staging tile
 constexpr int TC_TABLE_E = 4096;                  // experts whose offsets/plan live in smem
+constexpr int TC_TABLE_LEN = TC_TABLE_E + 4;      // entries per table (16-byte multiple)
 
 template <int BN> struct TcCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
@@ -176,7 +177,7 @@ template <int BN> struct TcCfg {
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
   static constexpr int FIXED = 1024 /*align*/ + 512 /*barriers*/ + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2 +
-                               2 * (TC_TABLE_E + 1) * 4 /*offsets + plan tables*/;
+                               2 * TC_TABLE_LEN * 4 /*offsets + plan tables*/;
   static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = ST > 8 ? 8 : ST;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
@@ -206,7 +207,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 512;
   float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * TC_STAGE_WARP);  // [2][BN]
   int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [E+1]
-  int32_t* plan_s = off_s + (TC_TABLE_E + 1);                               // [E+1]
+  int32_t* plan_s = off_s + TC_TABLE_LEN;                               // [E+1]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -553,7 +554,7 @@ template <int NT> struct SwCfg {
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
   static constexpr int STG_PITCH = SW_FEAT * 4 + 16;   // one token row of 128 features (fp32 worst case)
   static constexpr int STG_BYTES = 2 * 32 * STG_PITCH;   // [token half][32 tokens][128 features]
-  static constexpr int FIXED = 1024 + 512 + 2 * (TC_TABLE_E + 1) * 4 + STG_BYTES;
+  static constexpr int FIXED = 1024 + 512 + 2 * TC_TABLE_LEN * 4 + STG_BYTES;
   static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = ST > 12 ? 12 : ST;
   static constexpr int ACC = NT == 256 ? 2 : 4;         // accumulator buffers in TMEM
@@ -578,8 +579,8 @@ k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUten
   uint64_t* tempty = tfull + ACC;
   uint32_t* tmem_slot = (uint32_t*)(tempty + ACC);
   int32_t* off_s = (int32_t*)(smem + S * Cfg::STAGE_BYTES + 512);
-  int32_t* plan_s = off_s + (TC_TABLE_E + 1);
-  uint8_t* stg_all = (uint8_t*)(plan_s + (TC_TABLE_E + 1));
+  int32_t* plan_s = off_s + TC_TABLE_LEN;
+  uint8_t* stg_all = (uint8_t*)(plan_s + TC_TABLE_LEN);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   const int32_t* offs = p.offsets;
