@@ -165,7 +165,7 @@ struct TcParams {
 constexpr int TC_SMEM_MAX = 227 * 1024;
 constexpr int TC_STAGE_ROW = 144;              // staging row pitch: 128 B of data + 16 B pad
 constexpr int TC_STAGE_WARP = 32 * TC_STAGE_ROW;  // one warp's 32-row staging tile
-constexpr int TC_TABLE_E = 4096;                  // experts whose offsets/plan live in smem
+constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan live in smem
 constexpr int TC_TABLE_LEN = TC_TABLE_E + 4;      // entries per table (16-byte multiple)
 
 template <int BN> struct TcCfg {
@@ -545,14 +545,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 // features of one token row (coalesced) with rows masked to the expert's segment.
 constexpr int SW_FEAT = 128;  // MMA M (output features per tile)
 
-template <int NT> struct SwCfg {
+template <int NT, bool OUT_F32 = false> struct SwCfg {
   static_assert(NT == 64 || NT == 128 || NT == 256, "token tile");
   static constexpr int EPI_WARPS = 8;
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int W_BYTES = SW_FEAT * TC_BK * 2;   // 16 KB
   static constexpr int X_BYTES = NT * TC_BK * 2;
   static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  static constexpr int STG_PITCH = SW_FEAT * 4 + 16;   // one token row of 128 features (fp32 worst case)
+  static constexpr int STG_PITCH = SW_FEAT * (OUT_F32 ? 4 : 2) + 16;  // one staged token row of 128 features
   static constexpr int STG_BYTES = 2 * 32 * STG_PITCH;   // [token half][32 tokens][128 features]
   static constexpr int FIXED = 1024 + 512 + 2 * TC_TABLE_LEN * 4 + STG_BYTES;
   static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
@@ -566,10 +566,10 @@ template <int NT, bool W_MN, int EPI>
 __global__ void __launch_bounds__(SwCfg<NT>::THREADS, 1)
 k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
           const TcParams p) {
-  using Cfg = SwCfg<NT>;
+  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
+  using Cfg = SwCfg<NT, OUT_F32>;
   constexpr int S = Cfg::STAGES;
   constexpr int ACC = Cfg::ACC;
-  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
   constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -852,8 +852,14 @@ static int pick_bn(int N, bool b_mn) {
 // token tile of the row GEMMs from the expected rows per expert (capacity / experts)
 int tc_rows_tile(const GemmRows& g) {
   if (!g.offsets) return 64;
+  static int force = -1;
+  if (force < 0) {
+    const char* e = getenv("DMOE_TC_NT");  // experiment override: 64 / 128 / 256
+    force = e ? atoi(e) : 0;
+  }
+  if (force == 64 || force == 128 || force == 256) return force;
   const int64_t avg = g.rows_cap / (g.E > 0 ? g.E : 1);
-  return avg <= 64 ? 64 : (avg <= 160 ? 128 : 256);
+  return avg <= 32 ? 64 : (avg <= 160 ? 128 : 256);
 }
 
 bool tc_rows_supported(const GemmRows& g) {
@@ -900,7 +906,7 @@ template <int NT, bool W_MN, int EPI>
 static dmoe_status launch_rows(const CUtensorMap& w, const CUtensorMap& x, const TcParams& p, int64_t max_tiles,
                                cudaStream_t s) {
   auto kern = k_tc_rows<NT, W_MN, EPI>;
-  const int smem = SwCfg<NT>::SMEM;
+  const int smem = SwCfg<NT, EPI == EPI_F32_BIAS>::SMEM;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
