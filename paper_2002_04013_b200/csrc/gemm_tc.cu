@@ -849,8 +849,18 @@ static int pick_bn(int N, bool b_mn) {
   return 0;
 }
 
+static bool rows_swap() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DMOE_TC_ROWS");  // "swap": swap-AB row kernel (experiment)
+    v = (e && e[0] == 's') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // token tile of the row GEMMs from the expected rows per expert (capacity / experts)
 int tc_rows_tile(const GemmRows& g) {
+  if (!rows_swap()) return TC_BM;  // M-major kernel: 128-row token tiles
   if (!g.offsets) return 64;
   static int force = -1;
   if (force < 0) {
@@ -865,6 +875,7 @@ int tc_rows_tile(const GemmRows& g) {
 bool tc_rows_supported(const GemmRows& g) {
   if (g.K % TC_BK != 0 || g.K <= 0 || g.N % 16 != 0) return false;
   if (g.b_mn && g.N % 64 != 0) return false;
+  if (!rows_swap() && pick_bn(g.N, g.b_mn) == 0) return false;
   if (g.epi == EPI_F32_BIAS && g.offsets != nullptr) return false;
   if (encode_fn() == nullptr) return false;
   return true;
@@ -901,6 +912,59 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcPa
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
 }
+
+template <int BN>
+static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtensorMap& b, const TcParams& p,
+                           int64_t tiles, cudaStream_t s) {
+#define DMOE_TC_ROWS(BMN, E_) return launch<BN, false, BMN, E_>(a, b, p, tiles, s)
+#define DMOE_TC_EPI(BMN)                                   \
+  switch (g.epi) {                                         \
+    case EPI_F32_BIAS: DMOE_TC_ROWS(BMN, EPI_F32_BIAS);    \
+    case EPI_BIAS_RELU: DMOE_TC_ROWS(BMN, EPI_BIAS_RELU);  \
+    case EPI_BIAS: DMOE_TC_ROWS(BMN, EPI_BIAS);            \
+    case EPI_RELU_MASK: DMOE_TC_ROWS(BMN, EPI_RELU_MASK);  \
+    default: DMOE_TC_ROWS(BMN, EPI_PLAIN);                 \
+  }
+  if constexpr (BN % 64 == 0) {
+    if (g.b_mn) { DMOE_TC_EPI(true) }
+  }
+  DMOE_TC_EPI(false)
+#undef DMOE_TC_EPI
+#undef DMOE_TC_ROWS
+}
+
+static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
+  if (g.max_tiles <= 0) return DMOE_OK;
+  const int BN = pick_bn(g.N, g.b_mn);
+  // A: [rows_cap, K] K-major; rows past the extent are zero-filled by TMA, rows past a
+  // segment produce accumulator rows the epilogue never stores.
+  CUtensorMap ta, tb;
+  uint64_t adims[2] = {(uint64_t)g.K, (uint64_t)(g.rows_cap > 0 ? g.rows_cap : 1)};
+  DMOE_TRY(make_map(&ta, g.A, 2, adims, TC_BM));
+  if (g.b_mn) {
+    uint64_t bdims[3] = {(uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.E};
+    DMOE_TRY(make_map(&tb, g.B, 3, bdims, 64));
+  } else {
+    uint64_t bdims[3] = {(uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.E};
+    DMOE_TRY(make_map(&tb, g.B, 3, bdims, (uint32_t)BN));
+  }
+  TcParams p{};
+  p.offsets = g.offsets; p.plan = g.plan; p.bias = g.bias; p.aux = (const __nv_bfloat16*)g.aux;
+  p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
+  const int64_t tiles = g.max_tiles * ((g.N + BN - 1) / BN);
+  switch (BN) {
+    case 256: return rows_bn<256>(g, ta, tb, p, tiles, s);
+    case 128: return rows_bn<128>(g, ta, tb, p, tiles, s);
+    case 64: return rows_bn<64>(g, ta, tb, p, tiles, s);
+    case 192: return rows_bn<192>(g, ta, tb, p, tiles, s);
+    case 32: return rows_bn<32>(g, ta, tb, p, tiles, s);
+    case 48: return rows_bn<48>(g, ta, tb, p, tiles, s);
+    case 96: return rows_bn<96>(g, ta, tb, p, tiles, s);
+    case 16: return rows_bn<16>(g, ta, tb, p, tiles, s);
+    default: return set_error(DMOE_ERR_UNSUPPORTED, "tc_gemm_rows: N=%d", g.N);
+  }
+}
+
 
 template <int NT, bool W_MN, int EPI>
 static dmoe_status launch_rows(const CUtensorMap& w, const CUtensorMap& x, const TcParams& p, int64_t max_tiles,
@@ -942,6 +1006,7 @@ static dmoe_status rows_nt(const GemmRows& g, const CUtensorMap& w, const CUtens
 
 dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
   if (g.max_tiles <= 0) return DMOE_OK;
+  if (!rows_swap()) return tc_gemm_rows_mk(g, s);
   const int NT = tc_rows_tile(g);
   // W (MMA A): K-major [E][N][K] boxes {64 K, 128 features}, or MN-major [E][K][N] boxes
   // {64 features, 64 K} x 2.  X (MMA B): tokens [rows_cap][K], boxes {64 K, NT rows};
