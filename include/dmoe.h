@@ -176,6 +176,23 @@ dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, con
                           dmoe_grid g, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
                           size_t ws_bytes, dmoe_stream_t stream);
 
+/* S11 — expert-parallel exchange, receive side ("send inputs to those workers
+ * and collect outputs"; §3.3 the runtime batches requests per expert).  With experts sharded
+ * over G ranks by contiguous flat index, a rank receives its experts' rows source-rank-major;
+ * recv_counts [G][E_local] (device) gives the rows of local expert e from source s.
+ *   offsets [E_local+1] (out): expert-major segment starts (expert e: source 0's rows, then
+ *     source 1's, ... — the single-GPU token order when sources hold increasing token blocks);
+ *   src_of_dst [R_cap] (out): source-major row index of every expert-major row.
+ * ws >= 8 * G * E_local bytes.  Fails with DMOE_ERR_SHAPE on G < 1 or E_local < 1. */
+dmoe_status dmoe_exchange_layout(const int32_t* recv_counts, int32_t G, int32_t E_local, int64_t R_cap,
+                                 int32_t* offsets, int32_t* src_of_dst, void* ws, size_t ws_bytes,
+                                 dmoe_stream_t stream);
+
+/* Row permutation for the exchange: inverse = 0 gathers dst[r] = src[idx[r]], inverse = 1
+ * scatters dst[idx[r]] = src[r], for r < *n_rows (device int32).  Rows of D elements in dt. */
+dmoe_status dmoe_permute_rows(const void* src, dmoe_dtype dt, const int32_t* idx, const int32_t* n_rows,
+                              int32_t D, int32_t inverse, void* dst, dmoe_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

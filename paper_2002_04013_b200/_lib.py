@@ -50,6 +50,8 @@ _SIGS = {
                              _SZ, _P], ctypes.c_int),
     "dmoe_gate_bwd": ([_P, _P, _P, _P, _P, _P, _I64, _I32, dmoe_grid, _I32, _P, _P, _P, _P, _SZ, _P],
                       ctypes.c_int),
+    "dmoe_exchange_layout": ([_P, _I32, _I32, _I64, _P, _P, _P, _SZ, _P], ctypes.c_int),
+    "dmoe_permute_rows": ([_P, _I32, _P, _P, _I32, _I32, _P, _P], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_L, _name)
@@ -151,3 +153,14 @@ def dmoe_gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, g, dx, dWg, dbg, ws):
     _check("dmoe_gate_bwd", _L.dmoe_gate_bwd(
         _p(x), _p(Wg), _p(sel), _p(dscore), _p(dxd), _p(row_of_slot), T, D, g, _dt(x), _p(dx), _p(dWg),
         _p(dbg), _p(ws), ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_exchange_layout(recv_counts, G, E_local, offsets, src_of_dst, ws):
+    _check("dmoe_exchange_layout", _L.dmoe_exchange_layout(
+        _p(recv_counts), G, E_local, src_of_dst.shape[0], _p(offsets), _p(src_of_dst), _p(ws),
+        ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_permute_rows(src, idx, n_rows, inverse, dst):
+    _check("dmoe_permute_rows", _L.dmoe_permute_rows(_p(src), _dt(src), _p(idx), _p(n_rows), src.shape[1],
+                                                     int(inverse), _p(dst), _stream()))

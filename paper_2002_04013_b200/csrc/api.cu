@@ -63,6 +63,11 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
                      int k, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
                      size_t ws_bytes, cudaStream_t s);
 
+dmoe_status exchange_layout(const int32_t* counts, int G, int El, int32_t* offsets,
+                            int32_t* src_of_dst, int64_t R_cap, void* ws, size_t ws_bytes, cudaStream_t s);
+dmoe_status permute_rows(const void* src, const int32_t* idx, const int32_t* n_rows, int32_t D,
+                         dmoe_dtype dt, int inverse, void* dst, cudaStream_t s);
+
 static dmoe_status check_grid(dmoe_grid* g, int64_t* E) {
   if (g->beam == 0) g->beam = g->k;
   DMOE_REQUIRE(g->d >= 1 && g->d <= 4, DMOE_ERR_SHAPE, "grid: d=%d outside [1,4]", g->d);
@@ -129,7 +134,9 @@ size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_
   size_t disp = dispatch_ws_bytes(T, E);
   size_t ffn = 2 * align_up((size_t)(E_local + 1) * 4, 256) + align_up((size_t)R_cap * H * 4, 256) + 1024;
   size_t gate = gate_bwd_ws_bytes(T, D, g.d * g.M);
+  size_t exch = (size_t)8 * E + 1024;  // exchange tables (G * E_local <= E)
   size_t m = beam;
+  if (exch > m) m = exch;
   if (disp > m) m = disp;
   if (ffn > m) m = ffn;
   if (gate > m) m = gate;
@@ -296,6 +303,24 @@ dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, con
   if (T > 0) { NN(x); NN(sel); NN(dscore); NN(row_of_slot); NN(dx); }
   return gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, T, D, g.d, g.M, g.k, dt, dx, dWg, dbg, ws,
                   ws_bytes, (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_exchange_layout(const int32_t* recv_counts, int32_t G, int32_t E_local, int64_t R_cap,
+                                 int32_t* offsets, int32_t* src_of_dst, void* ws, size_t ws_bytes,
+                                 dmoe_stream_t stream) {
+  DMOE_REQUIRE(G >= 1 && E_local >= 1 && R_cap >= 0, DMOE_ERR_SHAPE, "G=%d E_local=%d", G, E_local);
+  NN(recv_counts); NN(offsets); NN(ws);
+  if (R_cap > 0) NN(src_of_dst);
+  return exchange_layout(recv_counts, G, E_local, offsets, src_of_dst, R_cap, ws, ws_bytes,
+                         (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_permute_rows(const void* src, dmoe_dtype dt, const int32_t* idx, const int32_t* n_rows,
+                              int32_t D, int32_t inverse, void* dst, dmoe_stream_t stream) {
+  DMOE_TRY(check_dt(dt, D));
+  NN(src); NN(idx); NN(n_rows); NN(dst);
+  DMOE_REQUIRE(inverse == 0 || inverse == 1, DMOE_ERR_ARG, "inverse must be 0 or 1");
+  return permute_rows(src, idx, n_rows, D, dt, inverse, dst, (cudaStream_t)stream);
 }
 
 }  // extern "C"
