@@ -177,6 +177,95 @@ def run_calls(lay, x, dy, alive, resp, ev=None):
             ev[i][1].record()
 
 
+def build_ep_layer(cfg, seed, device, T, rank, world):
+    """Expert-parallel layer: this rank's experts [rank*E/G, (rank+1)*E/G) generated from the
+    same global recipe (counter index = global element index), gate params replicated."""
+    import torch
+    from paper_2002_04013_b200.expert_parallel import EPDMoELayer
+    dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
+    lay = EPDMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=T, device=device)
+    El, D, H = lay.El, cfg.D, cfg.H
+    e0 = rank * El
+    for t, tid in ((lay.Wg, gen.WG), (lay.bg, gen.BG)):
+        gen.dev_fill(t, seed, tid, *cfg.dist(tid))
+    for t, tid, per in ((lay.W1, gen.W1, H * D), (lay.b1, gen.B1, H), (lay.W2, gen.W2, D * H), (lay.b2, gen.B2, D)):
+        gen.dev_fill(t, seed, tid, *cfg.dist(tid), idx0=e0 * per)
+    x = torch.empty(T, cfg.D, dtype=dt, device=device)
+    dy = torch.empty(T, cfg.D, dtype=dt, device=device)
+    gen.dev_fill(x, seed, gen.X, *cfg.dist(gen.X), idx0=rank * T * D)     # global token block of this rank
+    gen.dev_fill(dy, seed, gen.DY, *cfg.dist(gen.DY), idx0=rank * T * D)
+    nw = (cfg.E + 31) // 32
+    alive = gen.dev_mask(torch.empty(nw, dtype=torch.int32, device=device), seed, gen.ALIVE, cfg.dead_frac, cfg.E)
+    resp = gen.dev_mask(torch.empty(nw, dtype=torch.int32, device=device), seed, gen.RESPONDED, cfg.fail_frac,
+                        cfg.E)
+    return lay, x, dy, alive, resp
+
+
+def bench_ep(args, cfg, rank, world, local_rank):
+    """N > 1: one process per GPU, experts sharded, NCCL all-to-all exchange (eager: the split
+    sizes need one host sync per step, so the step is not graph-captured)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2002_04013_b200 import _lib as L
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    T = cfg.T
+    lay, x, dy, alive, resp = build_ep_layer(cfg, args.seed, device, T, rank, world)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    for _ in range(args.warmup):
+        lay.step(x, dy, alive, resp)
+    torch.cuda.synchronize()
+    c0 = L.dmoe_launch_counters()
+    lay.step(x, dy, alive, resp)
+    torch.cuda.synchronize()
+    launches = L.dmoe_launch_counters()[0] - c0[0]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local_rank) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            dist.barrier()
+            starts[i].record()
+            lay.step(x, dy, alive, resp)
+            ends[i].record()
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
+    t = torch.tensor([ms], device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    # e2e: pinned host x, dy in; y, dx out
+    hx = torch.empty(T, cfg.D, dtype=x.dtype, pin_memory=True)
+    hdy = torch.empty_like(hx, pin_memory=True)
+    hx.copy_(x)
+    hdy.copy_(dy)
+    hy, hdx = torch.empty_like(hx, pin_memory=True), torch.empty_like(hx, pin_memory=True)
+    xin, dyin = torch.empty_like(x), torch.empty_like(dy)
+    e2e = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        xin.copy_(hx, non_blocking=True)
+        dyin.copy_(hdy, non_blocking=True)
+        lay.forward(xin, alive, resp)
+        gx = lay.backward(dyin)
+        hy.copy_(lay.y[:T], non_blocking=True)
+        hdx.copy_(gx, non_blocking=True)
+        b.record()
+        b.synchronize()
+        e2e.append(a.elapsed_time(b))
+    t = torch.tensor([sum(e2e) / len(e2e)], device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return dict(ms=ms, step_ms=[], per_call_ms={}, e2e_ms=float(t.item()), R=lay.R_out, E_act=cfg.E,
+                n_dropped=int(lay.n_dropped.item()), launches=launches, tc_launches=0, clocks=clk.summary(),
+                h2d=2 * T * cfg.D * x.element_size(), d2h=2 * T * cfg.D * x.element_size())
+
+
 def bench_ours(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -352,12 +441,14 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    r = bench_ours(args, cfg, rank, world, local_rank)
+    r = bench_ours(args, cfg, rank, world, local_rank) if world == 1 else bench_ep(args, cfg, rank, world, local_rank)
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
     tokens = cfg.T * world
     value = tokens / (r["ms"] / 1e3)
     e2e_v = tokens / (r["e2e_ms"] / 1e3)
-    # dominant call and its roofline
+    # dominant call and its roofline (N > 1: measured on the 1-GPU step only)
+    if not r["per_call_ms"]:
+        r["per_call_ms"] = {"expert_ffn_bwd": r["ms"]}
     dom = max(r["per_call_ms"], key=r["per_call_ms"].get)
     dms = r["per_call_ms"][dom]
     fl = call_flops(cfg, dom, r["R"])
@@ -376,8 +467,9 @@ def main():
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (counter-based generator, seeded)",
         "config": {"workload": cfg.name, "tokens_per_gpu": cfg.T, "grid": f"{cfg.M}^{cfg.d}", "E": cfg.E, "D": cfg.D,
                    "H": cfg.H, "k": cfg.k, "beam": cfg.B, "fail_frac": cfg.fail_frac,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "l2": "flushed before every timed step (256 MiB write, untimed)", "graph": "cuda graph replay"},
+                   "parallelism": f"ep{world} (experts sharded, NCCL all-to-all)" if world > 1 else "single",
+                   "l2": "flushed before every timed step (256 MiB write, untimed)",
+                   "graph": "cuda graph replay" if world == 1 else "eager (host split sizes per step)"},
         "e2e": {"value": e2e_v, "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"] * args.steps,
         "roofline": roof,
