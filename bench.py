@@ -182,8 +182,10 @@ def build_ep_layer(cfg, seed, device, T, rank, world):
     same global recipe (counter index = global element index), gate params replicated."""
     import torch
     from paper_2002_04013_b200.expert_parallel import EPDMoELayer
+    from paper_2002_04013_b200.peer_ep import PeerEPDMoELayer
     dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
-    lay = EPDMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=T, device=device)
+    Cls = EPDMoELayer if os.environ.get("DMOE_EP", "peer") == "nccl" else PeerEPDMoELayer
+    lay = Cls(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=T, device=device)
     El, D, H = lay.El, cfg.D, cfg.H
     e0 = rank * El
     for t, tid in ((lay.Wg, gen.WG), (lay.bg, gen.BG)):
@@ -212,26 +214,40 @@ def bench_ep(args, cfg, rank, world, local_rank):
     T = cfg.T
     lay, x, dy, alive, resp = build_ep_layer(cfg, args.seed, device, T, rank, world)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
-    for _ in range(args.warmup):
-        lay.step(x, dy, alive, resp)
-    torch.cuda.synchronize()
+    peer = hasattr(lay, "check")
+    stream = torch.cuda.Stream(device)
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            lay.step(x, dy, alive, resp)
+    stream.synchronize()
     c0 = L.dmoe_launch_counters()
-    lay.step(x, dy, alive, resp)
-    torch.cuda.synchronize()
+    if peer:  # no host sync in the peer exchange: the whole multi-GPU step is one CUDA graph
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            lay.step(x, dy, alive, resp)
+        run = graph.replay
+    else:
+        run = lambda: lay.step(x, dy, alive, resp)
+        with torch.cuda.stream(stream):
+            run()
     launches = L.dmoe_launch_counters()[0] - c0[0]
+    torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local_rank) as clk:
-        for i in range(args.steps):
-            flush.fill_(i & 0xFF)
-            dist.barrier()
-            starts[i].record()
-            lay.step(x, dy, alive, resp)
-            ends[i].record()
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)
+                starts[i].record(stream)
+                run()
+                ends[i].record(stream)
         torch.cuda.synchronize()
     dist.barrier()
+    if peer:
+        lay.check()
     ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / args.steps
     t = torch.tensor([ms], device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -259,9 +275,15 @@ def bench_ep(args, cfg, rank, world, local_rank):
         b.record()
         b.synchronize()
         e2e.append(a.elapsed_time(b))
+    if peer:
+        lay.check()
     t = torch.tensor([sum(e2e) / len(e2e)], device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return dict(ms=ms, step_ms=[], per_call_ms={}, e2e_ms=float(t.item()), R=lay.R_out, E_act=cfg.E,
+    e2e_ms = float(t.item())
+    R_out = int(lay.offsets[cfg.E].item())
+    if peer:
+        lay.close()
+    return dict(ms=ms, step_ms=[], per_call_ms={}, e2e_ms=e2e_ms, R=R_out, E_act=cfg.E,
                 n_dropped=int(lay.n_dropped.item()), launches=launches, tc_launches=0, clocks=clk.summary(),
                 h2d=2 * T * cfg.D * x.element_size(), d2h=2 * T * cfg.D * x.element_size())
 
@@ -467,9 +489,11 @@ def main():
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (counter-based generator, seeded)",
         "config": {"workload": cfg.name, "tokens_per_gpu": cfg.T, "grid": f"{cfg.M}^{cfg.d}", "E": cfg.E, "D": cfg.D,
                    "H": cfg.H, "k": cfg.k, "beam": cfg.B, "fail_frac": cfg.fail_frac,
-                   "parallelism": f"ep{world} (experts sharded, NCCL all-to-all)" if world > 1 else "single",
+                   "parallelism": (f"ep{world} (experts sharded; " + ("NCCL all-to-all" if os.environ.get("DMOE_EP") == "nccl"
+                                   else "NVLink peer-memory exchange") + ")") if world > 1 else "single",
                    "l2": "flushed before every timed step (256 MiB write, untimed)",
-                   "graph": "cuda graph replay" if world == 1 else "eager (host split sizes per step)"},
+                   "graph": "eager (host split sizes per step)" if (world > 1 and os.environ.get("DMOE_EP") == "nccl")
+                   else "cuda graph replay"},
         "e2e": {"value": e2e_v, "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
         "gpu_launches": r["launches"] * args.steps,
         "roofline": roof,

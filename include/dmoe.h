@@ -118,7 +118,8 @@ dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_
  *   counts [E], offsets [E+1] (exclusive scan), row_of_slot [T,k] (-1 if !ok),
  *   token_of_row [R] (capacity T*k), xd [R, D] = x[token_of_row[r]] (capacity T*k rows).
  * x [T, D] in dt; responded_bits [ceil(E/32)] uint32; w [T,k] fp32; valid [T] uint8;
- * n_dropped [1] int32 (device). */
+ * n_dropped [1] int32 (device).  xd may be NULL: the row gather is skipped (the peer exchange
+ * gathers x while sending, dmoe_ep_push_rows). */
 dmoe_status dmoe_dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, dmoe_grid g,
                           const int32_t* sel, const float* sel_score,
                           const uint32_t* responded_bits, float* w, uint8_t* valid,
@@ -192,6 +193,54 @@ dmoe_status dmoe_exchange_layout(const int32_t* recv_counts, int32_t G, int32_t 
  * scatters dst[idx[r]] = src[r], for r < *n_rows (device int32).  Rows of D elements in dt. */
 dmoe_status dmoe_permute_rows(const void* src, dmoe_dtype dt, const int32_t* idx, const int32_t* n_rows,
                               int32_t D, int32_t inverse, void* dst, dmoe_stream_t stream);
+
+/* ---------------------------------------------------------------------------------------
+ * S11 fused form — expert-parallel exchange over NVLink peer memory ("send
+ * inputs to those workers and collect outputs", one process per GPU on one node).
+ * Rows are stored straight into the owner's expert-major receive buffer and outputs straight
+ * back into the source's dispatch-order buffer; completion is signalled by per-source epoch
+ * flags (release/acquire at system scope), so no host sync is needed and a whole step can be
+ * captured in a CUDA graph.  Every buffer below is device memory; the peer-written ones
+ * (flags, cnt and the row buffers passed as peer_dst) must be symmetric (same offsets on every
+ * rank) and mapped on every peer (dmoe_ipc_alloc / dmoe_ipc_open).  A wait that does not
+ * complete within timeout_ns sets err |= 1 and continues (no hang); a receive buffer
+ * overflow (more than rin_cap rows for one owner) sets err |= 2 and skips all row writes.
+ * Each push / return call is collective: every rank calls it with the same phase. */
+typedef struct {
+  int32_t G, rank, E, E_local;  /* E = G * E_local; rank owns experts [rank*E_local, +E_local) */
+  int64_t rin_cap;              /* rows of each rank's expert-major receive buffers            */
+  uint64_t timeout_ns;
+  uint64_t* epoch;              /* [1] step counter (local)                                     */
+  uint64_t* flags;              /* [G] flags written by the peers (symmetric)                   */
+  uint64_t* const* peer_flags;  /* [G] every rank's `flags`                                      */
+  int32_t* cnt;                 /* [G][E] count matrix, row s written by rank s (symmetric)      */
+  int32_t* const* peer_cnt;     /* [G] every rank's `cnt`                                        */
+  int32_t* err;                 /* [1] error word (local)                                        */
+  int32_t* base;                /* [E] plan: this rank's first row in owner(e)'s receive buffer  */
+  int32_t* off_loc;             /* [E_local+1] plan: expert-major segment starts (receive side)  */
+  int32_t* src_off;             /* [G][E_local] plan: source s's rows of own expert, its order   */
+  int32_t* dst_off;             /* [G][E_local] plan: where they sit in the receive buffer       */
+} dmoe_ep;
+
+dmoe_status dmoe_ep_begin(const dmoe_ep* ep, dmoe_stream_t stream); /* epoch += 1 */
+/* C1: broadcast counts [E] (from dmoe_dispatch) into every peer's cnt row `rank`, wait for all
+ * peers, then plan base / off_loc / src_off / dst_off. */
+dmoe_status dmoe_ep_exchange_counts(const dmoe_ep* ep, const int32_t* counts, dmoe_stream_t stream);
+/* C2 / C4: dispatch-order rows (offsets [E+1] from dmoe_dispatch) -> owners' receive buffers
+ * peer_dst [G] (expert-major, off_loc layout).  Row r is src[gather_idx[r]] if gather_idx is
+ * non-NULL (x with token_of_row: the dispatch gather fused with the send), else src[r]. */
+dmoe_status dmoe_ep_push_rows(const dmoe_ep* ep, const void* src, dmoe_dtype dt, const int32_t* gather_idx,
+                              const int32_t* offsets, int32_t D, void* const* peer_dst, int32_t phase,
+                              dmoe_stream_t stream);
+/* C3 / C5: own experts' expert-major rows src [off_loc[E_local], D] -> each source's
+ * dispatch-order buffer peer_dst [G] (the rows it sent, same positions). */
+dmoe_status dmoe_ep_return_rows(const dmoe_ep* ep, const void* src, dmoe_dtype dt, int32_t D,
+                                void* const* peer_dst, int32_t phase, dmoe_stream_t stream);
+/* plumbing: cudaMalloc'ed zeroed arena + its 64-byte IPC handle (host); open / close a peer's */
+dmoe_status dmoe_ipc_alloc(size_t bytes, void** ptr, void* handle);
+dmoe_status dmoe_ipc_open(const void* handle, void** ptr);
+dmoe_status dmoe_ipc_close(void* ptr);
+dmoe_status dmoe_ipc_free(void* ptr);
 
 #ifdef __cplusplus
 }

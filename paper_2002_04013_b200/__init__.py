@@ -1,10 +1,10 @@
 """B200-native DMoE layer hot path (Learning@home, arXiv 2002.04013).
 
-The product is libdmoe.so (C ABI, include/dmoe.h); this package is its thin binding.
+The product is libdmoe.so (C ABI, include/dmoe.h); this package is its thin binding
+(same names as the C functions) plus the layer sequencers DMoELayer (one GPU),
+EPDMoELayer (experts sharded, NCCL exchange) and PeerEPDMoELayer (experts sharded,
+NVLink peer-memory exchange, graph-capturable).
 """
-from ._lib import (  # noqa: F401
-    DMoEError, EXPORTED, LIB_PATH, dmoe_beam_topk, dmoe_combine, dmoe_combine_bwd, dmoe_dispatch,
-    dmoe_expert_ffn_bwd, dmoe_expert_ffn_fwd, dmoe_gate_bwd, dmoe_gate_scores, dmoe_launch_counters, dmoe_version,
-    dmoe_workspace_bytes, dmoe_exchange_layout, dmoe_permute_rows, grid,
-)
+from ._lib import *  # noqa: F401,F403
+from ._lib import DMoEError, EXPORTED, LIB_PATH, grid  # noqa: F401
 from .layer import DMoELayer  # noqa: F401

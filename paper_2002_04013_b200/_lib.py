@@ -25,6 +25,13 @@ class dmoe_grid(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("M", ctypes.c_int32), ("k", ctypes.c_int32), ("beam", ctypes.c_int32)]
 
 
+class dmoe_ep(ctypes.Structure):
+    _fields_ = [("G", ctypes.c_int32), ("rank", ctypes.c_int32), ("E", ctypes.c_int32), ("E_local", ctypes.c_int32),
+                ("rin_cap", ctypes.c_int64), ("timeout_ns", ctypes.c_uint64)] + [
+        (n, ctypes.c_void_p) for n in ("epoch", "flags", "peer_flags", "cnt", "peer_cnt", "err", "base", "off_loc",
+                                       "src_off", "dst_off")]
+
+
 class DMoEError(RuntimeError):
     def __init__(self, fn, status):
         msg = _L.dmoe_last_error().decode()
@@ -51,6 +58,14 @@ _SIGS = {
     "dmoe_gate_bwd": ([_P, _P, _P, _P, _P, _P, _I64, _I32, dmoe_grid, _I32, _P, _P, _P, _P, _SZ, _P],
                       ctypes.c_int),
     "dmoe_exchange_layout": ([_P, _I32, _I32, _I64, _P, _P, _P, _SZ, _P], ctypes.c_int),
+    "dmoe_ep_begin": ([_P, _P], ctypes.c_int),
+    "dmoe_ep_exchange_counts": ([_P, _P, _P], ctypes.c_int),
+    "dmoe_ep_push_rows": ([_P, _P, _I32, _P, _P, _I32, _P, _I32, _P], ctypes.c_int),
+    "dmoe_ep_return_rows": ([_P, _P, _I32, _I32, _P, _I32, _P], ctypes.c_int),
+    "dmoe_ipc_alloc": ([_SZ, _P, _P], ctypes.c_int),
+    "dmoe_ipc_open": ([_P, _P], ctypes.c_int),
+    "dmoe_ipc_close": ([_P], ctypes.c_int),
+    "dmoe_ipc_free": ([_P], ctypes.c_int),
     "dmoe_permute_rows": ([_P, _I32, _P, _P, _I32, _I32, _P, _P], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -59,6 +74,7 @@ for _name, (_args, _res) in _SIGS.items():
     _f.restype = _res
 
 EXPORTED = tuple(_SIGS)
+__all__ = [n for n in _SIGS if n != "dmoe_last_error"] + ["grid", "DMoEError", "dmoe_ep", "dmoe_grid"]
 
 
 def _check(fn, st):
@@ -164,3 +180,44 @@ def dmoe_exchange_layout(recv_counts, G, E_local, offsets, src_of_dst, ws):
 def dmoe_permute_rows(src, idx, n_rows, inverse, dst):
     _check("dmoe_permute_rows", _L.dmoe_permute_rows(_p(src), _dt(src), _p(idx), _p(n_rows), src.shape[1],
                                                      int(inverse), _p(dst), _stream()))
+
+
+# ---------------------------------------------------------------- peer-memory exchange
+def dmoe_ep_begin(ep):
+    _check("dmoe_ep_begin", _L.dmoe_ep_begin(ctypes.byref(ep), _stream()))
+
+
+def dmoe_ep_exchange_counts(ep, counts):
+    _check("dmoe_ep_exchange_counts", _L.dmoe_ep_exchange_counts(ctypes.byref(ep), _p(counts), _stream()))
+
+
+def dmoe_ep_push_rows(ep, src, gather_idx, offsets, peer_dst, phase):
+    _check("dmoe_ep_push_rows", _L.dmoe_ep_push_rows(ctypes.byref(ep), _p(src), _dt(src), _p(gather_idx), _p(offsets),
+                                                     src.shape[1], _p(peer_dst), phase, _stream()))
+
+
+def dmoe_ep_return_rows(ep, src, peer_dst, phase):
+    _check("dmoe_ep_return_rows", _L.dmoe_ep_return_rows(ctypes.byref(ep), _p(src), _dt(src), src.shape[1],
+                                                         _p(peer_dst), phase, _stream()))
+
+
+def dmoe_ipc_alloc(nbytes):
+    ptr = ctypes.c_void_p()
+    handle = (ctypes.c_char * 64)()
+    _check("dmoe_ipc_alloc", _L.dmoe_ipc_alloc(nbytes, ctypes.byref(ptr), handle))
+    return ptr.value, bytes(handle)
+
+
+def dmoe_ipc_open(handle):
+    ptr = ctypes.c_void_p()
+    buf = (ctypes.c_char * 64).from_buffer_copy(handle)
+    _check("dmoe_ipc_open", _L.dmoe_ipc_open(buf, ctypes.byref(ptr)))
+    return ptr.value
+
+
+def dmoe_ipc_close(ptr):
+    _check("dmoe_ipc_close", _L.dmoe_ipc_close(ptr))
+
+
+def dmoe_ipc_free(ptr):
+    _check("dmoe_ipc_free", _L.dmoe_ipc_free(ptr))

@@ -3,6 +3,7 @@
 // kernels; there is no host compute and no fallback outside the GPU.
 #include <stdarg.h>
 #include <stdio.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -67,6 +68,22 @@ dmoe_status exchange_layout(const int32_t* counts, int G, int El, int32_t* offse
                             int32_t* src_of_dst, int64_t R_cap, void* ws, size_t ws_bytes, cudaStream_t s);
 dmoe_status permute_rows(const void* src, const int32_t* idx, const int32_t* n_rows, int32_t D,
                          dmoe_dtype dt, int inverse, void* dst, cudaStream_t s);
+
+dmoe_status ep_begin(uint64_t* epoch, cudaStream_t s);
+dmoe_status ep_signal(uint64_t* const* peer_flags, int G, int rank, const uint64_t* epoch, int phase,
+                      cudaStream_t s);
+dmoe_status ep_wait(const uint64_t* flags, int G, const uint64_t* epoch, int phase, uint64_t timeout_ns,
+                    int32_t* err, cudaStream_t s);
+dmoe_status ep_counts_push(const int32_t* counts, int E, int G, int rank, int32_t* const* peer_cnt,
+                           cudaStream_t s);
+dmoe_status ep_plan(const int32_t* cnt, int G, int rank, int E, int El, int64_t rin_cap, int32_t* base,
+                    int32_t* off_loc, int32_t* src_off, int32_t* dst_off, int32_t* err, cudaStream_t s);
+dmoe_status ep_push_rows(const void* src, const int32_t* gidx, const int32_t* offsets, const int32_t* base,
+                         int E, int El, int32_t D, dmoe_dtype dt, void* const* peer_dst, const int32_t* err,
+                         cudaStream_t s);
+dmoe_status ep_return_rows(const void* src, const int32_t* cnt, const int32_t* off_loc, const int32_t* src_off,
+                           const int32_t* dst_off, int G, int rank, int E, int El, int32_t D, dmoe_dtype dt,
+                           void* const* peer_dst, const int32_t* err, cudaStream_t s);
 
 static dmoe_status check_grid(dmoe_grid* g, int64_t* E) {
   if (g->beam == 0) g->beam = g->k;
@@ -195,7 +212,7 @@ dmoe_status dmoe_dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, dm
   DMOE_TRY(check_dt(dt, D));
   DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
   NN(responded_bits); NN(n_dropped); NN(counts); NN(offsets); NN(ws);
-  if (T > 0) { NN(x); NN(sel); NN(sel_score); NN(w); NN(valid); NN(row_of_slot); NN(token_of_row); NN(xd); }
+  if (T > 0) { NN(x); NN(sel); NN(sel_score); NN(w); NN(valid); NN(row_of_slot); NN(token_of_row); }
   return dispatch(x, dt, T, D, E, g.k, sel, sel_score, responded_bits, w, valid, n_dropped, counts,
                   offsets, row_of_slot, token_of_row, xd, nullptr, nullptr, ws, ws_bytes,
                   (cudaStream_t)stream);
@@ -321,6 +338,90 @@ dmoe_status dmoe_permute_rows(const void* src, dmoe_dtype dt, const int32_t* idx
   NN(src); NN(idx); NN(n_rows); NN(dst);
   DMOE_REQUIRE(inverse == 0 || inverse == 1, DMOE_ERR_ARG, "inverse must be 0 or 1");
   return permute_rows(src, idx, n_rows, D, dt, inverse, dst, (cudaStream_t)stream);
+}
+
+// ------------------------------------------------------------ peer-memory exchange
+static dmoe_status check_ep(const dmoe_ep* ep) {
+  DMOE_REQUIRE(ep != nullptr, DMOE_ERR_ARG, "ep: null");
+  DMOE_REQUIRE(ep->G >= 1 && ep->rank >= 0 && ep->rank < ep->G && ep->E_local >= 1 &&
+                   ep->E == ep->G * ep->E_local && ep->rin_cap >= 0,
+               DMOE_ERR_SHAPE, "ep: G=%d rank=%d E=%d E_local=%d", ep->G, ep->rank, ep->E, ep->E_local);
+  DMOE_REQUIRE(ep->epoch && ep->flags && ep->peer_flags && ep->cnt && ep->peer_cnt && ep->err && ep->base &&
+                   ep->off_loc && ep->src_off && ep->dst_off,
+               DMOE_ERR_ARG, "ep: null buffer");
+  return DMOE_OK;
+}
+
+dmoe_status dmoe_ep_begin(const dmoe_ep* ep, dmoe_stream_t stream) {
+  DMOE_TRY(check_ep(ep));
+  return ep_begin(ep->epoch, (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_ep_exchange_counts(const dmoe_ep* ep, const int32_t* counts, dmoe_stream_t stream) {
+  DMOE_TRY(check_ep(ep));
+  NN(counts);
+  cudaStream_t s = (cudaStream_t)stream;
+  DMOE_TRY(ep_counts_push(counts, ep->E, ep->G, ep->rank, ep->peer_cnt, s));
+  DMOE_TRY(ep_signal(ep->peer_flags, ep->G, ep->rank, ep->epoch, 0, s));
+  DMOE_TRY(ep_wait(ep->flags, ep->G, ep->epoch, 0, ep->timeout_ns, ep->err, s));
+  return ep_plan(ep->cnt, ep->G, ep->rank, ep->E, ep->E_local, ep->rin_cap, ep->base, ep->off_loc, ep->src_off,
+                 ep->dst_off, ep->err, s);
+}
+
+dmoe_status dmoe_ep_push_rows(const dmoe_ep* ep, const void* src, dmoe_dtype dt, const int32_t* gather_idx,
+                              const int32_t* offsets, int32_t D, void* const* peer_dst, int32_t phase,
+                              dmoe_stream_t stream) {
+  DMOE_TRY(check_ep(ep));
+  DMOE_TRY(check_dt(dt, D));
+  NN(src); NN(offsets); NN(peer_dst);
+  DMOE_REQUIRE(phase >= 1 && phase <= 7, DMOE_ERR_ARG, "phase %d outside [1,7]", phase);
+  cudaStream_t s = (cudaStream_t)stream;
+  DMOE_TRY(ep_push_rows(src, gather_idx, offsets, ep->base, ep->E, ep->E_local, D, dt, peer_dst, ep->err, s));
+  DMOE_TRY(ep_signal(ep->peer_flags, ep->G, ep->rank, ep->epoch, phase, s));
+  return ep_wait(ep->flags, ep->G, ep->epoch, phase, ep->timeout_ns, ep->err, s);
+}
+
+dmoe_status dmoe_ep_return_rows(const dmoe_ep* ep, const void* src, dmoe_dtype dt, int32_t D,
+                                void* const* peer_dst, int32_t phase, dmoe_stream_t stream) {
+  DMOE_TRY(check_ep(ep));
+  DMOE_TRY(check_dt(dt, D));
+  NN(src); NN(peer_dst);
+  DMOE_REQUIRE(phase >= 1 && phase <= 7, DMOE_ERR_ARG, "phase %d outside [1,7]", phase);
+  cudaStream_t s = (cudaStream_t)stream;
+  DMOE_TRY(ep_return_rows(src, ep->cnt, ep->off_loc, ep->src_off, ep->dst_off, ep->G, ep->rank, ep->E,
+                          ep->E_local, D, dt, peer_dst, ep->err, s));
+  DMOE_TRY(ep_signal(ep->peer_flags, ep->G, ep->rank, ep->epoch, phase, s));
+  return ep_wait(ep->flags, ep->G, ep->epoch, phase, ep->timeout_ns, ep->err, s);
+}
+
+dmoe_status dmoe_ipc_alloc(size_t bytes, void** ptr, void* handle) {
+  NN(ptr); NN(handle);
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaSuccess) e = cudaMemset(*ptr, 0, bytes);
+  if (e == cudaSuccess) e = cudaIpcGetMemHandle((cudaIpcMemHandle_t*)handle, *ptr);
+  DMOE_REQUIRE(e == cudaSuccess, DMOE_ERR_CUDA, "ipc_alloc: %s", cudaGetErrorString(e));
+  return DMOE_OK;
+}
+
+dmoe_status dmoe_ipc_open(const void* handle, void** ptr) {
+  NN(handle); NN(ptr);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  DMOE_REQUIRE(e == cudaSuccess, DMOE_ERR_CUDA, "ipc_open: %s", cudaGetErrorString(e));
+  return DMOE_OK;
+}
+
+dmoe_status dmoe_ipc_close(void* ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  DMOE_REQUIRE(e == cudaSuccess, DMOE_ERR_CUDA, "ipc_close: %s", cudaGetErrorString(e));
+  return DMOE_OK;
+}
+
+dmoe_status dmoe_ipc_free(void* ptr) {
+  cudaError_t e = cudaFree(ptr);
+  DMOE_REQUIRE(e == cudaSuccess, DMOE_ERR_CUDA, "ipc_free: %s", cudaGetErrorString(e));
+  return DMOE_OK;
 }
 
 }  // extern "C"

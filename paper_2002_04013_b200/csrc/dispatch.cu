@@ -250,6 +250,7 @@ dmoe_status dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, int64_t
     k_rank<<<blocks, kDispWarps * 32, 0, s>>>(sel, responded, T, k, E, hist, offsets, row_of_slot,
                                               token_of_row, nc, kChunkTok);
     DMOE_TRY(check_launch("dispatch.rank"));
+    if (xd == nullptr) return DMOE_OK;  // gather fused into the peer exchange
     const int grid = num_sms() * 8;
     if (dt == DMOE_BF16)
       k_gather<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, token_of_row, offsets, E,

@@ -24,10 +24,11 @@ def _free_port():
     return p
 
 
-def _worker(rank, G, port, q):
+def _worker(rank, G, port, q, kind="nccl", graph=False):
     import torch.distributed as dist
     from harness import to_torch
     from paper_2002_04013_b200.expert_parallel import EPDMoELayer
+    from paper_2002_04013_b200.peer_ep import PeerEPDMoELayer
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
     dist.init_process_group("nccl", rank=rank, world_size=G, device_id=torch.device("cuda", rank))
@@ -35,7 +36,8 @@ def _worker(rank, G, port, q):
     inp = make_inputs(cfg, seed=21)
     T = cfg.T // G
     El = cfg.E // G
-    lay = EPDMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=torch.bfloat16, T_max=T)
+    Cls = PeerEPDMoELayer if kind == "peer" else EPDMoELayer
+    lay = Cls(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=torch.bfloat16, T_max=T)
     D, H, dM = cfg.D, cfg.H, cfg.dM
     lay.Wg.copy_(to_torch(inp["dev_Wg"], "bf16", (D, dM)))
     lay.bg.copy_(torch.from_numpy(inp["dev_bg"]).cuda())
@@ -49,24 +51,45 @@ def _worker(rank, G, port, q):
     dy = to_torch(inp["dev_dY"], "bf16", (cfg.T, D))[rank * T:(rank + 1) * T].contiguous()
     alive = torch.from_numpy(inp["alive_bits"].view(np.int32)).cuda()
     resp = torch.from_numpy(inp["responded_bits"].view(np.int32)).cuda()
-    y = lay.forward(x, alive, resp)
-    dx = lay.backward(dy)
+    if graph:
+        # capture one step in a CUDA graph (peer exchange needs no host sync), replay it twice
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            lay.step(x, dy, alive, resp)                 # warm-up (NCCL communicator init etc.)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            lay.step(x, dy, alive, resp)
+        for _ in range(2):
+            gr.replay()
+        y, dx = lay.y[:T], lay.dx[:T]
+    else:
+        y = lay.forward(x, alive, resp)
+        dx = lay.backward(dy)
     torch.cuda.synchronize()
+    if kind == "peer":
+        lay.check()
     q.put((rank, {n: np64(t) for n, t in dict(y=y, dx=dx, dW1=lay.dW1, dW2=lay.dW2, db1=lay.db1, db2=lay.db2,
                                               dWg=lay.dWg, dbg=lay.dbg).items()}))
     dist.barrier()
+    if kind == "peer":
+        lay.close()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("G", [2])
-def test_ep_equals_single_gpu(G):
+@pytest.mark.parametrize("G,kind,graph", [(2, "nccl", False), (2, "peer", False), (2, "peer", True)])
+def test_ep_equals_single_gpu(G, kind, graph):
+    if torch.cuda.device_count() < G:
+        pytest.skip(f"needs {G} GPUs")
     cfg = CFG
     ref = gpu_layer(cfg, make_inputs(cfg, seed=21))
     one = {n: np64(getattr(ref, n)) for n in ("y", "dx", "dW1", "dW2", "db1", "db2", "dWg", "dbg")}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, G, port, q)) for r in range(G)]
+    ps = [ctx.Process(target=_worker, args=(r, G, port, q, kind, graph)) for r in range(G)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=300) for _ in range(G))
