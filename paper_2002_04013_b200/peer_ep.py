@@ -49,6 +49,8 @@ class PeerEPDMoELayer:
         self.dtype = dtype
         self.T_max = T_max
         self.dev = torch.device(device)
+        if self.dev.index is None:
+            self.dev = torch.device("cuda", torch.cuda.current_device())
         self.g = L.grid(d, M, k, self.beam)
         f32, i32 = torch.float32, torch.int32
         e = lambda *s, dt=dtype: torch.empty(*s, dtype=dt, device=self.dev)
@@ -88,8 +90,8 @@ class PeerEPDMoELayer:
                              ("dret", self.rout_cap * D * es)):
             self._lay[name] = off
             off += al(nbytes)
-        torch.cuda.set_device(self.dev)
-        self.arena, handle = L.dmoe_ipc_alloc(off)
+        with torch.cuda.device(self.dev):
+            self.arena, handle = L.dmoe_ipc_alloc(off)
         handles = [None] * G
         dist.all_gather_object(handles, handle, group=group)
         self.peer_base = []

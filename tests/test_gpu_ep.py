@@ -92,7 +92,17 @@ def test_ep_equals_single_gpu(G, kind, graph):
     ps = [ctx.Process(target=_worker, args=(r, G, port, q, kind, graph)) for r in range(G)]
     for p in ps:
         p.start()
-    res = dict(q.get(timeout=300) for _ in range(G))
+    res = {}
+    import queue
+    while len(res) < G:
+        try:
+            r, out = q.get(timeout=5)
+            res[r] = out
+        except queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in ps):
+                for p in ps:
+                    p.kill()
+                pytest.fail("a rank died")
     for p in ps:
         p.join(timeout=60)
         assert p.exitcode == 0
