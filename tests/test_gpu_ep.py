@@ -37,7 +37,8 @@ def _worker(rank, G, port, q, kind="nccl", graph=False):
     T = cfg.T // G
     El = cfg.E // G
     Cls = PeerEPDMoELayer if kind == "peer" else EPDMoELayer
-    lay = Cls(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=torch.bfloat16, T_max=T)
+    kw = dict(timeout_s=2.0) if kind == "peer" else {}
+    lay = Cls(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=torch.bfloat16, T_max=T, **kw)
     D, H, dM = cfg.D, cfg.H, cfg.dM
     lay.Wg.copy_(to_torch(inp["dev_Wg"], "bf16", (D, dM)))
     lay.bg.copy_(torch.from_numpy(inp["dev_bg"]).cuda())
@@ -69,10 +70,14 @@ def _worker(rank, G, port, q, kind="nccl", graph=False):
         y = lay.forward(x, alive, resp)
         dx = lay.backward(dy)
     torch.cuda.synchronize()
+    err = int(lay.err.item()) if kind == "peer" else 0
+    out = {n: np64(t) for n, t in dict(y=y, dx=dx, dW1=lay.dW1, dW2=lay.dW2, db1=lay.db1, db2=lay.db2,
+                                       dWg=lay.dWg, dbg=lay.dbg).items()}
+    out["err"] = err
     if kind == "peer":
-        lay.check()
-    q.put((rank, {n: np64(t) for n, t in dict(y=y, dx=dx, dW1=lay.dW1, dW2=lay.dW2, db1=lay.db1, db2=lay.db2,
-                                              dWg=lay.dWg, dbg=lay.dbg).items()}))
+        out["epoch"] = int(lay.epoch.item())
+        out["flags"] = lay.flags.cpu().tolist()
+    q.put((rank, out))
     dist.barrier()
     if kind == "peer":
         lay.close()
@@ -108,6 +113,7 @@ def test_ep_equals_single_gpu(G, kind, graph):
         assert p.exitcode == 0
     T, El = cfg.T // G, cfg.E // G
     for r in range(G):
+        assert res[r]["err"] == 0, {k: res[k].get(n) for k in res for n in ("err", "epoch", "flags")}
         assert np.array_equal(res[r]["y"], one["y"][r * T:(r + 1) * T])
         assert np.array_equal(res[r]["dx"], one["dx"][r * T:(r + 1) * T])
         for n in ("dW1", "dW2", "db1", "db2"):
