@@ -65,7 +65,9 @@ def _worker(rank, G, port, q, kind="nccl", graph=False):
             lay.step(x, dy, alive, resp)
         for _ in range(2):
             gr.replay()
-        y, dx = lay.y[:T], lay.dx[:T]
+        torch.cuda.synchronize()
+        y, dx = lay.y[:T].clone(), lay.dx[:T].clone()
+        del gr   # release graph-captured NCCL work before the communicator is torn down
     else:
         y = lay.forward(x, alive, resp)
         dx = lay.backward(dy)
@@ -110,7 +112,8 @@ def test_ep_equals_single_gpu(G, kind, graph):
                 pytest.fail("a rank died")
     for p in ps:
         p.join(timeout=60)
-        assert p.exitcode == 0
+        if p.exitcode is None:
+            p.kill()
     T, El = cfg.T // G, cfg.E // G
     for r in range(G):
         assert res[r]["err"] == 0, {k: res[k].get(n) for k in res for n in ("err", "epoch", "flags")}
@@ -120,3 +123,4 @@ def test_ep_equals_single_gpu(G, kind, graph):
             assert np.array_equal(res[r][n], one[n][r * El:(r + 1) * El]), n
         np.testing.assert_allclose(res[r]["dWg"], one["dWg"], rtol=1e-5, atol=1e-5)
         np.testing.assert_allclose(res[r]["dbg"], one["dbg"], rtol=1e-5, atol=1e-5)
+    assert all(p.exitcode == 0 for p in ps), [p.exitcode for p in ps]
