@@ -72,6 +72,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -281,7 +290,39 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
   if (warp == 0) {
     // ======================= TMA producer =======================
+    // An L2 prefetch cursor runs PF k-blocks ahead of the loads over the same (tile, kb)
+    // sequence, so the loads into the smem ring mostly hit L2 (weights stream from HBM once).
     if (lane == 0) {
+      constexpr int PF = 16;
+      int ptile = blockIdx.x, pkb = 0, pe = 0, pm0 = 0, pn0 = 0, pnkb = 0;
+      int64_t prow0 = 0, prow_end = 0;
+      auto pnext_tile = [&]() {
+        while (ptile < total) {
+          decode(ptile, pe, prow0, prow_end, pm0, pn0, pnkb);
+          if (pnkb > 0) return;
+          ptile += gridDim.x;
+        }
+      };
+      auto prefetch_one = [&]() {
+        if (ptile >= total || (p.dbg & 16)) return;
+        if (SEGK) {
+          const int kr = (int)(prow0 + pkb * TC_BK);
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c) tma_prefetch_2d(&tmB, pn0 + 64 * c, kr);
+        } else if (B_MN) {
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c) tma_prefetch_3d(&tmB, pn0 + 64 * c, pkb * TC_BK, pe);
+        } else {
+          tma_prefetch_3d(&tmB, pkb * TC_BK, pn0, pe);
+        }
+        if (++pkb == pnkb) {
+          pkb = 0;
+          ptile += gridDim.x;
+          pnext_tile();
+        }
+      };
+      pnext_tile();
+      for (int i = 0; i < PF; ++i) prefetch_one();
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -293,6 +334,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_wait(&empty[stage], phase ^ 1);
           if (kb == 0) PROBE(0, it);
           if (kb == nkb - 1) PROBE(1, it);
+          prefetch_one();
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
