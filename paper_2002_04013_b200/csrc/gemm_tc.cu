@@ -885,10 +885,30 @@ static dmoe_status make_map(CUtensorMap* m, const void* ptr, int rank, const uin
 // N tile: 256 when it divides N, else 128; K-major B also takes any N = 16..256 in one tile
 // (the gate, N = d*M) and MN-major B any multiple of 64 up to 256.
 static int pick_bn(int N, bool b_mn) {
+  static int force = -1;
+  if (force < 0) {
+    const char* e = getenv("DMOE_TC_BN");  // experiment override: 128 / 256
+    force = e ? atoi(e) : 0;
+  }
+  if ((force == 128 || force == 256) && N % force == 0) return force;
   if (N % 256 == 0) return 256;
   if (N % 128 == 0) return 128;
   if (N <= 256 && (b_mn ? N % 64 == 0 : N % 16 == 0)) return N;
   return 0;
+}
+
+// N tile of a grouped GEMM with `units` (row tiles or experts x M tiles) per N tile: 256 unless
+// 128 balances the persistent grid markedly better (tiles per SM rounded up to whole waves)
+static int pick_bn_balanced(int N, bool b_mn, int64_t units) {
+  const int bn = pick_bn(N, b_mn);
+  if (bn != 256 || getenv("DMOE_TC_BN")) return bn;
+  const int64_t sms = num_sms();
+  auto eff = [&](int b) {
+    const int64_t tiles = units * (N / b);
+    const int64_t waves = (tiles + sms - 1) / sms;
+    return (double)tiles / (double)(waves * sms);
+  };
+  return eff(128) > eff(256) + 0.08 ? 128 : 256;
 }
 
 static bool rows_swap() {
@@ -977,7 +997,9 @@ static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtens
 
 static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
   if (g.max_tiles <= 0) return DMOE_OK;
-  const int BN = pick_bn(g.N, g.b_mn);
+  // expected row tiles ~ one per expert at <= 128 rows/expert, else rows/128
+  const int64_t units = g.offsets ? (g.rows_cap / TC_BM > g.E ? g.rows_cap / TC_BM : g.E) : g.max_tiles;
+  const int BN = pick_bn_balanced(g.N, g.b_mn, units);
   // A: [rows_cap, K] K-major; rows past the extent are zero-filled by TMA, rows past a
   // segment produce accumulator rows the epilogue never stores.
   CUtensorMap ta, tb;
@@ -1073,7 +1095,7 @@ dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
 }
 
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
-  const int BN = pick_bn(g.N, true);
+  const int BN = pick_bn_balanced(g.N, true, (int64_t)g.E * (g.Mdim / TC_BM));
   CUtensorMap ta, tb;
   // K rows past a segment end (other experts' rows, or capacity rows past R) are zeroed
   // in smem before the MMA; rows past R_cap are zero-filled by TMA.
