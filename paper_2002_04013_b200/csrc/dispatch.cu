@@ -76,24 +76,33 @@ k_weights_hist(const int32_t* __restrict__ sel, const float* __restrict__ sel_sc
   if (lane == 0) chunk_dropped[c] = dropped;
 }
 
-// per expert (one warp): exclusive prefix of hist[:, e] over chunks (in place) -> counts[e]
+// per expert (one warp): exclusive prefix of hist[:, e] over chunks (in place) -> counts[e].
+// Up to 256 chunks per pass: all loads are issued before the dependent scan.
 __global__ void k_scan_chunks(int32_t* __restrict__ hist, int64_t n_chunks, int64_t E,
                               int32_t* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int64_t e = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (e >= E) return;
   int32_t carry = 0;
-  for (int64_t c0 = 0; c0 < n_chunks; c0 += 32) {
-    const int64_t c = c0 + lane;
-    const int32_t v = c < n_chunks ? hist[c * E + e] : 0;
-    int32_t x = v;
+  for (int64_t c0 = 0; c0 < n_chunks; c0 += 256) {
+    int32_t v[8];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+    for (int j = 0; j < 8; ++j) {
+      const int64_t c = c0 + j * 32 + lane;
+      v[j] = c < n_chunks ? hist[c * E + e] : 0;
     }
-    if (c < n_chunks) hist[c * E + e] = carry + x - v;
-    carry += __shfl_sync(0xffffffffu, x, 31);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t c = c0 + j * 32 + lane;
+      int32_t x = v[j];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (c < n_chunks) hist[c * E + e] = carry + x - v[j];
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
   }
   if (lane == 0) counts[e] = carry;
 }

@@ -150,18 +150,24 @@ k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn,
 __global__ void k_dwg_reduce(const float* __restrict__ partial, const float* __restrict__ pb,
                              int64_t nsplit, int32_t D, int dM, float* __restrict__ dWg,
                              float* __restrict__ dbg) {
+  // fixed association: four interleaved partial sums combined in a fixed order
   const int64_t n = (int64_t)D * dM;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n + dM;
        i += (int64_t)gridDim.x * blockDim.x) {
-    float v = 0.0f;
-    if (i < n) {
-      for (int64_t s = 0; s < nsplit; ++s) v += partial[s * n + i];
-      dWg[i] = v;
-    } else {
-      const int64_t col = i - n;
-      for (int64_t s = 0; s < nsplit; ++s) v += pb[s * dM + col];
-      dbg[col] = v;
+    const float* src = i < n ? partial + i : pb + (i - n);
+    const int64_t stride = i < n ? n : dM;
+    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+    int64_t s = 0;
+    for (; s + 4 <= nsplit; s += 4) {
+      a0 += src[(s + 0) * stride];
+      a1 += src[(s + 1) * stride];
+      a2 += src[(s + 2) * stride];
+      a3 += src[(s + 3) * stride];
     }
+    for (; s < nsplit; ++s) a0 += src[s * stride];
+    const float v = (a0 + a1) + (a2 + a3);
+    if (i < n) dWg[i] = v;
+    else dbg[i - n] = v;
   }
 }
 

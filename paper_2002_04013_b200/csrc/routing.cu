@@ -69,14 +69,55 @@ __device__ __forceinline__ void insert_sorted(uint64_t (&top)[WMAX], uint64_t ke
 constexpr int kBeamWarps = 8;
 
 // smem per warp: G row (dM floats) + beam (WMAX x {p, s})
+constexpr int kSmemPAWords = 2048;  // prefix bitmaps up to 64K bits live in smem
+
+// prefix bitmaps into `PA` (smem or global) by the whole CTA; same definition as
+// k_prefix_alive
+__device__ void prefix_alive_cta(const uint32_t* __restrict__ alive, int d, int M, int64_t E, uint32_t* PA) {
+  int64_t wo = 0, n = M;
+  for (int i = 0; i < d; ++i) {
+    const int64_t words = (n + 31) / 32, span = E / n;
+    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) {
+      uint32_t v = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int64_t p = w * 32 + b;
+        if (p >= n) break;
+        bool any = false;
+        for (int64_t e = p * span, e1 = e + span; e < e1 && !any;) {
+          const uint32_t word = alive[e >> 5];
+          const int sh = (int)(e & 31);
+          int64_t take = 32 - sh;
+          if (take > e1 - e) take = e1 - e;
+          const uint32_t mask = (take == 32) ? 0xffffffffu : (((1u << take) - 1u) << sh);
+          any = (word & mask) != 0;
+          e += take;
+        }
+        if (any) v |= 1u << b;
+      }
+      PA[wo + w] = v;
+    }
+    wo += words;
+    n *= M;
+  }
+}
+
 template <int WMAX>
 __global__ void __launch_bounds__(kBeamWarps * 32)
 k_beam_topk(const float* __restrict__ G, int64_t T, int d, int M, int k, int B,
-            const uint32_t* __restrict__ PA, int32_t* __restrict__ sel,
-            float* __restrict__ sel_score) {
+            const uint32_t* __restrict__ PA_global, const uint32_t* __restrict__ alive,
+            int pa_words, int32_t* __restrict__ sel, float* __restrict__ sel_score) {
   extern __shared__ float smem_f[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int dM = d * M;
+  const uint32_t* PA = PA_global;
+  if (PA_global == nullptr) {  // small grids: every CTA builds the bitmaps in smem
+    uint32_t* pa_s = reinterpret_cast<uint32_t*>(smem_f + kBeamWarps * (dM + 2 * WMAX));
+    int64_t E = 1;
+    for (int i = 0; i < d; ++i) E *= M;
+    prefix_alive_cta(alive, d, M, E, pa_s);
+    __syncthreads();
+    PA = pa_s;
+  }
   float* grow = smem_f + warp * (dM + 2 * WMAX);
   int32_t* beam_p = reinterpret_cast<int32_t*>(grow + dM);
   float* beam_s = grow + dM + WMAX;
@@ -106,7 +147,7 @@ k_beam_topk(const float* __restrict__ G, int64_t T, int d, int M, int k, int B,
       for (int c = lane; c < ncand; c += 32) {
         int b = c / M, j = c - b * M;
         int64_t p = (int64_t)beam_p[b] * M + j;
-        if (!((__ldg(pa + (p >> 5)) >> (p & 31)) & 1u)) continue;  // FilterAlive
+        if (!((pa[p >> 5] >> (p & 31)) & 1u)) continue;  // FilterAlive
         float s = beam_s[b] + grow[i * M + j];
         uint64_t key = ((uint64_t)ord_score(s) << 32) | (uint64_t)(0xffffffffu - (uint32_t)p);
         insert_sorted<WMAX>(top, key);
@@ -153,17 +194,19 @@ size_t prefix_words(int d, int M) {
 }
 
 template <int WMAX>
-static dmoe_status launch_beam(const float* G, int64_t T, dmoe_grid g, const uint32_t* PA,
-                               int32_t* sel, float* sel_score, cudaStream_t s) {
+static dmoe_status launch_beam(const float* G, int64_t T, dmoe_grid g, const uint32_t* PA_global,
+                               const uint32_t* alive, int pa_words, int32_t* sel, float* sel_score,
+                               cudaStream_t s) {
   const int dM = g.d * g.M;
   size_t smem = (size_t)kBeamWarps * (dM + 2 * WMAX) * sizeof(float);
+  if (PA_global == nullptr) smem += (size_t)pa_words * 4;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_beam_topk<WMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int64_t blocks = ceil_div(T, kBeamWarps);
   int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  k_beam_topk<WMAX><<<(unsigned)blocks, kBeamWarps * 32, smem, s>>>(G, T, g.d, g.M, g.k, g.beam,
-                                                                     PA, sel, sel_score);
+  k_beam_topk<WMAX><<<(unsigned)blocks, kBeamWarps * 32, smem, s>>>(G, T, g.d, g.M, g.k, g.beam, PA_global,
+                                                                     alive, pa_words, sel, sel_score);
   return check_launch("beam_topk");
 }
 
@@ -171,17 +214,21 @@ dmoe_status beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* al
                       int32_t* sel, float* sel_score, uint32_t* PA, cudaStream_t s) {
   int64_t E = 1;
   for (int i = 0; i < g.d; ++i) E *= g.M;
-  int64_t maxwords = (E + 31) / 32;
-  int blocks = (int)((maxwords + 255) / 256);
-  if (blocks > 1024) blocks = 1024;
-  k_prefix_alive<<<blocks, 256, 0, s>>>(alive_bits, g.d, g.M, E, PA);
-  DMOE_TRY(check_launch("prefix_alive"));
+  const int64_t words = (int64_t)prefix_words(g.d, g.M);
+  const uint32_t* PA_global = nullptr;
+  if (words > kSmemPAWords) {  // big grids: one pass into the workspace, read through L1/L2
+    int blocks = (int)(((E + 31) / 32 + 255) / 256);
+    if (blocks > 1024) blocks = 1024;
+    k_prefix_alive<<<blocks, 256, 0, s>>>(alive_bits, g.d, g.M, E, PA);
+    DMOE_TRY(check_launch("prefix_alive"));
+    PA_global = PA;
+  }
   if (T == 0) return DMOE_OK;
   int w = g.beam > g.k ? g.beam : g.k;
-  if (w <= 4) return launch_beam<4>(G, T, g, PA, sel, sel_score, s);
-  if (w <= 8) return launch_beam<8>(G, T, g, PA, sel, sel_score, s);
-  if (w <= 16) return launch_beam<16>(G, T, g, PA, sel, sel_score, s);
-  return launch_beam<32>(G, T, g, PA, sel, sel_score, s);
+  if (w <= 4) return launch_beam<4>(G, T, g, PA_global, alive_bits, (int)words, sel, sel_score, s);
+  if (w <= 8) return launch_beam<8>(G, T, g, PA_global, alive_bits, (int)words, sel, sel_score, s);
+  if (w <= 16) return launch_beam<16>(G, T, g, PA_global, alive_bits, (int)words, sel, sel_score, s);
+  return launch_beam<32>(G, T, g, PA_global, alive_bits, (int)words, sel, sel_score, s);
 }
 
 }  // namespace dmoe
