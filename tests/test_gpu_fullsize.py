@@ -1,0 +1,143 @@
+"""Parity at BASELINE.json's full sizes, in the configuration bench.py times (one CUDA-graph-free
+eager step of DMoELayer with device-generated inputs, exactly as bench.build_layer builds them).
+
+* mnist (config 2, the bench workload): the whole 4096-token step against the oracle.
+* transformer (config 3: 64x64 grid, 65,536 tokens, 4,096 experts 1024->4096->1024) and
+  grid3d (config 4: 16^3 grid, 262,144 tokens): sampled tokens (routing, y, dX) and sampled
+  experts (dW1, db1, dW2, db2 over all their rows), each computed one by one by the oracle from
+  the same generator (weights regenerated on the host for the touched experts only).
+"""
+import numpy as np
+import pytest
+import torch
+
+import gen
+from gen import CONFIGS
+from gen.inputs import make_inputs
+from harness import GAP, TOL, check_routing, np64, oracle_step, rel_err
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _device_step(cfg, seed=0):
+    import bench
+    lay, x, dy, alive, resp = bench.build_layer(cfg, seed, torch.device("cuda", 0), cfg.T)
+    bench.run_calls(lay, x, dy, alive, resp)
+    torch.cuda.synchronize()
+    return lay
+
+
+def test_mnist_full_step_exact_oracle():
+    cfg = CONFIGS["mnist"]
+    lay = _device_step(cfg)
+    inp = make_inputs(cfg, seed=0)
+    ref = oracle_step(cfg, inp)
+    T = cfg.T
+    check_routing(cfg, np64(lay.sel[:T]), ref, False, inp["alive"])
+    r = oracle_step(cfg, inp, sel_override=np64(lay.sel[:T]))
+    assert np.array_equal(np64(lay.row_of_slot[:T]), r["row_of_slot"])
+    assert np.array_equal(np64(lay.offsets), r["offsets"])
+    for name, got, want in [("y", lay.y[:T], r["y"]), ("dX", lay.dx[:T], r["dX"]), ("dW1", lay.dW1, r["dW1"]),
+                            ("dW2", lay.dW2, r["dW2"]), ("db1", lay.db1, r["db1"]), ("db2", lay.db2, r["db2"]),
+                            ("dWg", lay.dWg, r["dWg"]), ("dbg", lay.dbg, r["dbg"])]:
+        e = rel_err(np64(got), want)
+        assert e <= TOL["bf16"], (name, e)
+
+
+def _host_param(cfg, seed, tid, e, n):
+    dist, scale = cfg.dist(tid)
+    if tid in (gen.B1, gen.B2):
+        return gen.host_f32(seed, tid, dist, scale, n, e * n).astype(np.float64)
+    return gen.bf16_bits_to_f64(gen.host_bf16_bits(seed, tid, dist, scale, n, e * n))
+
+
+def _experts(cfg, seed, ids):
+    D, H = cfg.D, cfg.H
+    W1 = np.stack([_host_param(cfg, seed, gen.W1, e, H * D).reshape(H, D) for e in ids])
+    b1 = np.stack([_host_param(cfg, seed, gen.B1, e, H) for e in ids])
+    W2 = np.stack([_host_param(cfg, seed, gen.W2, e, D * H).reshape(D, H) for e in ids])
+    b2 = np.stack([_host_param(cfg, seed, gen.B2, e, D) for e in ids])
+    return W1, b1, W2, b2
+
+
+def _rows(cfg, seed, tid, tokens):
+    D = cfg.D
+    dist, scale = cfg.dist(tid)
+    return np.stack([gen.bf16_bits_to_f64(gen.host_bf16_bits(seed, tid, dist, scale, D, int(t) * D)) for t in tokens])
+
+
+@pytest.mark.parametrize("name", ["transformer", "grid3d"])
+def test_full_size_sampled(name):
+    cfg = CONFIGS[name]
+    need = 2 * 2 * cfg.E * cfg.D * cfg.H * 2 + cfg.T * cfg.k * (cfg.D * 10 + cfg.H * 6) + (4 << 30)
+    free, _ = torch.cuda.mem_get_info()
+    if need > free:
+        pytest.skip(f"{name}: needs ~{need / 2**30:.0f} GiB of HBM, {free / 2**30:.0f} GiB free")
+    seed = 0
+    lay = _device_step(cfg, seed)
+    T, D, H, k, d, M, E = cfg.T, cfg.D, cfg.H, cfg.k, cfg.d, cfg.M, cfg.E
+    Wg = gen.bf16_bits_to_f64(gen.host_bf16_bits(seed, gen.WG, *cfg.dist(gen.WG), D * cfg.dM)).reshape(D, cfg.dM)
+    bg = np.zeros(cfg.dM)
+    alive = np.ones(E, np.uint8)
+    responded = gen.unpack_mask(gen.host_mask(seed, gen.RESPONDED, cfg.fail_frac, E), E)
+    # ---- sampled tokens: routing, weights, y, dscore, dX
+    toks = np.linspace(0, T - 1, 12).astype(np.int64)
+    X = _rows(cfg, seed, gen.X, toks)
+    dY = _rows(cfg, seed, gen.DY, toks)
+    G = O.gate_scores(X, Wg, bg)
+    sel_o, sc_o, gap = O.select_experts(G, d, M, k, cfg.B, alive)
+    gsel = np64(lay.sel)[toks]
+    mask = gap > GAP
+    assert (gsel[mask] == sel_o[mask]).all(), np.nonzero(~(gsel == sel_o).all(1) & mask)
+    sc = np.where(gsel >= 0, O._scores_of(G, gsel, d, M), -np.inf)
+    w, ok, valid, _ = O.weights(gsel, sc, responded)
+    used = np.unique(gsel[ok == 1])
+    slot = {int(e): i for i, e in enumerate(used)}
+    W1, b1, W2, b2 = _experts(cfg, seed, used)
+    # rows grouped by slot (stable in token order), as the oracle's dispatch defines them
+    pairs = sorted([(slot[int(gsel[t, s])], t, s) for t in range(len(toks)) for s in range(k) if ok[t, s]])
+    seg = np.zeros(len(used) + 1, np.int32)
+    for sl, _, _ in pairs:
+        seg[sl + 1] += 1
+    seg = np.cumsum(seg).astype(np.int32)
+    ros = -np.ones((len(toks), k), np.int32)
+    for r, (sl, t, s) in enumerate(pairs):
+        ros[t, s] = r
+    x_rows = X[[t for _, t, _ in pairs]]
+    a, out = O.ffn_fwd(x_rows, seg, W1, b1, W2, b2)
+    y = O.combine(out, ros, w)
+    g_rows, dscore = O.combine_bwd(dY, out, ros, w)
+    dx_rows, *_ = O.ffn_bwd(x_rows, a, g_rows, seg, W1, W2)
+    dX, _, _ = O.gate_bwd(X, Wg, gsel, dscore, dx_rows, ros, d, M)
+    tol = TOL["bf16"]
+    for nm, got, want in [("w", np64(lay.w)[toks], w), ("y", np64(lay.y)[toks], y),
+                          ("dscore", np64(lay.dscore)[toks], dscore), ("dX", np64(lay.dx)[toks], dX)]:
+        e = rel_err(got, want)
+        assert e <= tol, (nm, e)
+    # ---- sampled experts: weight gradients over all their rows
+    offsets = np64(lay.offsets)
+    tor = np64(lay.token_of_row)
+    counts = np.diff(offsets)
+    cand = np.nonzero(counts > 0)[0]
+    for e in [int(cand[0]), int(cand[len(cand) // 2])]:
+        rows = np.arange(offsets[e], offsets[e + 1])
+        tk = tor[rows]
+        Xe = _rows(cfg, seed, gen.X, tk)
+        dYe = _rows(cfg, seed, gen.DY, tk)
+        Ge = O.gate_scores(Xe, Wg, bg)
+        sel_e = np64(lay.sel)[tk]
+        sc_e = np.where(sel_e >= 0, O._scores_of(Ge, sel_e, d, M), -np.inf)
+        w_e, ok_e, _, _ = O.weights(sel_e, sc_e, responded)
+        wts = np.array([w_e[i, list(sel_e[i]).index(e)] for i in range(len(tk))])
+        W1e, b1e, W2e, b2e = _experts(cfg, seed, [e])
+        a_e, _ = O.ffn_fwd(Xe, np.array([0, len(tk)], np.int32), W1e, b1e, W2e, b2e)
+        _, dW1, db1, dW2, db2 = O.ffn_bwd(Xe, a_e, wts[:, None] * dYe, np.array([0, len(tk)], np.int32), W1e, W2e)
+        for nm, got, want in [("dW1", lay.dW1[e], dW1[0]), ("db1", lay.db1[e], db1[0]), ("dW2", lay.dW2[e], dW2[0]),
+                              ("db2", lay.db2[e], db2[0])]:
+            err = rel_err(np64(got), want)
+            assert err <= tol, (e, nm, err)
+    # an expert with no rows has exactly zero gradients
+    empty = np.nonzero(counts == 0)[0]
+    if len(empty):
+        assert not np64(lay.dW1[int(empty[0])]).any() and not np64(lay.dW2[int(empty[0])]).any()
