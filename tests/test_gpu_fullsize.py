@@ -48,8 +48,8 @@ def test_mnist_full_step_exact_oracle():
 def _host_param(cfg, seed, tid, e, n):
     dist, scale = cfg.dist(tid)
     if tid in (gen.B1, gen.B2):
-        return gen.host_f32(seed, tid, dist, scale, n, e * n).astype(np.float64)
-    return gen.bf16_bits_to_f64(gen.host_bf16_bits(seed, tid, dist, scale, n, e * n))
+        return gen.host_f32(seed, tid, dist, scale, n, int(e) * n).astype(np.float64)
+    return gen.bf16_bits_to_f64(gen.host_bf16_bits(seed, tid, dist, scale, n, int(e) * n))
 
 
 def _experts(cfg, seed, ids):
