@@ -131,12 +131,22 @@ def test_full_size_sampled(name):
         w_e, ok_e, _, _ = O.weights(sel_e, sc_e, responded)
         wts = np.array([w_e[i, list(sel_e[i]).index(e)] for i in range(len(tk))])
         W1e, b1e, W2e, b2e = _experts(cfg, seed, [e])
-        a_e, _ = O.ffn_fwd(Xe, np.array([0, len(tk)], np.int32), W1e, b1e, W2e, b2e)
-        _, dW1, db1, dW2, db2 = O.ffn_bwd(Xe, a_e, wts[:, None] * dYe, np.array([0, len(tk)], np.int32), W1e, W2e)
-        for nm, got, want in [("dW1", lay.dW1[e], dW1[0]), ("db1", lay.db1[e], db1[0]), ("dW2", lay.dW2[e], dW2[0]),
-                              ("db2", lay.db2[e], db2[0])]:
-            err = rel_err(np64(got), want)
-            assert err <= tol, (e, nm, err)
+        a_e, o_e = O.ffn_fwd(Xe, np.array([0, len(tk)], np.int32), W1e, b1e, W2e, b2e)
+        dx_e, dW1, db1, dW2, db2 = O.ffn_bwd(Xe, a_e, wts[:, None] * dYe, np.array([0, len(tk)], np.int32), W1e, W2e)
+        sl = slice(int(offsets[e]), int(offsets[e + 1]))
+        errs = {nm: rel_err(np64(got), want) for nm, got, want in [
+            ("h", lay.h[sl], a_e), ("out", lay.out[sl], o_e), ("dout", lay.dout[sl], wts[:, None] * dYe),
+            ("dxd", lay.dxd[sl], dx_e), ("dW1", lay.dW1[e], dW1[0]), ("db1", lay.db1[e], db1[0]),
+            ("dW2", lay.dW2[e], dW2[0]), ("db2", lay.db2[e], db2[0])]}
+        bad = {k_: v for k_, v in errs.items() if not v <= tol}
+        if bad:  # locate the error inside dW1: which rows/cols
+            g, wnt = np64(lay.dW1[e]), dW1[0]
+            diff = np.abs(g - wnt)
+            rows_bad = np.nonzero(diff.max(1) > tol * np.abs(wnt).max())[0]
+            cols_bad = np.nonzero(diff.max(0) > tol * np.abs(wnt).max())[0]
+            print("expert", e, "rows", len(tk), "offset", offsets[e], "errs", errs, "bad dW1 rows", rows_bad[:20],
+                  len(rows_bad), "cols", cols_bad[:20], len(cols_bad))
+        assert not bad, (e, errs)
     # an expert with no rows has exactly zero gradients
     empty = np.nonzero(counts == 0)[0]
     if len(empty):
