@@ -19,6 +19,10 @@ from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
+# |h| below which the fp32-accumulated pre-activation may round to the other side of 0:
+# K * 2^-24 * sum|x w| ~ 1024 * 6e-8 * 13 < 1e-3 for the configs here (D <= 2048)
+RELU_EPS = 1e-3
+
 
 def _device_step(cfg, seed=0):
     import bench
@@ -132,8 +136,16 @@ def test_full_size_sampled(name):
         wts = np.array([w_e[i, list(sel_e[i]).index(e)] for i in range(len(tk))])
         W1e, b1e, W2e, b2e = _experts(cfg, seed, [e])
         a_e, o_e = O.ffn_fwd(Xe, np.array([0, len(tk)], np.int32), W1e, b1e, W2e, b2e)
-        dx_e, dW1, db1, dW2, db2 = O.ffn_bwd(Xe, a_e, wts[:, None] * dYe, np.array([0, len(tk)], np.int32), W1e, W2e)
         sl = slice(int(offsets[e]), int(offsets[e + 1]))
+        # ReLU decisions (reading X13b): every decision whose oracle pre-activation is
+        # farther than RELU_EPS from 0 must match the kernel's; within RELU_EPS (below the fp32
+        # accumulation noise of a D-term dot product) the oracle takes the kernel's decision.
+        pre = Xe @ W1e[0].T + b1e[0]
+        gpu_pos = np64(lay.h[sl]) > 0
+        near = np.abs(pre) <= RELU_EPS
+        assert np.array_equal(gpu_pos[~near], (pre > 0)[~near])
+        a_e = np.where(near, np.where(gpu_pos, np.maximum(a_e, 1e-30), 0.0), a_e)
+        dx_e, dW1, db1, dW2, db2 = O.ffn_bwd(Xe, a_e, wts[:, None] * dYe, np.array([0, len(tk)], np.int32), W1e, W2e)
         errs = {nm: rel_err(np64(got), want) for nm, got, want in [
             ("h", lay.h[sl], a_e), ("out", lay.out[sl], o_e), ("dout", lay.dout[sl], wts[:, None] * dYe),
             ("dxd", lay.dxd[sl], dx_e), ("dW1", lay.dW1[e], dW1[0]), ("db1", lay.db1[e], db1[0]),
