@@ -394,27 +394,63 @@ def bench_ours(args, cfg, rank, world, local_rank):
 def oracle_sample_tokens(cfg):
     """Bounded CPU sample: ~10-30 s of float64 oracle work for one step's worth of tokens."""
     per_tok = cfg.k * 6.0 * cfg.D * cfg.H + 2.0 * cfg.D * cfg.dM   # multiply-adds per token, fwd+bwd
-    return int(max(16, min(cfg.T, 4e10 / per_tok)))
-
-
-def oracle_inputs(cfg, seed, Ts):
-    from gen.inputs import make_inputs  # generator only (no method arithmetic)
-    return make_inputs(cfg, seed=seed, T=Ts)
+    ts = int(max(16, min(cfg.T, 4e10 / per_tok)))
+    if cfg.E * cfg.D * cfg.H > (1 << 28):
+        # sampled-expert path: <= ~12 GB of float64 expert tensors (W1, W2, dW1, dW2 per touched expert)
+        ts = min(ts, max(8, int(12e9 / (cfg.k * 4 * 8 * cfg.D * cfg.H))))
+    return ts
 
 
 def time_oracle(cfg, seed, steps=1):
+    """The float64 oracle on the first Ts tokens of the step.  Small workloads: the whole layer
+    step with every expert (oracle.layer_step).  Large ones (the full expert set cannot be held in
+    float64): oracle.layer_step_tokens on the sample, weights regenerated for the experts it
+    touches (generation excluded from the timed region)."""
+    from gen.inputs import make_inputs  # generator only (no method arithmetic)
     from oracle import oracle as O
     Ts = oracle_sample_tokens(cfg)
-    inp = oracle_inputs(cfg, seed, Ts)
+    full = cfg.E * cfg.D * cfg.H <= (1 << 28)
     times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        O.layer_step(inp["X"], inp["Wg"], inp["bg"], inp["W1"], inp["b1"], inp["W2"], inp["b2"], inp["dY"],
-                     inp["alive"], inp["responded"], cfg.d, cfg.M, cfg.k, cfg.B)
-        times.append(time.perf_counter() - t0)
+    if full:
+        inp = make_inputs(cfg, seed=seed, T=Ts)
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            O.layer_step(inp["X"], inp["Wg"], inp["bg"], inp["W1"], inp["b1"], inp["W2"], inp["b2"], inp["dY"],
+                         inp["alive"], inp["responded"], cfg.d, cfg.M, cfg.k, cfg.B)
+            times.append(time.perf_counter() - t0)
+        what = f"all {cfg.E} experts' weights"
+    else:
+        inp = make_inputs(cfg, seed=seed, T=Ts, experts=[])
+        D, H = cfg.D, cfg.H
+
+        def host(tid, e, n):
+            dist, scale = cfg.dist(tid)
+            if tid in (gen.B1, gen.B2):
+                return gen.host_f32(seed, tid, dist, scale, n, int(e) * n).astype(np.float64)
+            return gen.bf16_bits_to_f64(gen.host_bf16_bits(seed, tid, dist, scale, n, int(e) * n))
+
+        cache = {}
+
+        def experts(ids):
+            key = tuple(int(i) for i in ids)
+            if key not in cache:
+                cache[key] = (np.stack([host(gen.W1, e, H * D).reshape(H, D) for e in ids]),
+                              np.stack([host(gen.B1, e, H) for e in ids]),
+                              np.stack([host(gen.W2, e, D * H).reshape(D, H) for e in ids]),
+                              np.stack([host(gen.B2, e, D) for e in ids]))
+            return cache[key]
+
+        args = (inp["X"], inp["dY"], inp["Wg"], inp["bg"], experts, inp["alive"], inp["responded"], cfg.d, cfg.M,
+                cfg.k, cfg.B)
+        O.layer_step_tokens(*args)  # materialise the touched experts' weights (untimed)
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            O.layer_step_tokens(*args)
+            times.append(time.perf_counter() - t0)
+        what = "the weights of the experts those tokens select (regenerated, untimed)"
     cores = len(os.sched_getaffinity(0))
-    sample = (f"first {Ts} of {cfg.T} tokens of the '{cfg.name}' step (same seed/recipe), all {cfg.E} experts' "
-              f"weights; float64 oracle forward+backward; value = sample tokens / wall seconds")
+    sample = (f"first {Ts} of {cfg.T} tokens of the '{cfg.name}' step (same seed/recipe), {what}; "
+              f"float64 oracle forward+backward; value = sample tokens / wall seconds")
     return Ts, times, cores, sample
 
 

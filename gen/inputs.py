@@ -37,9 +37,10 @@ def make_inputs(cfg, seed=0, T=None, experts=None):
         b1.append(param("_b1", gen.B1, H, e * H, force_f32=True)); dev["b1"].append(out.pop("dev__b1"))
         W2.append(param("_w2", gen.W2, D * H, e * D * H).reshape(D, H)); dev["W2"].append(out.pop("dev__w2"))
         b2.append(param("_b2", gen.B2, D, e * D, force_f32=True)); dev["b2"].append(out.pop("dev__b2"))
-    out["W1"], out["b1"], out["W2"], out["b2"] = (np.stack(v) for v in (W1, b1, W2, b2))
-    for k_, v in dev.items():
-        out["dev_" + k_] = np.concatenate(v)
+    if len(W1):
+        out["W1"], out["b1"], out["W2"], out["b2"] = (np.stack(v) for v in (W1, b1, W2, b2))
+        for k_, v in dev.items():
+            out["dev_" + k_] = np.concatenate(v)
     out["dY"] = param("dY", gen.DY, T * D).reshape(T, D)
     out["alive_bits"] = gen.host_mask(seed, gen.ALIVE, cfg.dead_frac, E)
     out["responded_bits"] = gen.host_mask(seed, gen.RESPONDED, cfg.fail_frac, E)

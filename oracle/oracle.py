@@ -217,3 +217,34 @@ def _scores_of(G, sel, d, M):
         u = (e // (M ** (d - 1 - i))) % M
         s += np.take_along_axis(G, i * M + u, axis=1)
     return s
+
+
+def layer_step_tokens(X, dY, Wg, bg, experts, alive, responded, d, M, k, B, sel_override=None):
+    """The layer step restricted to a subset of tokens (rows of X / dY), for workloads whose full
+    expert set cannot be materialised in float64: S1-S4 on the given tokens, the experts they
+    select fetched through `experts(ids) -> (W1, b1, W2, b2)` (stacked in `ids` order), S5-S10
+    over those tokens' rows only.  y, w, dscore and dX of each token are exactly the full layer's
+    (a token's outputs depend only on its own routing and the experts' weights); expert
+    gradients cover only the sampled rows.  `sel_override` forces the routing (forced-routing
+    parity).  Returns a dict like layer_step plus `experts` (ids in slot order)."""
+    G = gate_scores(X, Wg, bg)
+    sel, sc, gap = select_experts(G, d, M, k, B, alive)
+    if sel_override is not None:
+        sel = np.ascontiguousarray(sel_override, np.int32)
+        sc = np.where(sel >= 0, _scores_of(G, sel, d, M), -np.inf)
+    w, ok, valid, nd = weights(sel, sc, responded)
+    used = np.unique(sel[ok == 1]).astype(np.int64)
+    slot = -np.ones(M ** d, np.int64)
+    slot[used] = np.arange(len(used))
+    local = np.where(ok == 1, slot[np.where(sel >= 0, sel, 0)], -1).astype(np.int32)
+    # dispatch over the local expert slots (same stable definition as S5)
+    counts, offsets, ros, tor = dispatch(local, ok, max(len(used), 1))
+    W1, b1, W2, b2 = experts(used) if len(used) else (np.zeros((1, 1, 1)),) * 4
+    x_rows = np.asarray(X, np.float64)[tor]
+    a, out = ffn_fwd(x_rows, offsets, W1, b1, W2, b2)
+    y = combine(out, ros, w)
+    g, dscore = combine_bwd(dY, out, ros, w)
+    dx_rows, dW1, db1, dW2, db2 = ffn_bwd(x_rows, a, g, offsets, W1, W2)
+    dX, dWg, dbg = gate_bwd(X, Wg, sel, dscore, dx_rows, ros, d, M)
+    return dict(G=G, sel=sel, sel_score=sc, gap=gap, w=w, ok=ok, valid=valid, n_dropped=nd, experts=used,
+                y=y, dscore=dscore, dX=dX, a=a, out=out, dW1=dW1, db1=db1, dW2=dW2, db2=db2, dWg=dWg, dbg=dbg)

@@ -74,7 +74,7 @@ def _rows(cfg, seed, tid, tokens):
 @pytest.mark.parametrize("name", ["transformer", "grid3d"])
 def test_full_size_sampled(name):
     cfg = CONFIGS[name]
-    need = 2 * 2 * cfg.E * cfg.D * cfg.H * 2 + cfg.T * cfg.k * (cfg.D * 10 + cfg.H * 6) + (4 << 30)
+    need = 2 * 2 * cfg.E * cfg.D * cfg.H * 2 + cfg.T * cfg.k * (cfg.D * 8 + cfg.H * 4) + (4 << 30)
     free, _ = torch.cuda.mem_get_info()
     if need > free:
         pytest.skip(f"{name}: needs ~{need / 2**30:.0f} GiB of HBM, {free / 2**30:.0f} GiB free")
