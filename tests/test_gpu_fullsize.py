@@ -74,6 +74,9 @@ def _rows(cfg, seed, tid, tokens):
 @pytest.mark.parametrize("name", ["transformer", "grid3d"])
 def test_full_size_sampled(name):
     cfg = CONFIGS[name]
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
     need = 2 * 2 * cfg.E * cfg.D * cfg.H * 2 + cfg.T * cfg.k * (cfg.D * 8 + cfg.H * 4) + (4 << 30)
     free, _ = torch.cuda.mem_get_info()
     if need > free:
