@@ -173,7 +173,7 @@ struct TcParams {
 
 constexpr int TC_SMEM_MAX = 227 * 1024;
 constexpr int TC_STAGE_ROW = 144;              // staging row pitch: 128 B of data + 16 B pad
-constexpr int TC_STAGE_WARP = 32 * TC_STAGE_ROW;  // one warp's 32-row staging tile
+constexpr int TC_STAGE_WARP = 5 * 1024;           // one warp's 32-row staging tile (1 KB aligned)
 constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan live in smem
 constexpr int TC_TABLE_LEN = TC_TABLE_E + 4;      // entries per table (16-byte multiple)
 
@@ -185,7 +185,7 @@ template <int BN> struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;       // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
-  static constexpr int FIXED = 1024 /*align*/ + 512 /*barriers*/ + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2 +
+  static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2 +
                                2 * TC_TABLE_LEN * 4 /*offsets + plan tables*/;
   static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = ST > 8 ? 8 : ST;
@@ -199,7 +199,7 @@ __device__ __forceinline__ bool bf16_pos(uint32_t b) { return b != 0 && !(b & 0x
 template <int BN, bool SEGK, bool B_MN, int EPI>
 __global__ void __launch_bounds__(TcCfg<BN>::THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-          const TcParams p) {
+          const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   using Cfg = TcCfg<BN>;
   constexpr int S = Cfg::STAGES;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
@@ -213,7 +213,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 512;
+  uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 1024;  // 1 KB aligned (128B-swizzled TMA stores)
   float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * TC_STAGE_WARP);  // [2][BN]
   int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [E+1]
   int32_t* plan_s = off_s + TC_TABLE_LEN;                               // [E+1]
@@ -527,6 +527,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               if (!((hmask[col >> 5] >> (col & 31)) & 1u)) v[j] = 0.0f;
             }
           }
+          if (SEGK && !OUT_F32) {
+            // 128B-swizzled box row (the TMA store layout): 16-byte chunk q of row `lane`
+            // sits at chunk q ^ (lane & 7)
+#pragma unroll
+            for (int j = 0; j < 16; j += 8) {
+              const int q = (c16 + j) >> 3;
+              *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                  make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                             pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+            }
+            continue;
+          }
           uint8_t* dst = stg + lane * TC_STAGE_ROW + c16 * OUT_ES;
           if (OUT_F32) {
 #pragma unroll
@@ -539,6 +551,21 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                   make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
                              pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
           }
+        }
+        if (SEGK && !OUT_F32) {
+          // full 32 x 64 box: one bulk tensor store; the staging buffer is reused only after
+          // the engine has read it (wait_group.read)
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && !(p.dbg & 1)) {
+            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmC),
+                         "r"(smem_u32(stg)), "r"(n0 + cs), "r"((int)((int64_t)e * p.Mdim + qrow0))
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
+          __syncwarp();
+          continue;
         }
         __syncwarp();
         // staging -> global: lane (r = i*4 + lane/8, piece = lane%8) -> 4 full rows per instruction
@@ -568,6 +595,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     }
   }
 
+  if (SEGK && warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
@@ -956,8 +984,8 @@ static int debug_flags() {
 }
 
 template <int BN, bool SEGK, bool B_MN, int EPI>
-static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int64_t max_tiles,
-                          cudaStream_t s) {
+static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcParams& p,
+                          int64_t max_tiles, cudaStream_t s) {
   auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
   const int smem = TcCfg<BN>::SMEM;
   static bool attr = false;
@@ -970,7 +998,7 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcPa
   TcParams pp = p;
   pp.dbg = debug_flags();
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  kern<<<(unsigned)grid, TcCfg<BN>::THREADS, smem, s>>>(a, b, pp);
+  kern<<<(unsigned)grid, TcCfg<BN>::THREADS, smem, s>>>(a, b, c, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
 }
@@ -978,7 +1006,7 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const TcPa
 template <int BN>
 static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtensorMap& b, const TcParams& p,
                            int64_t tiles, cudaStream_t s) {
-#define DMOE_TC_ROWS(BMN, E_) return launch<BN, false, BMN, E_>(a, b, p, tiles, s)
+#define DMOE_TC_ROWS(BMN, E_) return launch<BN, false, BMN, E_>(a, b, a, p, tiles, s)
 #define DMOE_TC_EPI(BMN)                                   \
   switch (g.epi) {                                         \
     case EPI_F32_BIAS: DMOE_TC_ROWS(BMN, EPI_F32_BIAS);    \
@@ -1106,11 +1134,15 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   uint64_t bdims[2] = {(uint64_t)g.N, rc};
   DMOE_TRY(make_map(&ta, g.A, 2, adims, 64));
   DMOE_TRY(make_map(&tb, g.B, 2, bdims, 64));
+  // output dW [E][Mdim][N] as a 2D [E*Mdim, N] map, 64 x 32 boxes (bulk tensor stores)
+  CUtensorMap tc;
+  uint64_t cdims[2] = {(uint64_t)g.N, (uint64_t)g.E * g.Mdim};
+  DMOE_TRY(make_map(&tc, g.C, 2, cdims, 32));
   TcParams p{};
   p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim;
   const int64_t tiles = (int64_t)g.E * (g.Mdim / TC_BM) * (g.N / BN);
-  if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, p, tiles, s);
-  return launch<128, true, true, EPI_PLAIN>(ta, tb, p, tiles, s);
+  if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
+  return launch<128, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
 }
 
 }  // namespace dmoe
