@@ -517,7 +517,18 @@ def main():
         roof = {"bound": "tensor", "achieved": fl / (dms / 1e3) / 1e12, "peak": tf_sus, "unit": "TFLOP/s"}
     else:
         roof = {"bound": "hbm", "achieved": by / (dms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s"}
-    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": None, "kernel": f"dmoe_{dom}",
+    traffic, traffic_src = None, None
+    import glob
+    tfiles = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_traffic_{cfg.name}.json")))
+    if tfiles and world == 1:
+        try:
+            tj = json.load(open(tfiles[-1]))
+            traffic = tj["per_call"][dom]["bytes"]
+            traffic_src = os.path.relpath(tfiles[-1], ROOT) + " (ncu dram__bytes_read.sum + dram__bytes_write.sum)"
+        except Exception:
+            traffic = None
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic, "traffic_source": traffic_src,
+                 "kernel": f"dmoe_{dom}",
                  "algorithmic_bytes": by, "algorithmic_flops": fl, "ms": dms, "peak_source": peak_src})
     out = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
