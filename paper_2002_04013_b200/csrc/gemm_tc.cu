@@ -72,6 +72,34 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// L2 eviction policies for the bulk copies (createpolicy): streamed-once data evict-first,
+// re-read tiles evict-last
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void tma_load_2d_h(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_h(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                              int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
                : "memory");
@@ -323,6 +351,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       };
       pnext_tile();
       for (int i = 0; i < PF; ++i) prefetch_one();
+      // expert weights stream through once (evict first); token / activation tiles are re-read
+      // across N tiles (evict last).  DMOE_TC_DEBUG=32 disables the hints.
+      const uint64_t pol_stream = (p.dbg & 32) ? l2_policy_last() : l2_policy_first();
+      const uint64_t pol_keep = l2_policy_last();
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -340,18 +372,19 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           if (SEGK) {
             const int kr = (int)(row0 + kb * TC_BK);
-            tma_load_2d(sa, &tmA, &full[stage], m0, kr);
-            tma_load_2d(sa + 8192, &tmA, &full[stage], m0 + 64, kr);
+            tma_load_2d_h(sa, &tmA, &full[stage], m0, kr, pol_keep);
+            tma_load_2d_h(sa + 8192, &tmA, &full[stage], m0 + 64, kr, pol_keep);
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tma_load_2d(sb + c * 8192, &tmB, &full[stage], n0 + 64 * c, kr);
+            for (int c = 0; c < BN / 64; ++c)
+              tma_load_2d_h(sb + c * 8192, &tmB, &full[stage], n0 + 64 * c, kr, pol_keep);
           } else {
-            tma_load_2d(sa, &tmA, &full[stage], kb * TC_BK, (int)row0);
+            tma_load_2d_h(sa, &tmA, &full[stage], kb * TC_BK, (int)row0, pol_keep);
             if (B_MN) {
 #pragma unroll
               for (int c = 0; c < BN / 64; ++c)
-                tma_load_3d(sb + c * 8192, &tmB, &full[stage], n0 + 64 * c, kb * TC_BK, e);
+                tma_load_3d_h(sb + c * 8192, &tmB, &full[stage], n0 + 64 * c, kb * TC_BK, e, pol_stream);
             } else {
-              tma_load_3d(sb, &tmB, &full[stage], kb * TC_BK, n0, e);
+              tma_load_3d_h(sb, &tmB, &full[stage], kb * TC_BK, n0, e, pol_stream);
             }
           }
           if (++stage == S) { stage = 0; phase ^= 1; }
@@ -422,6 +455,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int ew = warp - 4;
     const int q = warp & 3;
     const int c_beg = (ew >> 2) * Cfg::EPI_COLS;
+    const uint64_t pol_out = (p.dbg & 32) ? l2_policy_last() : l2_policy_first();  // dW: written once
     uint8_t* stg = stage_base + ew * TC_STAGE_WARP;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -558,9 +592,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0 && !(p.dbg & 1)) {
-            asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(&tmC),
-                         "r"(smem_u32(stg)), "r"(n0 + cs), "r"((int)((int64_t)e * p.Mdim + qrow0))
-                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                    &tmC),
+                "r"(smem_u32(stg)), "r"(n0 + cs), "r"((int)((int64_t)e * p.Mdim + qrow0)), "l"(pol_out)
+                : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           }
