@@ -8,9 +8,8 @@
 namespace dmoe {
 
 constexpr int kCombWarps = 8;
-constexpr int kMaxK = 16;
 
-template <typename T>
+template <typename T, int kMaxK>
 __global__ void __launch_bounds__(kCombWarps * 32)
 k_combine(const T* __restrict__ out, const int32_t* __restrict__ row_of_slot,
           const float* __restrict__ w, const uint8_t* __restrict__ valid, int64_t Tn, int32_t D,
@@ -21,9 +20,10 @@ k_combine(const T* __restrict__ out, const int32_t* __restrict__ row_of_slot,
        t += (int64_t)gridDim.x * kCombWarps) {
     int32_t rows[kMaxK];
     float ws[kMaxK];
-    for (int s = 0; s < k; ++s) {
-      rows[s] = row_of_slot[t * k + s];
-      ws[s] = w[t * k + s];
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s) {
+      rows[s] = s < k ? row_of_slot[t * k + s] : -1;
+      ws[s] = s < k ? w[t * k + s] : 0.0f;
     }
     const bool ok_tok = valid[t] != 0;
     for (int c = lane * V; c < D; c += 32 * V) {
@@ -31,10 +31,16 @@ k_combine(const T* __restrict__ out, const int32_t* __restrict__ row_of_slot,
 #pragma unroll
       for (int i = 0; i < V; ++i) acc[i] = 0.0f;
       if (ok_tok) {
-        for (int s = 0; s < k; ++s) {
-          if (rows[s] < 0) continue;
+        // issue every slot's row load before accumulating (k independent loads in flight)
+        uint4 u[kMaxK];
+#pragma unroll
+        for (int s = 0; s < kMaxK; ++s)
+          if (s < k && rows[s] >= 0) u[s] = ld_nc_v4(out + (int64_t)rows[s] * D + c);
+#pragma unroll
+        for (int s = 0; s < kMaxK; ++s) {
+          if (s >= k || rows[s] < 0) continue;
           float f[V];
-          unpack16(ld_nc_v4(out + (int64_t)rows[s] * D + c), f, (const T*)nullptr);
+          unpack16(u[s], f, (const T*)nullptr);
 #pragma unroll
           for (int i = 0; i < V; ++i) acc[i] = fmaf(ws[s], f[i], acc[i]);
         }
@@ -44,7 +50,7 @@ k_combine(const T* __restrict__ out, const int32_t* __restrict__ row_of_slot,
   }
 }
 
-template <typename T>
+template <typename T, int kMaxK>
 __global__ void __launch_bounds__(kCombWarps * 32)
 k_combine_bwd(const T* __restrict__ dy, const T* __restrict__ out,
               const int32_t* __restrict__ row_of_slot, const float* __restrict__ w, int64_t Tn,
@@ -55,35 +61,48 @@ k_combine_bwd(const T* __restrict__ dy, const T* __restrict__ out,
        t += (int64_t)gridDim.x * kCombWarps) {
     int32_t rows[kMaxK];
     float ws[kMaxK], a[kMaxK];
-    for (int s = 0; s < k; ++s) {
-      rows[s] = row_of_slot[t * k + s];
-      ws[s] = w[t * k + s];
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s) {
+      rows[s] = s < k ? row_of_slot[t * k + s] : -1;
+      ws[s] = s < k ? w[t * k + s] : 0.0f;
       a[s] = 0.0f;
     }
     // a_s = <dy_t, out_row>, and dout_row = w_s dy_t in the same pass over dy_t
     for (int c = lane * V; c < D; c += 32 * V) {
       float g[V];
-      unpack16(ld_nc_v4(dy + t * D + c), g, (const T*)nullptr);
-      for (int s = 0; s < k; ++s) {
-        if (rows[s] < 0) continue;
+      uint4 u[kMaxK];
+      const uint4 gu = ld_nc_v4(dy + t * D + c);
+#pragma unroll
+      for (int s = 0; s < kMaxK; ++s)
+        if (s < k && rows[s] >= 0) u[s] = ld_nc_v4(out + (int64_t)rows[s] * D + c);
+      unpack16(gu, g, (const T*)nullptr);
+#pragma unroll
+      for (int s = 0; s < kMaxK; ++s) {
+        if (s >= k || rows[s] < 0) continue;
         float f[V], o[V];
-        unpack16(ld_nc_v4(out + (int64_t)rows[s] * D + c), f, (const T*)nullptr);
-        float p = 0.0f;
+        unpack16(u[s], f, (const T*)nullptr);
+        float pr = 0.0f;
 #pragma unroll
         for (int i = 0; i < V; ++i) {
-          p = fmaf(g[i], f[i], p);
+          pr = fmaf(g[i], f[i], pr);
           o[i] = ws[s] * g[i];
         }
-        a[s] += p;
+        a[s] += pr;
         st_v4(dout + (int64_t)rows[s] * D + c, pack16(o, (const T*)nullptr));
       }
     }
     float abar = 0.0f;
-    for (int s = 0; s < k; ++s) {
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s) {
+      if (s >= k) break;
       a[s] = warp_sum(a[s]);
       if (rows[s] >= 0) abar = fmaf(ws[s], a[s], abar);
     }
-    if (lane < k) dscore[t * k + lane] = rows[lane] >= 0 ? ws[lane] * (a[lane] - abar) : 0.0f;
+    float mine = 0.0f;
+#pragma unroll
+    for (int s = 0; s < kMaxK; ++s)
+      if (s == lane && s < k && rows[s] >= 0) mine = ws[s] * (a[s] - abar);
+    if (lane < k) dscore[t * k + lane] = mine;
   }
 }
 
@@ -97,12 +116,15 @@ dmoe_status combine(const void* out, const int32_t* row_of_slot, const float* w,
                     const uint8_t* valid, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* y,
                     cudaStream_t s) {
   if (T == 0) return DMOE_OK;
-  if (dt == DMOE_BF16)
-    k_combine<__nv_bfloat16><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(
-        (const __nv_bfloat16*)out, row_of_slot, w, valid, T, D, k, (__nv_bfloat16*)y);
-  else
-    k_combine<float><<<grid_tokens(T), kCombWarps * 32, 0, s>>>((const float*)out, row_of_slot, w,
-                                                                valid, T, D, k, (float*)y);
+#define DMOE_COMB(KM)                                                                              \
+  if (dt == DMOE_BF16)                                                                             \
+    k_combine<__nv_bfloat16, KM><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(                      \
+        (const __nv_bfloat16*)out, row_of_slot, w, valid, T, D, k, (__nv_bfloat16*)y);            \
+  else                                                                                             \
+    k_combine<float, KM><<<grid_tokens(T), kCombWarps * 32, 0, s>>>((const float*)out, row_of_slot, w, \
+                                                                    valid, T, D, k, (float*)y);
+  if (k <= 4) { DMOE_COMB(4) } else if (k <= 8) { DMOE_COMB(8) } else { DMOE_COMB(16) }
+#undef DMOE_COMB
   return check_launch("combine");
 }
 
@@ -110,13 +132,16 @@ dmoe_status combine_bwd(const void* dy, const void* out, const int32_t* row_of_s
                         const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout,
                         float* dscore, cudaStream_t s) {
   if (T == 0) return DMOE_OK;
-  if (dt == DMOE_BF16)
-    k_combine_bwd<__nv_bfloat16><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(
-        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)out, row_of_slot, w, T, D, k,
-        (__nv_bfloat16*)dout, dscore);
-  else
-    k_combine_bwd<float><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(
+#define DMOE_COMBB(KM)                                                                             \
+  if (dt == DMOE_BF16)                                                                             \
+    k_combine_bwd<__nv_bfloat16, KM><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(                  \
+        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)out, row_of_slot, w, T, D, k,              \
+        (__nv_bfloat16*)dout, dscore);                                                             \
+  else                                                                                             \
+    k_combine_bwd<float, KM><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(                          \
         (const float*)dy, (const float*)out, row_of_slot, w, T, D, k, (float*)dout, dscore);
+  if (k <= 4) { DMOE_COMBB(4) } else if (k <= 8) { DMOE_COMBB(8) } else { DMOE_COMBB(16) }
+#undef DMOE_COMBB
   return check_launch("combine_bwd");
 }
 

@@ -39,9 +39,8 @@ dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt
 }
 
 constexpr int kGbWarps = 8;
-constexpr int kGbMaxK = 16;
 
-template <typename T>
+template <typename T, int kGbMaxK>
 __global__ void __launch_bounds__(kGbWarps * 32)
 k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
               const float* __restrict__ dscore, const T* __restrict__ dxd,
@@ -54,10 +53,11 @@ k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
        t += (int64_t)gridDim.x * kGbWarps) {
     int32_t rows[kGbMaxK], es[kGbMaxK];
     float ds[kGbMaxK];
-    for (int s = 0; s < k; ++s) {
-      rows[s] = row_of_slot[t * k + s];
-      es[s] = sel[t * k + s];
-      ds[s] = dscore[t * k + s];
+#pragma unroll
+    for (int s = 0; s < kGbMaxK; ++s) {
+      rows[s] = s < k ? row_of_slot[t * k + s] : -1;
+      es[s] = s < k ? sel[t * k + s] : -1;
+      ds[s] = s < k ? dscore[t * k + s] : 0.0f;
     }
     // dense dG row (fp32) for dW_g / db_g
     for (int col = lane; col < dM; col += 32) {
@@ -65,24 +65,32 @@ k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
       int div = 1;
       for (int q = i + 1; q < d; ++q) div *= M;
       float v = 0.0f;
-      for (int s = 0; s < k; ++s)
-        if (es[s] >= 0 && (es[s] / div) % M == j) v += ds[s];
+#pragma unroll
+      for (int s = 0; s < kGbMaxK; ++s)
+        if (s < k && es[s] >= 0 && (es[s] / div) % M == j) v += ds[s];
       dG[t * dM + col] = v;
     }
     for (int c = lane * V; c < D; c += 32 * V) {
       float acc[V];
 #pragma unroll
       for (int q = 0; q < V; ++q) acc[q] = 0.0f;
-      for (int s = 0; s < k; ++s) {
-        if (rows[s] >= 0) {
+      {
+        uint4 u[kGbMaxK];
+#pragma unroll
+        for (int s = 0; s < kGbMaxK; ++s)
+          if (s < k && rows[s] >= 0) u[s] = ld_nc_v4(dxd + (int64_t)rows[s] * D + c);
+#pragma unroll
+        for (int s = 0; s < kGbMaxK; ++s) {
+          if (s >= k || rows[s] < 0) continue;
           float f[V];
-          unpack16(ld_nc_v4(dxd + (int64_t)rows[s] * D + c), f, (const T*)nullptr);
+          unpack16(u[s], f, (const T*)nullptr);
 #pragma unroll
           for (int q = 0; q < V; ++q) acc[q] += f[q];
         }
       }
-      for (int s = 0; s < k; ++s) {
-        if (es[s] < 0 || ds[s] == 0.0f) continue;
+#pragma unroll
+      for (int s = 0; s < kGbMaxK; ++s) {
+        if (s >= k || es[s] < 0 || ds[s] == 0.0f) continue;
         int e = es[s];
         for (int i = d - 1; i >= 0; --i) {
           const int col = i * M + (e % M);
@@ -208,14 +216,17 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
   if (T > 0) {
     int64_t b = ceil_div(T, kGbWarps), cap = (int64_t)num_sms() * 16;
     unsigned grid = (unsigned)(b < cap ? b : cap);
-    if (dt == DMOE_BF16)
-      k_gate_bwd_dx<__nv_bfloat16><<<grid, kGbWarps * 32, 0, s>>>(
-          (const __nv_bfloat16*)WgT, sel, dscore, (const __nv_bfloat16*)dxd, row_of_slot, T, D, d, M,
-          k, (__nv_bfloat16*)dx, dG);
-    else
-      k_gate_bwd_dx<float><<<grid, kGbWarps * 32, 0, s>>>((const float*)WgT, sel, dscore,
-                                                          (const float*)dxd, row_of_slot, T, D, d,
-                                                          M, k, (float*)dx, dG);
+#define DMOE_GBDX(KM)                                                                                   \
+    if (dt == DMOE_BF16)                                                                                \
+      k_gate_bwd_dx<__nv_bfloat16, KM><<<grid, kGbWarps * 32, 0, s>>>(                                 \
+          (const __nv_bfloat16*)WgT, sel, dscore, (const __nv_bfloat16*)dxd, row_of_slot, T, D, d, M,   \
+          k, (__nv_bfloat16*)dx, dG);                                                                   \
+    else                                                                                                \
+      k_gate_bwd_dx<float, KM><<<grid, kGbWarps * 32, 0, s>>>((const float*)WgT, sel, dscore,          \
+                                                              (const float*)dxd, row_of_slot, T, D, d, \
+                                                              M, k, (float*)dx, dG);
+    if (k <= 4) { DMOE_GBDX(4) } else if (k <= 8) { DMOE_GBDX(8) } else { DMOE_GBDX(16) }
+#undef DMOE_GBDX
     DMOE_TRY(check_launch("gate_bwd.dx"));
   }
   const int64_t tps = T > 0 ? ceil_div(T, S) : 1;
