@@ -120,8 +120,13 @@ static dmoe_status segk_gemm(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
 constexpr int kPlanBM_SIMT = 64;
 
 // row-tile plans only for the engines the two GEMMs of a call will use
-static dmoe_status plans_for(const GemmRows& a, const GemmRows& b, const int32_t* offsets, int E,
+static dmoe_status plans_for(GemmRows& a, GemmRows& b, const int32_t* offsets, int E,
                              int32_t* plan_tc, int32_t* plan_simt, cudaStream_t s) {
+  // the tcgen05 M-major engine builds its plan in smem for E <= tc_plan_in_kernel_max()
+  if (E <= tc_plan_in_kernel_max()) {
+    if (a.plan == plan_tc) a.plan = nullptr;
+    if (b.plan == plan_tc) b.plan = nullptr;
+  }
   const bool need_tc = a.plan == plan_tc || b.plan == plan_tc;
   const bool need_simt = a.plan == plan_simt || b.plan == plan_simt;
   if (need_tc) DMOE_TRY(tile_plan(offsets, E, tc_rows_tile(a.plan == plan_tc ? a : b), plan_tc, s));

@@ -50,7 +50,8 @@ dmoe_status tile_plan(const int32_t* offsets, int64_t E, int bm, int32_t* plan, 
 dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s);
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s);
 bool tc_rows_supported(const GemmRows& g);
-int tc_rows_tile(const GemmRows& g);  // token rows per tile of the row engine (plan granularity)
+int tc_rows_tile(const GemmRows& g);
+int tc_plan_in_kernel_max();  // experts up to which the M-major engine plans row tiles itself  // token rows per tile of the row engine (plan granularity)
 bool tc_segk_supported(const GemmSegK& g);
 
 }  // namespace dmoe

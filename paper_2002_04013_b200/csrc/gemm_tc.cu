@@ -248,16 +248,51 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // ---- per-expert tables in smem (every role decodes every tile: keep it off the L2 path)
+  // ---- per-expert tables in smem (every role decodes every tile: keep it off the L2 path).
+  // ROWS with plan == nullptr: the row-tile plan (exclusive prefix of ceil(m_e/128)) is built
+  // here with a block scan instead of a separate launch.
   const int32_t* offs = p.offsets;
   const int32_t* plan = p.plan;
+  __shared__ int32_t scan_sh[33];
   if (p.offsets && p.E <= TC_TABLE_E) {
     for (int i = threadIdx.x; i <= p.E; i += blockDim.x) {
       off_s[i] = p.offsets[i];
-      if (!SEGK) plan_s[i] = p.plan[i];
+      if (!SEGK && p.plan) plan_s[i] = p.plan[i];
     }
     offs = off_s;
     plan = plan_s;
+    if (!SEGK && !p.plan) {
+      __syncthreads();
+      const int nw = blockDim.x >> 5;
+      int32_t carry = 0;
+      for (int e0 = 0; e0 < p.E; e0 += blockDim.x) {
+        const int e = e0 + threadIdx.x;
+        const int32_t v = e < p.E ? (off_s[e + 1] - off_s[e] + TC_BM - 1) / TC_BM : 0;
+        int32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) scan_sh[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+          int32_t t = lane < nw ? scan_sh[lane] : 0;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+          }
+          if (lane < nw) scan_sh[lane] = t;
+        }
+        __syncthreads();
+        if (e < p.E) plan_s[e] = carry + (warp > 0 ? scan_sh[warp - 1] : 0) + x - v;
+        carry += scan_sh[nw - 1];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) plan_s[p.E] = carry;
+    }
+    __syncthreads();
   }
 
   // ---- tile space (identical walk in every role)
@@ -265,7 +300,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const int MT = SEGK ? p.Mdim / TC_BM : 0;
   int total;
   if (SEGK) total = p.E * MT * NT;
-  else if (p.offsets) total = p.plan[p.E] * NT;  // (global read: tables are not yet visible)
+  else if (p.offsets) total = plan[p.E] * NT;
   else total = (int)((p.rows_single + TC_BM - 1) / TC_BM) * NT;
 
   if (warp == 0 && lane == 0) {
@@ -974,6 +1009,9 @@ static int pick_bn_balanced(int N, bool b_mn, int64_t units) {
   };
   return eff(128) > eff(256) + 0.08 ? 128 : 256;
 }
+
+static bool rows_swap();
+int tc_plan_in_kernel_max() { return rows_swap() ? 0 : TC_TABLE_E; }
 
 static bool rows_swap() {
   static int v = -1;
