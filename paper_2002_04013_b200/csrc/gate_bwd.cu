@@ -107,12 +107,15 @@ k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
 }
 
 // partial[split][c][col] = sum_{t in split} X[t][c] dG[t][col]; pb[split][col] = sum dG[t][col]
+// Tile: 64 columns of X (c) x 32 columns of dG (col) per CTA, 32 tokens per smem pass, each
+// thread 8 outputs; X and dG rows are read with 16-byte vector loads.
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn, int32_t D, int dM,
               int64_t tok_per_split, float* __restrict__ partial, float* __restrict__ pb) {
   __shared__ float xs[32][65];
   __shared__ float gs[32][33];
+  constexpr int V = Vec16<T>::N;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // ty: 0..7
   const int c0 = blockIdx.x * 64, col0 = blockIdx.y * 32;
   const int64_t split = blockIdx.z;
@@ -123,19 +126,41 @@ k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn,
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
   float bsum = 0.0f;
+  const bool xvec = (c0 + 64 <= D);
+  const bool gvec = (col0 + 32 <= dM) && (dM % 4 == 0);
   for (int64_t tb = t_begin; tb < t_end; tb += 32) {
-    for (int i = threadIdx.x; i < 32 * 64; i += 256) {
-      int r = i / 64, c = i % 64;
-      int64_t t = tb + r;
-      xs[r][c] = (t < t_end && c0 + c < D) ? Elem<T>::load(X + t * D + c0 + c) : 0.0f;
+    // X tile: 32 tokens x 64 columns
+    for (int i = threadIdx.x; i < 32 * (64 / V); i += 256) {
+      const int r = i / (64 / V), cv = (i % (64 / V)) * V;
+      const int64_t t = tb + r;
+      float f[V];
+      if (t < t_end && xvec) {
+        unpack16(ld_nc_v4(X + t * D + c0 + cv), f, (const T*)nullptr);
+      } else {
+#pragma unroll
+        for (int q = 0; q < V; ++q) f[q] = (t < t_end && c0 + cv + q < D) ? Elem<T>::load(X + t * D + c0 + cv + q) : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < V; ++q) xs[r][cv + q] = f[q];
     }
-    for (int i = threadIdx.x; i < 32 * 32; i += 256) {
-      int r = i / 32, c = i % 32;
-      int64_t t = tb + r;
-      gs[r][c] = (t < t_end && col0 + c < dM) ? dG[t * dM + col0 + c] : 0.0f;
+    // dG tile: 32 tokens x 32 columns (fp32)
+    for (int i = threadIdx.x; i < 32 * 8; i += 256) {
+      const int r = i / 8, cv = (i % 8) * 4;
+      const int64_t t = tb + r;
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < t_end) {
+        if (gvec) g = __ldg(reinterpret_cast<const float4*>(dG + t * dM + col0 + cv));
+        else {
+          g.x = col0 + cv + 0 < dM ? dG[t * dM + col0 + cv + 0] : 0.f;
+          g.y = col0 + cv + 1 < dM ? dG[t * dM + col0 + cv + 1] : 0.f;
+          g.z = col0 + cv + 2 < dM ? dG[t * dM + col0 + cv + 2] : 0.f;
+          g.w = col0 + cv + 3 < dM ? dG[t * dM + col0 + cv + 3] : 0.f;
+        }
+      }
+      gs[r][cv] = g.x; gs[r][cv + 1] = g.y; gs[r][cv + 2] = g.z; gs[r][cv + 3] = g.w;
     }
     __syncthreads();
-#pragma unroll 4
+#pragma unroll 8
     for (int r = 0; r < 32; ++r) {
       const float g = gs[r][tx];
 #pragma unroll
@@ -155,27 +180,38 @@ k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn,
   }
 }
 
-__global__ void k_dwg_reduce(const float* __restrict__ partial, const float* __restrict__ pb,
-                             int64_t nsplit, int32_t D, int dM, float* __restrict__ dWg,
-                             float* __restrict__ dbg) {
-  // fixed association: four interleaved partial sums combined in a fixed order
+// out[i] = sum over splits, 8 thread groups x (every 8th split) then a fixed-order combine
+__global__ void __launch_bounds__(256)
+k_dwg_reduce(const float* __restrict__ partial, const float* __restrict__ pb, int64_t nsplit, int32_t D, int dM,
+             float* __restrict__ dWg, float* __restrict__ dbg) {
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t n = (int64_t)D * dM;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n + dM;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t i = blockIdx.x * 32 + lane;  // output index (dWg then dbg)
+  float v = 0.0f;
+  if (i < n + dM) {
     const float* src = i < n ? partial + i : pb + (i - n);
     const int64_t stride = i < n ? n : dM;
-    float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
-    int64_t s = 0;
-    for (; s + 4 <= nsplit; s += 4) {
-      a0 += src[(s + 0) * stride];
-      a1 += src[(s + 1) * stride];
-      a2 += src[(s + 2) * stride];
-      a3 += src[(s + 3) * stride];
+    float a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t sidx = grp + 8 * j;
+      a[j] = sidx < nsplit ? src[sidx * stride] : 0.0f;
     }
-    for (; s < nsplit; ++s) a0 += src[s * stride];
-    const float v = (a0 + a1) + (a2 + a3);
-    if (i < n) dWg[i] = v;
-    else dbg[i - n] = v;
+    for (int64_t s0 = grp + 64; s0 < nsplit; s0 += 64)
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (s0 + 8 * j < nsplit) a[j] += src[(s0 + 8 * j) * stride];
+    v = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  }
+  red[grp][lane] = v;
+  __syncthreads();
+  if (grp == 0 && i < n + dM) {
+    float t = 0.0f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t += red[g][lane];
+    if (i < n) dWg[i] = t;
+    else dbg[i - n] = t;
   }
 }
 
@@ -183,7 +219,7 @@ __global__ void k_dwg_reduce(const float* __restrict__ partial, const float* __r
 static int64_t dwg_splits(int64_t T, int32_t D, int dM) {
   int64_t smax = ((int64_t)8 << 20) / ((int64_t)D * dM);
   if (smax < 1) smax = 1;
-  int64_t s = ceil_div(T, 64);
+  int64_t s = ceil_div(T, 32);
   if (s > smax) s = smax;
   return s < 1 ? 1 : s;
 }
@@ -236,7 +272,7 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
   else
     k_dwg_partial<float><<<pg, 256, 0, s>>>((const float*)x, dG, T, D, dM, tps, part, pb);
   DMOE_TRY(check_launch("gate_bwd.dwg_partial"));
-  k_dwg_reduce<<<(unsigned)ceil_div((int64_t)D * dM + dM, 256), 256, 0, s>>>(part, pb, S, D, dM, dWg, dbg);
+  k_dwg_reduce<<<(unsigned)ceil_div((int64_t)D * dM + dM, 32), 256, 0, s>>>(part, pb, S, D, dM, dWg, dbg);
   return check_launch("gate_bwd.dwg_reduce");
 }
 
