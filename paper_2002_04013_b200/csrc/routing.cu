@@ -71,30 +71,38 @@ constexpr int kBeamWarps = 8;
 // smem per warp: G row (dM floats) + beam (WMAX x {p, s})
 constexpr int kSmemPAWords = 2048;  // prefix bitmaps up to 64K bits live in smem
 
-// prefix bitmaps into `PA` (smem or global) by the whole CTA; same definition as
-// k_prefix_alive
+// any alive expert in [e0, e0 + span)
+__device__ __forceinline__ bool span_any(const uint32_t* __restrict__ alive, int64_t e0, int64_t span) {
+  const int64_t e1 = e0 + span;
+  for (int64_t e = e0; e < e1;) {
+    const uint32_t word = alive[e >> 5];
+    const int sh = (int)(e & 31);
+    int64_t take = 32 - sh;
+    if (take > e1 - e) take = e1 - e;
+    const uint32_t mask = (take == 32) ? 0xffffffffu : (((1u << take) - 1u) << sh);
+    if (word & mask) return true;
+    e += take;
+  }
+  return false;
+}
+
+// prefix bitmaps into `PA` (smem or global) by the whole CTA, one thread per prefix and a
+// warp ballot per 32-bit word; the last level is the alive mask itself.  Same definition as
+// k_prefix_alive (reading X5).
 __device__ void prefix_alive_cta(const uint32_t* __restrict__ alive, int d, int M, int64_t E, uint32_t* PA) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int64_t wo = 0, n = M;
   for (int i = 0; i < d; ++i) {
     const int64_t words = (n + 31) / 32, span = E / n;
-    for (int64_t w = threadIdx.x; w < words; w += blockDim.x) {
-      uint32_t v = 0;
-      for (int b = 0; b < 32; ++b) {
-        const int64_t p = w * 32 + b;
-        if (p >= n) break;
-        bool any = false;
-        for (int64_t e = p * span, e1 = e + span; e < e1 && !any;) {
-          const uint32_t word = alive[e >> 5];
-          const int sh = (int)(e & 31);
-          int64_t take = 32 - sh;
-          if (take > e1 - e) take = e1 - e;
-          const uint32_t mask = (take == 32) ? 0xffffffffu : (((1u << take) - 1u) << sh);
-          any = (word & mask) != 0;
-          e += take;
-        }
-        if (any) v |= 1u << b;
+    if (i == d - 1) {
+      for (int64_t w = threadIdx.x; w < words; w += blockDim.x) PA[wo + w] = alive[w];
+    } else {
+      for (int64_t w = warp; w < words; w += nw) {
+        const int64_t p = w * 32 + lane;
+        const bool any = p < n && span_any(alive, p * span, span);
+        const uint32_t bits = __ballot_sync(0xffffffffu, any);
+        if (lane == 0) PA[wo + w] = bits;
       }
-      PA[wo + w] = v;
     }
     wo += words;
     n *= M;
