@@ -304,11 +304,15 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
   DMOE_TRY(plans_for(g3, g4, offsets, E_local, plan_tc, plan_simt, s));
   DMOE_TRY(rows_gemm(g3, dt, s));
   DMOE_TRY(rows_gemm(g4, dt, s));
-  // dW2_e = dout^T h;  dW1_e = dh^T xd;  db2 / db1 = segment column sums
-  GemmSegK g5{dout, h, dW2, offsets, E_local, D, H, R_cap};
-  GemmSegK g6{dh, xd, dW1, offsets, E_local, H, D, R_cap};
+  // dW2_e = dout^T h;  dW1_e = dh^T xd;  db2 / db1 = segment column sums of dout / dh (on the
+  // tensor-core path: an extra ones-MMA inside the same GEMMs)
+  GemmSegK g5{dout, h, dW2, offsets, E_local, D, H, R_cap, db2};
+  GemmSegK g6{dh, xd, dW1, offsets, E_local, H, D, R_cap, db1};
+  const bool fused = dt == DMOE_BF16 && tc_segk_colsum_supported(g5) && tc_segk_colsum_supported(g6);
+  if (!fused) g5.colsum = g6.colsum = nullptr;
   DMOE_TRY(segk_gemm(g5, dt, s));
   DMOE_TRY(segk_gemm(g6, dt, s));
+  if (fused) return DMOE_OK;
   DMOE_TRY(seg_colsum(dout, dt, offsets, E_local, D, db2, s));
   return seg_colsum(dh, dt, offsets, E_local, H, db1, s);
 }

@@ -36,7 +36,8 @@ struct GemmSegK {
   void* C;        // [E][Mdim][N]
   const int32_t* offsets;
   int E, Mdim, N;
-  int64_t R_cap;  // allocated rows of A and B
+  int64_t R_cap;    // allocated rows of A and B
+  float* colsum;    // optional [E][Mdim] fp32: sum over the segment's rows of A (bias gradient)
 };
 
 dmoe_status simt_gemm_rows(const GemmRows& g, dmoe_dtype dt, cudaStream_t s);
@@ -53,5 +54,6 @@ bool tc_rows_supported(const GemmRows& g);
 int tc_rows_tile(const GemmRows& g);
 int tc_plan_in_kernel_max();  // experts up to which the M-major engine plans row tiles itself  // token rows per tile of the row engine (plan granularity)
 bool tc_segk_supported(const GemmSegK& g);
+bool tc_segk_colsum_supported(const GemmSegK& g);  // the SEGK engine also writes colsum
 
 }  // namespace dmoe

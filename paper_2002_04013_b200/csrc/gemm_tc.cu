@@ -191,6 +191,7 @@ struct TcParams {
   const int32_t* offsets;  // [E+1] or nullptr (single group of rows_single rows)
   const int32_t* plan;     // ROWS: [E+1] row-tile prefix (128-row tiles)
   const float* bias;
+  float* colsum;             // SEGK: optional [E][Mdim] column sums of A (the bias gradient)
   const __nv_bfloat16* aux;  // ReLU mask source [rows, N]
   void* C;
   int E, N, K, Mdim;
@@ -213,11 +214,13 @@ template <int BN> struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;       // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
-  static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2 +
+  static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + ONES_BYTES + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2 +
                                2 * TC_TABLE_LEN * 4 /*offsets + plan tables*/;
   static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = ST > 8 ? 8 : ST;
-  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int TMEM_NEED = 2 * BN + 32;  // 2 accumulators + 2 x 16 columns (SEGK column sums)
+  static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
+  static constexpr int ONES_BYTES = 16 * 128;    // [16 N][64 K] bf16 ones (K-major B operand)
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
 };
 
@@ -241,7 +244,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 1024;  // 1 KB aligned (128B-swizzled TMA stores)
+  uint8_t* ones_s = smem + S * Cfg::STAGE_BYTES + 1024;       // 1 KB aligned constant tile
+  uint8_t* stage_base = ones_s + Cfg::ONES_BYTES;             // 1 KB aligned (128B-swizzled TMA stores)
   float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * TC_STAGE_WARP);  // [2][BN]
   int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [E+1]
   int32_t* plan_s = off_s + TC_TABLE_LEN;                               // [E+1]
@@ -293,6 +297,12 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       if (threadIdx.x == 0) plan_s[p.E] = carry;
     }
     __syncthreads();
+  }
+
+  if (SEGK && p.colsum) {
+    for (int i = threadIdx.x; i < Cfg::ONES_BYTES / 4; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(ones_s)[i] = 0x3F803F80u;  // bf16 1.0 x 2
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
 
   // ---- tile space (identical walk in every role)
@@ -429,6 +439,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   } else if (warp == 1) {
     // ======================= MMA issuer =======================
     constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN);
+    constexpr uint32_t idesc_ones = make_idesc(16, A_MN, false);  // colsum: A^T x ones[16]
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -473,6 +484,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             const uint64_t ad = A_MN ? make_desc(a0 + k * 2048, 8192, 1024) : make_desc(a0 + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(b0 + k * 2048, 8192, 1024) : make_desc(b0 + k * 32, 16, 1024);
             tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            if (SEGK && p.colsum && n0 == 0)
+              tc_mma(tmem_base + 2 * BN + acc * 16, ad, make_desc(smem_u32(ones_s) + k * 32, 16, 1024), idesc_ones,
+                     (kb | k) != 0);
           }
           tc_commit(&empty[stage]);
           if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
@@ -656,6 +670,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
       }
+      if (SEGK && p.colsum && n0 == 0 && c_beg == 0) {
+        // column sums of A over the segment's rows (bias gradient), from the ones-MMA
+        float v = 0.0f;
+        if (has_acc) {
+          uint32_t r[16];
+          TMEM_LD16(tmem_base + ((uint32_t)(q * 32) << 16) + 2 * BN + acc * 16, r);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          v = __uint_as_float(r[0]);
+        }
+        p.colsum[(int64_t)e * p.Mdim + m0 + q * 32 + lane] = v;
+      }
       if (ew == 0 && lane == 0) PROBE(5, it);
       if (has_acc) {
         tc_fence_before();
@@ -825,6 +850,9 @@ k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUten
             const uint64_t ad = W_MN ? make_desc(w0 + k * 2048, 8192, 1024) : make_desc(w0 + k * 32, 16, 1024);
             const uint64_t bd = make_desc(x0 + k * 32, 16, 1024);
             tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            if (SEGK && p.colsum && n0 == 0)
+              tc_mma(tmem_base + 2 * BN + acc * 16, ad, make_desc(smem_u32(ones_s) + k * 32, 16, 1024), idesc_ones,
+                     (kb | k) != 0);
           }
           tc_commit(&empty[stage]);
           if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
@@ -1047,6 +1075,7 @@ bool tc_rows_supported(const GemmRows& g) {
 bool tc_segk_supported(const GemmSegK& g) {
   return g.Mdim % TC_BM == 0 && g.N % 128 == 0 && encode_fn() != nullptr;
 }
+bool tc_segk_colsum_supported(const GemmSegK& g) { return tc_segk_supported(g); }
 
 static int debug_flags() {
   static int f = -1;
@@ -1199,7 +1228,8 @@ dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   // weight-gradient tiles have ~1 K block each: a 128-wide N tile keeps 5 tiles in the smem
   // ring instead of 3 (measured 48 vs 56 us per call at 64 rows/expert)
-  const int BN = getenv("DMOE_TC_BN") ? pick_bn(g.N, true) : (g.N % 128 == 0 ? 128 : pick_bn(g.N, true));
+  int BN = getenv("DMOE_TC_BN") ? pick_bn(g.N, true) : (g.N % 128 == 0 ? 128 : pick_bn(g.N, true));
+  if (g.colsum && BN > 128) BN = 128;  // TMEM: 2 x BN + 2 x 16 columns
   CUtensorMap ta, tb;
   // K rows past a segment end (other experts' rows, or capacity rows past R) are zeroed
   // in smem before the MMA; rows past R_cap are zero-filled by TMA.
@@ -1213,7 +1243,7 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   uint64_t cdims[2] = {(uint64_t)g.N, (uint64_t)g.E * g.Mdim};
   DMOE_TRY(make_map(&tc, g.C, 2, cdims, 32));
   TcParams p{};
-  p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim;
+  p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim; p.colsum = g.colsum;
   const int64_t tiles = (int64_t)g.E * (g.Mdim / TC_BM) * (g.N / BN);
   if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
   return launch<128, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
