@@ -207,6 +207,7 @@ constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan 
 constexpr int TC_TABLE_LEN = TC_TABLE_E + 4;      // entries per table (16-byte multiple)
 
 template <int BN> struct TcCfg {
+  static constexpr int ONES_BYTES = 16 * 128;    // [16 N][64 K] bf16 ones (K-major B operand)
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
   static constexpr int EPI_WARPS = (BN >= 128) ? 8 : 4;   // 2 column halves when wide
   static constexpr int EPI_COLS = BN / (EPI_WARPS / 4);   // columns per epilogue warp
@@ -220,7 +221,6 @@ template <int BN> struct TcCfg {
   static constexpr int STAGES = ST > 8 ? 8 : ST;
   static constexpr int TMEM_NEED = 2 * BN + 32;  // 2 accumulators + 2 x 16 columns (SEGK column sums)
   static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
-  static constexpr int ONES_BYTES = 16 * 128;    // [16 N][64 K] bf16 ones (K-major B operand)
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
 };
 
@@ -850,9 +850,6 @@ k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUten
             const uint64_t ad = W_MN ? make_desc(w0 + k * 2048, 8192, 1024) : make_desc(w0 + k * 32, 16, 1024);
             const uint64_t bd = make_desc(x0 + k * 32, 16, 1024);
             tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
-            if (SEGK && p.colsum && n0 == 0)
-              tc_mma(tmem_base + 2 * BN + acc * 16, ad, make_desc(smem_u32(ones_s) + k * 32, 16, 1024), idesc_ones,
-                     (kb | k) != 0);
           }
           tc_commit(&empty[stage]);
           if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
