@@ -3,6 +3,7 @@
 // kernels; there is no host compute and no fallback outside the GPU.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -308,7 +309,8 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
   // tensor-core path: an extra ones-MMA inside the same GEMMs)
   GemmSegK g5{dout, h, dW2, offsets, E_local, D, H, R_cap, db2};
   GemmSegK g6{dh, xd, dW1, offsets, E_local, H, D, R_cap, db1};
-  const bool fused = dt == DMOE_BF16 && tc_segk_colsum_supported(g5) && tc_segk_colsum_supported(g6);
+  static const bool no_fuse = getenv("DMOE_NO_COLSUM_FUSE") != nullptr;  // A/B experiments
+  const bool fused = !no_fuse && dt == DMOE_BF16 && tc_segk_colsum_supported(g5) && tc_segk_colsum_supported(g6);
   if (!fused) g5.colsum = g6.colsum = nullptr;
   DMOE_TRY(segk_gemm(g5, dt, s));
   DMOE_TRY(segk_gemm(g6, dt, s));
