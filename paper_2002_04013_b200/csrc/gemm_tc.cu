@@ -219,8 +219,9 @@ template <int BN> struct TcCfg {
                                2 * TC_TABLE_LEN * 4 /*offsets + plan tables*/;
   static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = ST > 8 ? 8 : ST;
-  static constexpr int TMEM_NEED = 2 * BN + 32;  // 2 accumulators + 2 x 16 columns (SEGK column sums)
-  static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128 : TMEM_NEED <= 256 ? 256 : 512;
+  static constexpr int pow2cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
+  static constexpr int TMEM_COLS = pow2cols(2 * BN);            // 2 accumulators
+  static constexpr int TMEM_COLS_CS = pow2cols(2 * BN + 32);    // + 2 x 16 columns (SEGK column sums)
   static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
 };
 
@@ -322,9 +323,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], Cfg::EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  const uint32_t tmem_cols = (SEGK && p.colsum) ? Cfg::TMEM_COLS_CS : Cfg::TMEM_COLS;
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(Cfg::TMEM_COLS));
+                 "r"(tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -696,7 +698,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
   }
 }
 
