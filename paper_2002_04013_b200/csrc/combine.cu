@@ -14,6 +14,7 @@ __global__ void __launch_bounds__(kCombWarps * 32)
 k_combine(const T* __restrict__ out, const int32_t* __restrict__ row_of_slot,
           const float* __restrict__ w, const uint8_t* __restrict__ valid, int64_t Tn, int32_t D,
           int k, T* __restrict__ y) {
+  DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
   const int lane = threadIdx.x & 31;
   for (int64_t t = blockIdx.x * (int64_t)kCombWarps + (threadIdx.x >> 5); t < Tn;
@@ -55,6 +56,7 @@ __global__ void __launch_bounds__(kCombWarps * 32)
 k_combine_bwd(const T* __restrict__ dy, const T* __restrict__ out,
               const int32_t* __restrict__ row_of_slot, const float* __restrict__ w, int64_t Tn,
               int32_t D, int k, T* __restrict__ dout, float* __restrict__ dscore) {
+  DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
   const int lane = threadIdx.x & 31;
   for (int64_t t = blockIdx.x * (int64_t)kCombWarps + (threadIdx.x >> 5); t < Tn;
@@ -118,10 +120,10 @@ dmoe_status combine(const void* out, const int32_t* row_of_slot, const float* w,
   if (T == 0) return DMOE_OK;
 #define DMOE_COMB(KM)                                                                              \
   if (dt == DMOE_BF16)                                                                             \
-    k_combine<__nv_bfloat16, KM><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(                      \
+    launch_pdl(k_combine<__nv_bfloat16, KM>, grid_tokens(T), kCombWarps * 32, 0, s, \
         (const __nv_bfloat16*)out, row_of_slot, w, valid, T, D, k, (__nv_bfloat16*)y);            \
   else                                                                                             \
-    k_combine<float, KM><<<grid_tokens(T), kCombWarps * 32, 0, s>>>((const float*)out, row_of_slot, w, \
+    launch_pdl(k_combine<float, KM>, grid_tokens(T), kCombWarps * 32, 0, s, (const float*)out, row_of_slot, w, \
                                                                     valid, T, D, k, (float*)y);
   if (k <= 4) { DMOE_COMB(4) } else if (k <= 8) { DMOE_COMB(8) } else { DMOE_COMB(16) }
 #undef DMOE_COMB
@@ -134,11 +136,11 @@ dmoe_status combine_bwd(const void* dy, const void* out, const int32_t* row_of_s
   if (T == 0) return DMOE_OK;
 #define DMOE_COMBB(KM)                                                                             \
   if (dt == DMOE_BF16)                                                                             \
-    k_combine_bwd<__nv_bfloat16, KM><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(                  \
+    launch_pdl(k_combine_bwd<__nv_bfloat16, KM>, grid_tokens(T), kCombWarps * 32, 0, s, \
         (const __nv_bfloat16*)dy, (const __nv_bfloat16*)out, row_of_slot, w, T, D, k,              \
         (__nv_bfloat16*)dout, dscore);                                                             \
   else                                                                                             \
-    k_combine_bwd<float, KM><<<grid_tokens(T), kCombWarps * 32, 0, s>>>(                          \
+    launch_pdl(k_combine_bwd<float, KM>, grid_tokens(T), kCombWarps * 32, 0, s, \
         (const float*)dy, (const float*)out, row_of_slot, w, T, D, k, (float*)dout, dscore);
   if (k <= 4) { DMOE_COMBB(4) } else if (k <= 8) { DMOE_COMBB(8) } else { DMOE_COMBB(16) }
 #undef DMOE_COMBB

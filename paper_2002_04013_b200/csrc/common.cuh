@@ -26,6 +26,36 @@ int num_sms();
     if (_s != DMOE_OK) return _s;          \
   } while (0)
 
+// ------------------------------------------------- programmatic dependent launch (PDL)
+// Every library kernel is launched with programmatic stream serialization and starts with
+// DMOE_PDL_ENTRY(): it lets the next kernel in the stream be scheduled at once
+// (griddepcontrol.launch_dependents) and waits for the previous kernel to complete and its
+// writes to be visible (griddepcontrol.wait) before touching global memory.  The next kernel's
+// CTAs can only be scheduled after all of this grid's CTAs have started, so no deadlock; the
+// launch latency of back-to-back small kernels overlaps the predecessor's tail.  Captured
+// into CUDA graphs as programmatic edges.
+#define DMOE_PDL_ENTRY()                                                 \
+  do {                                                                   \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");      \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                   \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- element access
 template <typename T> struct Elem;
 template <> struct Elem<float> {

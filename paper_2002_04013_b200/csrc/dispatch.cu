@@ -35,6 +35,7 @@ k_weights_hist(const int32_t* __restrict__ sel, const float* __restrict__ sel_sc
                const uint32_t* __restrict__ responded, int64_t T, int k, int64_t E,
                float* __restrict__ w, uint8_t* __restrict__ valid, int32_t* __restrict__ hist,
                int32_t* __restrict__ chunk_dropped, int64_t n_chunks, int64_t kChunkTok) {
+  DMOE_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t c = blockIdx.x * (int64_t)kDispWarps + (threadIdx.x >> 5);
   if (c >= n_chunks) return;
@@ -80,6 +81,7 @@ k_weights_hist(const int32_t* __restrict__ sel, const float* __restrict__ sel_sc
 // Up to 256 chunks per pass: all loads are issued before the dependent scan.
 __global__ void k_scan_chunks(int32_t* __restrict__ hist, int64_t n_chunks, int64_t E,
                               int32_t* __restrict__ counts) {
+  DMOE_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t e = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (e >= E) return;
@@ -141,6 +143,7 @@ k_scan_experts(const int32_t* __restrict__ counts, int64_t E, int32_t* __restric
                int32_t* __restrict__ plan128, int32_t* __restrict__ plan64,
                const int32_t* __restrict__ chunk_dropped, int64_t n_chunks,
                int32_t* __restrict__ n_dropped) {
+  DMOE_PDL_ENTRY();
   __shared__ int32_t sh[32];
   int32_t carry = 0, carry128 = 0, carry64 = 0;
   for (int64_t e0 = 0; e0 < E; e0 += blockDim.x) {
@@ -179,6 +182,7 @@ k_rank(const int32_t* __restrict__ sel, const uint32_t* __restrict__ responded, 
        int64_t E, int32_t* __restrict__ hist, const int32_t* __restrict__ offsets,
        int32_t* __restrict__ row_of_slot, int32_t* __restrict__ token_of_row, int64_t n_chunks,
        int64_t kChunkTok) {
+  DMOE_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t c = blockIdx.x * (int64_t)kDispWarps + (threadIdx.x >> 5);
   if (c >= n_chunks) return;
@@ -215,6 +219,7 @@ template <typename T>
 __global__ void k_gather(const T* __restrict__ x, const int32_t* __restrict__ token_of_row,
                          const int32_t* __restrict__ offsets, int64_t E, int32_t D,
                          T* __restrict__ xd) {
+  DMOE_PDL_ENTRY();
   const int64_t R = offsets[E];
   constexpr int V = Vec16<T>::N;
   const int vecs = D / V;  // D % V == 0 checked by the caller
@@ -247,25 +252,25 @@ dmoe_status dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, int64_t
   DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "dispatch: workspace too small (%zu < %zu)", ws_bytes, cv.used);
   const unsigned blocks = (unsigned)ceil_div(nc, kDispWarps);
   if (nc > 0) {
-    k_weights_hist<<<blocks, kDispWarps * 32, 0, s>>>(sel, sel_score, responded, T, k, E, w, valid,
+    launch_pdl(k_weights_hist, blocks, kDispWarps * 32, 0, s, sel, sel_score, responded, T, k, E, w, valid,
                                                        hist, cdrop, nc, kChunkTok);
     DMOE_TRY(check_launch("dispatch.weights_hist"));
   }
-  k_scan_chunks<<<(unsigned)ceil_div(E, 8), 256, 0, s>>>(hist, nc, E, counts);
+  launch_pdl(k_scan_chunks, (unsigned)ceil_div(E, 8), 256, 0, s, hist, nc, E, counts);
   DMOE_TRY(check_launch("dispatch.scan_chunks"));
-  k_scan_experts<<<1, 1024, 0, s>>>(counts, E, offsets, plan128, plan64, cdrop, nc, n_dropped);
+  launch_pdl(k_scan_experts, 1, 1024, 0, s, counts, E, offsets, plan128, plan64, cdrop, nc, n_dropped);
   DMOE_TRY(check_launch("dispatch.scan_experts"));
   if (nc > 0) {
-    k_rank<<<blocks, kDispWarps * 32, 0, s>>>(sel, responded, T, k, E, hist, offsets, row_of_slot,
+    launch_pdl(k_rank, blocks, kDispWarps * 32, 0, s, sel, responded, T, k, E, hist, offsets, row_of_slot,
                                               token_of_row, nc, kChunkTok);
     DMOE_TRY(check_launch("dispatch.rank"));
     if (xd == nullptr) return DMOE_OK;  // gather fused into the peer exchange
     const int grid = num_sms() * 8;
     if (dt == DMOE_BF16)
-      k_gather<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)x, token_of_row, offsets, E,
+      launch_pdl(k_gather<__nv_bfloat16>, grid, 256, 0, s, (const __nv_bfloat16*)x, token_of_row, offsets, E,
                                                    D, (__nv_bfloat16*)xd);
     else
-      k_gather<float><<<grid, 256, 0, s>>>((const float*)x, token_of_row, offsets, E, D, (float*)xd);
+      launch_pdl(k_gather<float>, grid, 256, 0, s, (const float*)x, token_of_row, offsets, E, D, (float*)xd);
     DMOE_TRY(check_launch("dispatch.gather"));
   }
   return DMOE_OK;
@@ -276,6 +281,7 @@ dmoe_status dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, int64_t
 // sum_{e'<e} ceil((offsets[e'+1]-offsets[e'])/bm)
 __global__ void __launch_bounds__(1024)
 k_tile_plan(const int32_t* __restrict__ offsets, int64_t E, int bm, int32_t* __restrict__ plan) {
+  DMOE_PDL_ENTRY();
   __shared__ int32_t sh[32];
   int32_t carry = 0;
   for (int64_t e0 = 0; e0 < E; e0 += blockDim.x) {
@@ -290,7 +296,7 @@ k_tile_plan(const int32_t* __restrict__ offsets, int64_t E, int bm, int32_t* __r
 }
 
 dmoe_status tile_plan(const int32_t* offsets, int64_t E, int bm, int32_t* plan, cudaStream_t s) {
-  k_tile_plan<<<1, 1024, 0, s>>>(offsets, E, bm, plan);
+  launch_pdl(k_tile_plan, 1, 1024, 0, s, offsets, E, bm, plan);
   return check_launch("tile_plan");
 }
 

@@ -45,6 +45,7 @@ __device__ int32_t xblock_excl_scan(int32_t v, int32_t* sh, int32_t* total) {
 __global__ void __launch_bounds__(1024)
 k_exchange_tables(const int32_t* __restrict__ counts, int G, int El, int32_t* __restrict__ offsets,
                   int32_t* __restrict__ src_off, int32_t* __restrict__ dst_off) {
+  DMOE_PDL_ENTRY();
   __shared__ int32_t sh[32];
   int32_t carry = 0, tot;
   for (int i0 = 0; i0 < G * El; i0 += blockDim.x) {
@@ -76,6 +77,7 @@ k_exchange_tables(const int32_t* __restrict__ counts, int G, int El, int32_t* __
 __global__ void k_exchange_index(const int32_t* __restrict__ counts, int G, int El,
                                  const int32_t* __restrict__ offsets, const int32_t* __restrict__ src_off,
                                  const int32_t* __restrict__ dst_off, int32_t* __restrict__ src_of_dst) {
+  DMOE_PDL_ENTRY();
   const int32_t R = offsets[El];
   for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
     int lo = 0, hi = El;
@@ -93,6 +95,7 @@ template <typename T>
 __global__ void k_permute_rows(const T* __restrict__ src, const int32_t* __restrict__ idx,
                                const int32_t* __restrict__ n_rows, int32_t D, int inverse,
                                T* __restrict__ dst) {
+  DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
   const int64_t R = *n_rows;
   const int vecs = D / V;
@@ -111,12 +114,12 @@ dmoe_status exchange_layout(const int32_t* counts, int G, int El, int32_t* offse
   int32_t* src_off = cv.take<int32_t>((size_t)G * El);
   int32_t* dst_off = cv.take<int32_t>((size_t)G * El);
   DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "exchange_layout: workspace too small");
-  k_exchange_tables<<<1, 1024, 0, s>>>(counts, G, El, offsets, src_off, dst_off);
+  launch_pdl(k_exchange_tables, 1, 1024, 0, s, counts, G, El, offsets, src_off, dst_off);
   DMOE_TRY(check_launch("exchange_tables"));
   int64_t blocks = ceil_div(R_cap > 0 ? R_cap : 1, 256);
   const int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  k_exchange_index<<<(unsigned)blocks, 256, 0, s>>>(counts, G, El, offsets, src_off, dst_off, src_of_dst);
+  launch_pdl(k_exchange_index, (unsigned)blocks, 256, 0, s, counts, G, El, offsets, src_off, dst_off, src_of_dst);
   return check_launch("exchange_index");
 }
 
@@ -124,10 +127,10 @@ dmoe_status permute_rows(const void* src, const int32_t* idx, const int32_t* n_r
                          dmoe_dtype dt, int inverse, void* dst, cudaStream_t s) {
   const int grid = num_sms() * 8;
   if (dt == DMOE_BF16)
-    k_permute_rows<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)src, idx, n_rows, D, inverse,
+    launch_pdl(k_permute_rows<__nv_bfloat16>, grid, 256, 0, s, (const __nv_bfloat16*)src, idx, n_rows, D, inverse,
                                                       (__nv_bfloat16*)dst);
   else
-    k_permute_rows<float><<<grid, 256, 0, s>>>((const float*)src, idx, n_rows, D, inverse, (float*)dst);
+    launch_pdl(k_permute_rows<float>, grid, 256, 0, s, (const float*)src, idx, n_rows, D, inverse, (float*)dst);
   return check_launch("permute_rows");
 }
 

@@ -15,6 +15,7 @@ namespace dmoe {
 template <typename T>
 __global__ void k_transpose(const T* __restrict__ src, int64_t rows, int64_t cols,
                             T* __restrict__ dst) {
+  DMOE_PDL_ENTRY();
   __shared__ float tile[32][33];
   const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -32,9 +33,9 @@ dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt
                       cudaStream_t s) {
   dim3 tb(32, 8), tg((unsigned)ceil_div(cols, 32), (unsigned)ceil_div(rows, 32));
   if (dt == DMOE_BF16)
-    k_transpose<__nv_bfloat16><<<tg, tb, 0, s>>>((const __nv_bfloat16*)src, rows, cols, (__nv_bfloat16*)dst);
+    launch_pdl(k_transpose<__nv_bfloat16>, tg, tb, 0, s, (const __nv_bfloat16*)src, rows, cols, (__nv_bfloat16*)dst);
   else
-    k_transpose<float><<<tg, tb, 0, s>>>((const float*)src, rows, cols, (float*)dst);
+    launch_pdl(k_transpose<float>, tg, tb, 0, s, (const float*)src, rows, cols, (float*)dst);
   return check_launch("transpose");
 }
 
@@ -46,6 +47,7 @@ k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
               const float* __restrict__ dscore, const T* __restrict__ dxd,
               const int32_t* __restrict__ row_of_slot, int64_t Tn, int32_t D, int d, int M, int k,
               T* __restrict__ dx, float* __restrict__ dG) {
+  DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
   const int lane = threadIdx.x & 31;
   const int dM = d * M;
@@ -113,6 +115,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn, int32_t D, int dM,
               int64_t tok_per_split, float* __restrict__ partial, float* __restrict__ pb) {
+  DMOE_PDL_ENTRY();
   __shared__ float xs[32][65];
   __shared__ float gs[32][33];
   constexpr int V = Vec16<T>::N;
@@ -184,6 +187,7 @@ k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn,
 __global__ void __launch_bounds__(256)
 k_dwg_reduce(const float* __restrict__ partial, const float* __restrict__ pb, int64_t nsplit, int32_t D, int dM,
              float* __restrict__ dWg, float* __restrict__ dbg) {
+  DMOE_PDL_ENTRY();
   __shared__ float red[8][33];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t n = (int64_t)D * dM;
@@ -245,20 +249,20 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
   DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "gate_bwd: workspace too small (%zu < %zu)", ws_bytes, cv.used);
   dim3 tb(32, 8), tg((unsigned)ceil_div(dM, 32), (unsigned)ceil_div(D, 32));
   if (dt == DMOE_BF16)
-    k_transpose<__nv_bfloat16><<<tg, tb, 0, s>>>((const __nv_bfloat16*)Wg, D, dM, (__nv_bfloat16*)WgT);
+    launch_pdl(k_transpose<__nv_bfloat16>, tg, tb, 0, s, (const __nv_bfloat16*)Wg, D, dM, (__nv_bfloat16*)WgT);
   else
-    k_transpose<float><<<tg, tb, 0, s>>>((const float*)Wg, D, dM, (float*)WgT);
+    launch_pdl(k_transpose<float>, tg, tb, 0, s, (const float*)Wg, D, dM, (float*)WgT);
   DMOE_TRY(check_launch("gate_bwd.transpose"));
   if (T > 0) {
     int64_t b = ceil_div(T, kGbWarps), cap = (int64_t)num_sms() * 16;
     unsigned grid = (unsigned)(b < cap ? b : cap);
 #define DMOE_GBDX(KM)                                                                                   \
     if (dt == DMOE_BF16)                                                                                \
-      k_gate_bwd_dx<__nv_bfloat16, KM><<<grid, kGbWarps * 32, 0, s>>>(                                 \
+      launch_pdl(k_gate_bwd_dx<__nv_bfloat16, KM>, grid, kGbWarps * 32, 0, s, \
           (const __nv_bfloat16*)WgT, sel, dscore, (const __nv_bfloat16*)dxd, row_of_slot, T, D, d, M,   \
           k, (__nv_bfloat16*)dx, dG);                                                                   \
     else                                                                                                \
-      k_gate_bwd_dx<float, KM><<<grid, kGbWarps * 32, 0, s>>>((const float*)WgT, sel, dscore,          \
+      launch_pdl(k_gate_bwd_dx<float, KM>, grid, kGbWarps * 32, 0, s, (const float*)WgT, sel, dscore,          \
                                                               (const float*)dxd, row_of_slot, T, D, d, \
                                                               M, k, (float*)dx, dG);
     if (k <= 4) { DMOE_GBDX(4) } else if (k <= 8) { DMOE_GBDX(8) } else { DMOE_GBDX(16) }
@@ -268,11 +272,11 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
   const int64_t tps = T > 0 ? ceil_div(T, S) : 1;
   dim3 pg((unsigned)ceil_div(D, 64), (unsigned)ceil_div(dM, 32), (unsigned)S);
   if (dt == DMOE_BF16)
-    k_dwg_partial<__nv_bfloat16><<<pg, 256, 0, s>>>((const __nv_bfloat16*)x, dG, T, D, dM, tps, part, pb);
+    launch_pdl(k_dwg_partial<__nv_bfloat16>, pg, 256, 0, s, (const __nv_bfloat16*)x, dG, T, D, dM, tps, part, pb);
   else
-    k_dwg_partial<float><<<pg, 256, 0, s>>>((const float*)x, dG, T, D, dM, tps, part, pb);
+    launch_pdl(k_dwg_partial<float>, pg, 256, 0, s, (const float*)x, dG, T, D, dM, tps, part, pb);
   DMOE_TRY(check_launch("gate_bwd.dwg_partial"));
-  k_dwg_reduce<<<(unsigned)ceil_div((int64_t)D * dM + dM, 32), 256, 0, s>>>(part, pb, S, D, dM, dWg, dbg);
+  launch_pdl(k_dwg_reduce, (unsigned)ceil_div((int64_t)D * dM + dM, 32), 256, 0, s, part, pb, S, D, dM, dWg, dbg);
   return check_launch("gate_bwd.dwg_reduce");
 }
 

@@ -31,6 +31,7 @@ k_simt_rows(const T* __restrict__ A, const T* __restrict__ B, TC* __restrict__ C
             const float* __restrict__ bias, const T* __restrict__ aux,
             const int32_t* __restrict__ offsets, const int32_t* __restrict__ plan, int E, int N,
             int K, int64_t rows_single) {
+  DMOE_PDL_ENTRY();
   __shared__ float As[SK][SB + 1];
   __shared__ float Bs[SK][SB + 1];
   const int tile = blockIdx.x;
@@ -96,6 +97,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_simt_segk(const T* __restrict__ A, const T* __restrict__ B, T* __restrict__ C,
             const int32_t* __restrict__ offsets, int Mdim, int N) {
+  DMOE_PDL_ENTRY();
   __shared__ float As[SK][SB + 1];
   __shared__ float Bs[SK][SB + 1];
   const int e = blockIdx.z;
@@ -146,6 +148,7 @@ template <typename T>
 __global__ void __launch_bounds__(kCsWarps * 32)
 k_seg_colsum(const T* __restrict__ X, const int32_t* __restrict__ offsets, int N,
              float* __restrict__ out) {
+  DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
   __shared__ float part[kCsWarps][32 * V + 1];
   const int e = blockIdx.y;
@@ -190,7 +193,7 @@ template <typename T, typename TC>
 static void launch_rows(const GemmRows& g, cudaStream_t s) {
   dim3 grid((unsigned)g.max_tiles, (unsigned)ceil_div(g.N, SB));
 #define DMOE_ROWS(BMN, EPI_)                                                                   \
-  k_simt_rows<T, TC, BMN, EPI_><<<grid, 256, 0, s>>>((const T*)g.A, (const T*)g.B, (TC*)g.C,     \
+  launch_pdl(k_simt_rows<T, TC, BMN, EPI_>, grid, 256, 0, s, (const T*)g.A, (const T*)g.B, (TC*)g.C,     \
                                                       g.bias, (const T*)g.aux, g.offsets, g.plan, \
                                                       g.E, g.N, g.K, g.rows_single)
 #define DMOE_ROWS_EPI(BMN)                                      \
@@ -221,10 +224,10 @@ dmoe_status simt_gemm_rows(const GemmRows& g, dmoe_dtype dt, cudaStream_t s) {
 dmoe_status simt_gemm_segk(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
   dim3 grid((unsigned)ceil_div(g.N, SB), (unsigned)ceil_div(g.Mdim, SB), (unsigned)g.E);
   if (dt == DMOE_BF16)
-    k_simt_segk<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)g.A, (const __nv_bfloat16*)g.B,
+    launch_pdl(k_simt_segk<__nv_bfloat16>, grid, 256, 0, s, (const __nv_bfloat16*)g.A, (const __nv_bfloat16*)g.B,
                                                     (__nv_bfloat16*)g.C, g.offsets, g.Mdim, g.N);
   else
-    k_simt_segk<float><<<grid, 256, 0, s>>>((const float*)g.A, (const float*)g.B, (float*)g.C,
+    launch_pdl(k_simt_segk<float>, grid, 256, 0, s, (const float*)g.A, (const float*)g.B, (float*)g.C,
                                             g.offsets, g.Mdim, g.N);
   __atomic_fetch_add(&g_counters[2], 1, __ATOMIC_RELAXED);
   return check_launch("simt_gemm_segk");
@@ -235,9 +238,9 @@ dmoe_status seg_colsum(const void* X, dmoe_dtype dt, const int32_t* offsets, int
   const int V = dt == DMOE_BF16 ? 8 : 4;  // N % V == 0 is validated by the caller
   dim3 grid((unsigned)ceil_div(N, 32 * V), (unsigned)E);
   if (dt == DMOE_BF16)
-    k_seg_colsum<__nv_bfloat16><<<grid, kCsWarps * 32, 0, s>>>((const __nv_bfloat16*)X, offsets, N, out);
+    launch_pdl(k_seg_colsum<__nv_bfloat16>, grid, kCsWarps * 32, 0, s, (const __nv_bfloat16*)X, offsets, N, out);
   else
-    k_seg_colsum<float><<<grid, kCsWarps * 32, 0, s>>>((const float*)X, offsets, N, out);
+    launch_pdl(k_seg_colsum<float>, grid, kCsWarps * 32, 0, s, (const float*)X, offsets, N, out);
   return check_launch("seg_colsum");
 }
 

@@ -232,6 +232,7 @@ template <int BN, bool SEGK, bool B_MN, int EPI>
 __global__ void __launch_bounds__(TcCfg<BN>::THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const TcParams p) {
+  DMOE_PDL_ENTRY();
   using Cfg = TcCfg<BN>;
   constexpr int S = Cfg::STAGES;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
@@ -734,6 +735,7 @@ template <int NT, bool W_MN, int EPI>
 __global__ void __launch_bounds__(SwCfg<NT>::THREADS, 1)
 k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
           const TcParams p) {
+  DMOE_PDL_ENTRY();
   constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
   using Cfg = SwCfg<NT, OUT_F32>;
   constexpr int S = Cfg::STAGES;
@@ -1100,7 +1102,7 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUte
   TcParams pp = p;
   pp.dbg = debug_flags();
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  kern<<<(unsigned)grid, TcCfg<BN>::THREADS, smem, s>>>(a, b, c, pp);
+  launch_pdl(kern, (unsigned)grid, TcCfg<BN>::THREADS, smem, s, a, b, c, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
 }
@@ -1175,7 +1177,7 @@ static dmoe_status launch_rows(const CUtensorMap& w, const CUtensorMap& x, const
   TcParams pp = p;
   pp.dbg = debug_flags();
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  kern<<<(unsigned)grid, SwCfg<NT>::THREADS, smem, s>>>(w, x, pp);
+  launch_pdl(kern, (unsigned)grid, SwCfg<NT>::THREADS, smem, s, w, x, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm_rows");
 }

@@ -36,11 +36,13 @@ __device__ __forceinline__ uint64_t now_ns() {
 }
 
 // epoch[0] += 1 (start of a step)
-__global__ void k_ep_begin(uint64_t* epoch) { epoch[0] += 1; }
+__global__ void k_ep_begin(uint64_t* epoch) {
+  DMOE_PDL_ENTRY(); epoch[0] += 1; }
 
 // signal phase p to every peer: flags_j[rank] = 8*epoch + p (after all prior writes of this
 // stream are complete: separate launch, then a system fence)
 __global__ void k_ep_signal(uint64_t* const* peer_flags, int G, int rank, const uint64_t* epoch, int phase) {
+  DMOE_PDL_ENTRY();
   __threadfence_system();
   const uint64_t v = epoch[0] * 8 + (uint64_t)phase;
   for (int j = threadIdx.x; j < G; j += blockDim.x) st_release_sys(peer_flags[j] + rank, v);
@@ -49,6 +51,7 @@ __global__ void k_ep_signal(uint64_t* const* peer_flags, int G, int rank, const 
 // wait until every source signalled phase p of this epoch; on timeout set err[0] |= 1 and go on
 __global__ void k_ep_wait(const uint64_t* flags, int G, const uint64_t* epoch, int phase, uint64_t timeout_ns,
                           int32_t* err) {
+  DMOE_PDL_ENTRY();
   const uint64_t want = epoch[0] * 8 + (uint64_t)phase;
   for (int s = threadIdx.x; s < G; s += blockDim.x) {
     const uint64_t t0 = now_ns();
@@ -65,6 +68,7 @@ __global__ void k_ep_wait(const uint64_t* flags, int G, const uint64_t* epoch, i
 // phase 0: broadcast this rank's per-expert counts into every peer's count matrix row `rank`
 __global__ void k_ep_counts_push(const int32_t* __restrict__ counts, int E, int G, int rank,
                                  int32_t* const* peer_cnt) {
+  DMOE_PDL_ENTRY();
   for (int j = 0; j < G; ++j) {
     int32_t* dst = peer_cnt[j] + (int64_t)rank * E;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < E; e += gridDim.x * blockDim.x) dst[e] = counts[e];
@@ -82,6 +86,7 @@ __global__ void __launch_bounds__(1024)
 k_ep_plan(const int32_t* __restrict__ cnt, int G, int rank, int E, int El, int64_t rin_cap,
           int32_t* __restrict__ base, int32_t* __restrict__ off_loc, int32_t* __restrict__ src_off,
           int32_t* __restrict__ dst_off, int32_t* __restrict__ err) {
+  DMOE_PDL_ENTRY();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // per-expert totals and the exclusive scan within each owner's slice (one warp per owner)
   for (int j = warp; j < G; j += nw) {
@@ -146,6 +151,7 @@ template <typename T>
 __global__ void k_ep_push_rows(const T* __restrict__ src, const int32_t* __restrict__ gidx,
                                const int32_t* __restrict__ offsets, const int32_t* __restrict__ base, int E, int El,
                                int32_t D, T* const* peer_dst, const int32_t* __restrict__ err) {
+  DMOE_PDL_ENTRY();
   if (*err) return;
   constexpr int V = Vec16<T>::N;
   const int64_t R = offsets[E];
@@ -171,6 +177,7 @@ __global__ void k_ep_return_rows(const T* __restrict__ src, const int32_t* __res
                                  const int32_t* __restrict__ off_loc, const int32_t* __restrict__ src_off,
                                  const int32_t* __restrict__ dst_off, int G, int rank, int E, int El, int32_t D,
                                  T* const* peer_dst, const int32_t* __restrict__ err) {
+  DMOE_PDL_ENTRY();
   if (*err) return;
   constexpr int V = Vec16<T>::N;
   const int64_t R = off_loc[El];
@@ -194,37 +201,37 @@ __global__ void k_ep_return_rows(const T* __restrict__ src, const int32_t* __res
 static int rows_grid() { return num_sms() * 8; }
 
 dmoe_status ep_begin(uint64_t* epoch, cudaStream_t s) {
-  k_ep_begin<<<1, 1, 0, s>>>(epoch);
+  launch_pdl(k_ep_begin, 1, 1, 0, s, epoch);
   return check_launch("ep_begin");
 }
 dmoe_status ep_signal(uint64_t* const* peer_flags, int G, int rank, const uint64_t* epoch, int phase,
                       cudaStream_t s) {
-  k_ep_signal<<<1, 32, 0, s>>>(peer_flags, G, rank, epoch, phase);
+  launch_pdl(k_ep_signal, 1, 32, 0, s, peer_flags, G, rank, epoch, phase);
   return check_launch("ep_signal");
 }
 dmoe_status ep_wait(const uint64_t* flags, int G, const uint64_t* epoch, int phase, uint64_t timeout_ns,
                     int32_t* err, cudaStream_t s) {
-  k_ep_wait<<<1, 32, 0, s>>>(flags, G, epoch, phase, timeout_ns, err);
+  launch_pdl(k_ep_wait, 1, 32, 0, s, flags, G, epoch, phase, timeout_ns, err);
   return check_launch("ep_wait");
 }
 dmoe_status ep_counts_push(const int32_t* counts, int E, int G, int rank, int32_t* const* peer_cnt,
                            cudaStream_t s) {
-  k_ep_counts_push<<<(unsigned)ceil_div(E, 256), 256, 0, s>>>(counts, E, G, rank, peer_cnt);
+  launch_pdl(k_ep_counts_push, (unsigned)ceil_div(E, 256), 256, 0, s, counts, E, G, rank, peer_cnt);
   return check_launch("ep_counts_push");
 }
 dmoe_status ep_plan(const int32_t* cnt, int G, int rank, int E, int El, int64_t rin_cap, int32_t* base,
                     int32_t* off_loc, int32_t* src_off, int32_t* dst_off, int32_t* err, cudaStream_t s) {
-  k_ep_plan<<<1, 1024, 0, s>>>(cnt, G, rank, E, El, rin_cap, base, off_loc, src_off, dst_off, err);
+  launch_pdl(k_ep_plan, 1, 1024, 0, s, cnt, G, rank, E, El, rin_cap, base, off_loc, src_off, dst_off, err);
   return check_launch("ep_plan");
 }
 dmoe_status ep_push_rows(const void* src, const int32_t* gidx, const int32_t* offsets, const int32_t* base,
                          int E, int El, int32_t D, dmoe_dtype dt, void* const* peer_dst, const int32_t* err,
                          cudaStream_t s) {
   if (dt == DMOE_BF16)
-    k_ep_push_rows<__nv_bfloat16><<<rows_grid(), 256, 0, s>>>((const __nv_bfloat16*)src, gidx, offsets, base, E,
+    launch_pdl(k_ep_push_rows<__nv_bfloat16>, rows_grid(), 256, 0, s, (const __nv_bfloat16*)src, gidx, offsets, base, E,
                                                              El, D, (__nv_bfloat16* const*)peer_dst, err);
   else
-    k_ep_push_rows<float><<<rows_grid(), 256, 0, s>>>((const float*)src, gidx, offsets, base, E, El, D,
+    launch_pdl(k_ep_push_rows<float>, rows_grid(), 256, 0, s, (const float*)src, gidx, offsets, base, E, El, D,
                                                      (float* const*)peer_dst, err);
   return check_launch("ep_push_rows");
 }
@@ -232,11 +239,11 @@ dmoe_status ep_return_rows(const void* src, const int32_t* cnt, const int32_t* o
                            const int32_t* dst_off, int G, int rank, int E, int El, int32_t D, dmoe_dtype dt,
                            void* const* peer_dst, const int32_t* err, cudaStream_t s) {
   if (dt == DMOE_BF16)
-    k_ep_return_rows<__nv_bfloat16><<<rows_grid(), 256, 0, s>>>((const __nv_bfloat16*)src, cnt, off_loc,
+    launch_pdl(k_ep_return_rows<__nv_bfloat16>, rows_grid(), 256, 0, s, (const __nv_bfloat16*)src, cnt, off_loc,
                                                                src_off, dst_off, G, rank, E, El, D,
                                                                (__nv_bfloat16* const*)peer_dst, err);
   else
-    k_ep_return_rows<float><<<rows_grid(), 256, 0, s>>>((const float*)src, cnt, off_loc, src_off, dst_off, G,
+    launch_pdl(k_ep_return_rows<float>, rows_grid(), 256, 0, s, (const float*)src, cnt, off_loc, src_off, dst_off, G,
                                                        rank, E, El, D, (float* const*)peer_dst, err);
   return check_launch("ep_return_rows");
 }

@@ -17,6 +17,7 @@ namespace dmoe {
 // is the alive mask itself (copied).
 __global__ void k_prefix_alive(const uint32_t* __restrict__ alive, int d, int M, int64_t E,
                                uint32_t* __restrict__ PA) {
+  DMOE_PDL_ENTRY();
   int64_t wo = 0, n = M;
   for (int i = 0; i < d; ++i) {
     int64_t words = (n + 31) / 32;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(kBeamWarps * 32)
 k_beam_topk(const float* __restrict__ G, int64_t T, int d, int M, int k, int B,
             const uint32_t* __restrict__ PA_global, const uint32_t* __restrict__ alive,
             int pa_words, int32_t* __restrict__ sel, float* __restrict__ sel_score) {
+  DMOE_PDL_ENTRY();
   extern __shared__ float smem_f[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int dM = d * M;
@@ -213,7 +215,7 @@ static dmoe_status launch_beam(const float* G, int64_t T, dmoe_grid g, const uin
   int64_t blocks = ceil_div(T, kBeamWarps);
   int64_t cap = (int64_t)num_sms() * 8;
   if (blocks > cap) blocks = cap;
-  k_beam_topk<WMAX><<<(unsigned)blocks, kBeamWarps * 32, smem, s>>>(G, T, g.d, g.M, g.k, g.beam, PA_global,
+  launch_pdl(k_beam_topk<WMAX>, (unsigned)blocks, kBeamWarps * 32, smem, s, G, T, g.d, g.M, g.k, g.beam, PA_global,
                                                                      alive, pa_words, sel, sel_score);
   return check_launch("beam_topk");
 }
@@ -227,7 +229,7 @@ dmoe_status beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* al
   if (words > kSmemPAWords) {  // big grids: one pass into the workspace, read through L1/L2
     int blocks = (int)(((E + 31) / 32 + 255) / 256);
     if (blocks > 1024) blocks = 1024;
-    k_prefix_alive<<<blocks, 256, 0, s>>>(alive_bits, g.d, g.M, E, PA);
+    launch_pdl(k_prefix_alive, blocks, 256, 0, s, alive_bits, g.d, g.M, E, PA);
     DMOE_TRY(check_launch("prefix_alive"));
     PA_global = PA;
   }
