@@ -252,29 +252,25 @@ def bench_ep(args, cfg, rank, world, local_rank):
     t = torch.tensor([ms], device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
-    # e2e: pinned host x, dy in; y, dx out
+    # e2e: pinned host x, dy in; y, dx out (dy upload / y download overlapped with compute)
     hx = torch.empty(T, cfg.D, dtype=x.dtype, pin_memory=True)
     hdy = torch.empty_like(hx, pin_memory=True)
     hx.copy_(x)
     hdy.copy_(dy)
     hy, hdx = torch.empty_like(hx, pin_memory=True), torch.empty_like(hx, pin_memory=True)
-    xin, dyin = torch.empty_like(x), torch.empty_like(dy)
     e2e = []
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)
-        dist.barrier()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        xin.copy_(hx, non_blocking=True)
-        dyin.copy_(hdy, non_blocking=True)
-        lay.forward(xin, alive, resp)
-        gx = lay.backward(dyin)
-        hy.copy_(lay.y[:T], non_blocking=True)
-        hdx.copy_(gx, non_blocking=True)
-        b.record()
-        b.synchronize()
-        e2e.append(a.elapsed_time(b))
+    with torch.cuda.stream(stream):
+        lay.step_host(hx, hdy, hy, hdx, alive, resp)
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            stream.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            lay.step_host(hx, hdy, hy, hdx, alive, resp)
+            b.record(stream)
+            b.synchronize()
+            e2e.append(a.elapsed_time(b))
     if peer:
         lay.check()
     t = torch.tensor([sum(e2e) / len(e2e)], device=device)
@@ -352,31 +348,27 @@ def bench_ours(args, cfg, rank, world, local_rank):
                 per_call[c].append(a.elapsed_time(b))
     per_call_ms = {c: sum(v) / len(v) for c, v in per_call.items()}
 
-    # ---- e2e through the public API with pinned host buffers
+    # ---- e2e through the public API with pinned host buffers (DMoELayer.step_host: x in,
+    # y and dX out; dy upload / y download overlapped with compute)
     hx = torch.empty(T, cfg.D, dtype=x.dtype, pin_memory=True)
     hdy = torch.empty_like(hx, pin_memory=True)
     hx.copy_(x)
     hdy.copy_(dy)
     hy = torch.empty_like(hx, pin_memory=True)
     hdx = torch.empty_like(hx, pin_memory=True)
-    dx_in = torch.empty_like(x)
-    dy_in = torch.empty_like(dy)
     e2e_ms = []
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        dx_in.copy_(hx, non_blocking=True)
-        dy_in.copy_(hdy, non_blocking=True)
-        lay.forward(dx_in, alive, resp)
-        gx = lay.backward(dy_in)
-        hy.copy_(lay.y[:T], non_blocking=True)
-        hdx.copy_(gx, non_blocking=True)
-        b.record()
-        b.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
+    with torch.cuda.stream(stream):
+        lay.step_host(hx, hdy, hy, hdx, alive, resp)
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            stream.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            lay.step_host(hx, hdy, hy, hdx, alive, resp)
+            b.record(stream)
+            b.synchronize()
+            e2e_ms.append(a.elapsed_time(b))
     e2e = sum(e2e_ms) / len(e2e_ms)
     if world > 1:
         t = torch.tensor([e2e], device=device)

@@ -141,3 +141,8 @@ class EPDMoELayer:
     def step(self, x, dy, alive_bits, responded_bits):
         self.forward(x, alive_bits, responded_bits)
         return self.backward(dy)
+
+    def step_host(self, hx, hdy, hy, hdx, alive_bits, responded_bits):
+        """Pinned-host step with the dy upload / y download overlapped (see layer.host_step)."""
+        from .layer import host_step
+        return host_step(self, hx, hdy, hy, hdx, alive_bits, responded_bits)

@@ -90,3 +90,38 @@ class DMoELayer:
         """One layer step: forward + backward (the unit bench.py times)."""
         self.forward(x, alive_bits, responded_bits)
         return self.backward(dy)
+
+    def step_host(self, hx, hdy, hy, hdx, alive_bits, responded_bits):
+        """One step from pinned host buffers: x in, y and dX out.  The dy upload overlaps the
+        forward pass and the y download overlaps the backward pass (copy stream + events);
+        only x-in and dX-out are on the critical path."""
+        return host_step(self, hx, hdy, hy, hdx, alive_bits, responded_bits)
+
+
+def host_step(lay, hx, hdy, hy, hdx, alive_bits, responded_bits):
+    """Host-buffer step for any layer with forward/backward/y (DMoELayer, PeerEPDMoELayer, ...)."""
+    T = hx.shape[0]
+    cur = torch.cuda.current_stream()
+    if not hasattr(lay, "_copy_stream"):
+        lay._copy_stream = torch.cuda.Stream(device=lay.y.device)
+        lay._xin = torch.empty(lay.T_max, lay.D, dtype=lay.dtype, device=lay.y.device)
+        lay._dyin = torch.empty(lay.T_max, lay.D, dtype=lay.dtype, device=lay.y.device)
+        lay._ev = [torch.cuda.Event() for _ in range(3)]
+    side = lay._copy_stream
+    x, dy = lay._xin[:T], lay._dyin[:T]
+    side.wait_stream(cur)                       # buffers free (previous step done with them)
+    x.copy_(hx, non_blocking=True)
+    with torch.cuda.stream(side):
+        dy.copy_(hdy, non_blocking=True)
+        lay._ev[0].record(side)
+    lay.forward(x, alive_bits, responded_bits)
+    lay._ev[1].record(cur)
+    with torch.cuda.stream(side):
+        side.wait_event(lay._ev[1])
+        hy.copy_(lay.y[:T], non_blocking=True)
+        lay._ev[2].record(side)
+    cur.wait_event(lay._ev[0])
+    dx = lay.backward(dy)
+    hdx.copy_(dx, non_blocking=True)
+    cur.wait_event(lay._ev[2])
+    return dx

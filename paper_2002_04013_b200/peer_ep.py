@@ -162,6 +162,11 @@ class PeerEPDMoELayer:
         self.forward(x, alive_bits, responded_bits)
         return self.backward(dy)
 
+    def step_host(self, hx, hdy, hy, hdx, alive_bits, responded_bits):
+        """Pinned-host step with the dy upload / y download overlapped (see layer.host_step)."""
+        from .layer import host_step
+        return host_step(self, hx, hdy, hy, hdx, alive_bits, responded_bits)
+
     def check(self):
         """Raise if a wait timed out (err & 1) or a receive buffer would have overflowed (err & 2)."""
         v = int(self.err.item())

@@ -107,3 +107,19 @@ def test_deterministic_rerun():
     a, b = gpu_layer(cfg, inp), gpu_layer(cfg, inp)
     for n in ("y", "dx", "dW1", "dW2", "db1", "db2", "dWg", "dbg", "row_of_slot"):
         assert np.array_equal(np64(getattr(a, n)), np64(getattr(b, n))), n
+
+
+def test_step_host_matches_device_step():
+    """The public host-buffer step (overlapped copies) gives the device step's y and dX."""
+    import torch
+    cfg = CONFIGS["mnist"]
+    inp = make_inputs(cfg, seed=9, T=777)
+    lay = gpu_layer(cfg, inp)
+    y_ref, dx_ref = np64(lay.y[:777]).copy(), np64(lay.dx[:777]).copy()
+    x, dy, alive, resp = lay._inputs
+    hx, hdy = x.cpu().pin_memory(), dy.cpu().pin_memory()
+    hy, hdx = torch.empty_like(hx).pin_memory(), torch.empty_like(hx).pin_memory()
+    lay.y.zero_()
+    lay.step_host(hx, hdy, hy, hdx, alive, resp)
+    torch.cuda.synchronize()
+    assert np.array_equal(np64(hy), y_ref) and np.array_equal(np64(hdx), dx_ref)
