@@ -120,6 +120,48 @@ static dmoe_status segk_gemm(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
 }
 constexpr int kPlanBM_SIMT = 64;
 
+// ------------------------------------------------------- library side stream (fork / join)
+// One non-blocking stream + event pool per device, created on first use (setup, not hot path).
+// fork_stream(s): the side stream waits for everything enqueued on s so far; join_stream: s
+// waits for the side stream.  Event record / wait are captured into CUDA graphs as edges.
+// DMOE_SERIAL=1 disables the fork (everything on the caller's stream).
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+};
+static SideStream g_side[64];
+
+static cudaStream_t fork_stream(cudaStream_t s) {
+  static const bool serial = getenv("DMOE_SERIAL") != nullptr;
+  if (serial) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  SideStream& ss = g_side[dev];
+  if (!ss.st) {
+    if (cudaStreamCreateWithFlags(&ss.st, cudaStreamNonBlocking) != cudaSuccess) { ss.st = nullptr; return nullptr; }
+    for (auto& e : ss.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  if (cudaEventRecord(ss.ev[0], s) != cudaSuccess || cudaStreamWaitEvent(ss.st, ss.ev[0], 0) != cudaSuccess)
+    return nullptr;
+  return ss.st;
+}
+static dmoe_status fork_point(cudaStream_t s, cudaStream_t side) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaEvent_t e = g_side[dev].ev[1];
+  if (cudaEventRecord(e, s) != cudaSuccess || cudaStreamWaitEvent(side, e, 0) != cudaSuccess)
+    return set_error(DMOE_ERR_CUDA, "fork_point: %s", cudaGetErrorString(cudaGetLastError()));
+  return DMOE_OK;
+}
+static dmoe_status join_stream(cudaStream_t s, cudaStream_t side) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaEvent_t e = g_side[dev].ev[2];
+  if (cudaEventRecord(e, side) != cudaSuccess || cudaStreamWaitEvent(s, e, 0) != cudaSuccess)
+    return set_error(DMOE_ERR_CUDA, "join_stream: %s", cudaGetErrorString(cudaGetLastError()));
+  return DMOE_OK;
+}
+
 // row-tile plans only for the engines the two GEMMs of a call will use
 static dmoe_status plans_for(GemmRows& a, GemmRows& b, const int32_t* offsets, int E,
                              int32_t* plan_tc, int32_t* plan_simt, cudaStream_t s) {
@@ -303,8 +345,6 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
     g->max_tiles = ceil_div(R_cap, bm) + E_local;
   }
   DMOE_TRY(plans_for(g3, g4, offsets, E_local, plan_tc, plan_simt, s));
-  DMOE_TRY(rows_gemm(g3, dt, s));
-  DMOE_TRY(rows_gemm(g4, dt, s));
   // dW2_e = dout^T h;  dW1_e = dh^T xd;  db2 / db1 = segment column sums of dout / dh (on the
   // tensor-core path: an extra ones-MMA inside the same GEMMs)
   GemmSegK g5{dout, h, dW2, offsets, E_local, D, H, R_cap, db2};
@@ -312,8 +352,23 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
   static const bool no_fuse = getenv("DMOE_NO_COLSUM_FUSE") != nullptr;  // A/B experiments
   const bool fused = !no_fuse && dt == DMOE_BF16 && tc_segk_colsum_supported(g5) && tc_segk_colsum_supported(g6);
   if (!fused) g5.colsum = g6.colsum = nullptr;
-  DMOE_TRY(segk_gemm(g5, dt, s));
-  DMOE_TRY(segk_gemm(g6, dt, s));
+  // Dependency graph: dh (g3) -> dxd (g4); dh -> dW1 (g6); dW2 (g5) independent.  g5 and g6 run
+  // on a library stream forked/joined with events (graph-capturable), so each persistent GEMM's
+  // tail is filled by the other chain's tiles instead of idling SMs.
+  cudaStream_t side = fork_stream(s);
+  if (side) DMOE_TRY(segk_gemm(g5, dt, side));
+  DMOE_TRY(rows_gemm(g3, dt, s));
+  if (side) {
+    DMOE_TRY(fork_point(s, side));  // side waits for dh
+    DMOE_TRY(segk_gemm(g6, dt, side));
+  }
+  DMOE_TRY(rows_gemm(g4, dt, s));
+  if (side) {
+    DMOE_TRY(join_stream(s, side));
+  } else {
+    DMOE_TRY(segk_gemm(g5, dt, s));
+    DMOE_TRY(segk_gemm(g6, dt, s));
+  }
   if (fused) return DMOE_OK;
   DMOE_TRY(seg_colsum(dout, dt, offsets, E_local, D, db2, s));
   return seg_colsum(dh, dt, offsets, E_local, H, db1, s);
