@@ -196,33 +196,41 @@ struct TcParams {
   void* C;
   int E, N, K, Mdim;
   int64_t rows_single;
+  int stages;     // M-major engine: smem ring depth (runtime, <= TC_MAX_STAGES)
+  int table_len;  // M-major engine: per-expert smem table entries (0: tables stay in global)
   int slot;  // probe slot (launch ordinal % 8)
   int dbg;  // experiment switches (env DMOE_TC_DEBUG): 1 skip stores, 2 skip TMEM loads, 4 skip MMAs
 };
 
-constexpr int TC_SMEM_MAX = 227 * 1024;
+constexpr int TC_SMEM_MAX = 227 * 1024 - 2048;   // opt-in maximum less the kernels' static smem (<= 2 KB)
 constexpr int TC_STAGE_ROW = 144;              // staging row pitch: 128 B of data + 16 B pad
 constexpr int TC_STAGE_WARP = 5 * 1024;           // one warp's 32-row staging tile (1 KB aligned)
 constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan live in smem
 constexpr int TC_TABLE_LEN = TC_TABLE_E + 4;      // entries per table (16-byte multiple)
 
+constexpr int TC_MAX_STAGES = 8;
+
 template <int BN> struct TcCfg {
   static constexpr int ONES_BYTES = 16 * 128;    // [16 N][64 K] bf16 ones (K-major B operand)
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
-  static constexpr int EPI_WARPS = (BN >= 128) ? 8 : 4;   // 2 column halves when wide
+  // epilogue warps: 8 (two column halves) for tiles >= 128 wide.  4 warps on 256-wide tiles buy
+  // a 4th ring stage but the epilogue then trails the mainloop (measured: mnist FFN fwd 78 -> 92 us)
+  static constexpr int EPI_WARPS = (BN >= 128) ? 8 : 4;
   static constexpr int EPI_COLS = BN / (EPI_WARPS / 4);   // columns per epilogue warp
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;       // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
-  static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + ONES_BYTES + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2 +
-                               2 * TC_TABLE_LEN * 4 /*offsets + plan tables*/;
-  static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
-  static constexpr int STAGES = ST > 8 ? 8 : ST;
+  // fixed smem without the per-expert tables (those are sized at launch: 2 x table_len ints)
+  static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + ONES_BYTES + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2;
+  static int stages_for(int table_len) {
+    const int st = (TC_SMEM_MAX - FIXED - 2 * table_len * 4) / STAGE_BYTES;
+    return st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
+  }
+  static int smem_for(int table_len) { return stages_for(table_len) * STAGE_BYTES + FIXED + 2 * table_len * 4; }
   static constexpr int pow2cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
   static constexpr int TMEM_COLS = pow2cols(2 * BN);            // 2 accumulators
   static constexpr int TMEM_COLS_CS = pow2cols(2 * BN + 32);    // + 2 x 16 columns (SEGK column sums)
-  static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
 };
 
 // bf16 h > 0  <=>  sign bit clear and not +0
@@ -234,7 +242,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   DMOE_PDL_ENTRY();
   using Cfg = TcCfg<BN>;
-  constexpr int S = Cfg::STAGES;
+  const int S = p.stages;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
   constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
   constexpr int OUT_ES = OUT_F32 ? 4 : 2;
@@ -242,15 +250,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + S * Cfg::STAGE_BYTES);
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
+  uint64_t* empty = full + TC_MAX_STAGES;
+  uint64_t* tfull = empty + TC_MAX_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
   uint8_t* ones_s = smem + S * Cfg::STAGE_BYTES + 1024;       // 1 KB aligned constant tile
   uint8_t* stage_base = ones_s + Cfg::ONES_BYTES;             // 1 KB aligned (128B-swizzled TMA stores)
   float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * TC_STAGE_WARP);  // [2][BN]
-  int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [E+1]
-  int32_t* plan_s = off_s + TC_TABLE_LEN;                               // [E+1]
+  int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [table_len]
+  int32_t* plan_s = off_s + p.table_len;                                    // [table_len]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -260,7 +268,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const int32_t* offs = p.offsets;
   const int32_t* plan = p.plan;
   __shared__ int32_t scan_sh[33];
-  if (p.offsets && p.E <= TC_TABLE_E) {
+  if (p.offsets && p.table_len > 0) {
     for (int i = threadIdx.x; i <= p.E; i += blockDim.x) {
       off_s[i] = p.offsets[i];
       if (!SEGK && p.plan) plan_s[i] = p.plan[i];
@@ -1091,17 +1099,20 @@ template <int BN, bool SEGK, bool B_MN, int EPI>
 static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcParams& p,
                           int64_t max_tiles, cudaStream_t s) {
   auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
-  const int smem = TcCfg<BN>::SMEM;
-  static bool attr = false;
-  if (!attr) {
+  const int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
+  const int smem = TcCfg<BN>::smem_for(table_len);
+  static int attr = 0;
+  if (smem > attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+    attr = smem;
   }
   int64_t grid = max_tiles < num_sms() ? max_tiles : num_sms();
   if (grid < 1) grid = 1;
   TcParams pp = p;
   pp.dbg = debug_flags();
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
+  pp.stages = TcCfg<BN>::stages_for(table_len);
+  pp.table_len = table_len;
   launch_pdl(kern, (unsigned)grid, TcCfg<BN>::THREADS, smem, s, a, b, c, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
