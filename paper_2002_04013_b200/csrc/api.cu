@@ -120,6 +120,27 @@ static dmoe_status segk_gemm(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
 }
 constexpr int kPlanBM_SIMT = 64;
 
+static int num_sms_api() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+// CTAs of the weight-gradient chain in the expert backward (0: no split, every GEMM takes all
+// SMs and the chains only fill each other's tails).  DMOE_BWD_SEGK_CTAS overrides.
+static int bwd_segk_ctas() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DMOE_BWD_SEGK_CTAS");
+    v = e ? atoi(e) : 0;
+    if (v >= num_sms_api()) v = 0;
+  }
+  return v;
+}
+
 // ------------------------------------------------------- library side stream (fork / join)
 // One non-blocking stream + event pool per device, created on first use (setup, not hot path).
 // fork_stream(s): the side stream waits for everything enqueued on s so far; join_stream: s
@@ -355,8 +376,26 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
   // Dependency graph: dh (g3) -> dxd (g4); dh -> dW1 (g6); dW2 (g5) independent.  g5 and g6 run
   // on a library stream forked/joined with events (graph-capturable), so each persistent GEMM's
   // tail is filled by the other chain's tiles instead of idling SMs.
+  // DMOE_BWD_ONLY=<mask> (timing experiments only; results are then incomplete): run only the
+  // GEMMs whose bit is set: 1 dh, 2 dxd, 4 dW2, 8 dW1
+  static const int only = getenv("DMOE_BWD_ONLY") ? atoi(getenv("DMOE_BWD_ONLY")) : 15;
+  if (only != 15) {
+    if (only & 1) DMOE_TRY(rows_gemm(g3, dt, s));
+    if (only & 2) DMOE_TRY(rows_gemm(g4, dt, s));
+    if (only & 4) DMOE_TRY(segk_gemm(g5, dt, s));
+    if (only & 8) DMOE_TRY(segk_gemm(g6, dt, s));
+    return DMOE_OK;
+  }
   cudaStream_t side = fork_stream(s);
-  if (side) DMOE_TRY(segk_gemm(g5, dt, side));
+  if (side) {
+    // SM split between the chains: the weight-gradient GEMMs are bound by HBM writes (dW), the
+    // row GEMMs by HBM reads (W); run side by side on disjoint SMs the two mix into copy-like
+    // traffic instead of alternating write-only and read-only phases.
+    const int seg_ctas = bwd_segk_ctas();
+    g5.max_ctas = g6.max_ctas = seg_ctas;
+    g3.max_ctas = g4.max_ctas = seg_ctas > 0 ? num_sms_api() - seg_ctas : 0;
+    DMOE_TRY(segk_gemm(g5, dt, side));
+  }
   DMOE_TRY(rows_gemm(g3, dt, s));
   if (side) {
     DMOE_TRY(fork_point(s, side));  // side waits for dh

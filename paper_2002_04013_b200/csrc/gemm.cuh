@@ -27,6 +27,7 @@ struct GemmRows {
   int64_t max_tiles;       // host upper bound on plan[E] (grid size)
   bool b_mn;
   int epi;
+  int max_ctas = 0;        // persistent grid cap (0: one CTA per SM); leaves SMs to a concurrent GEMM
 };
 
 // SEGK family: C_e[m, n] = sum_{r in seg e} A[r, m] B[r, n]  (K = segment rows)
@@ -38,6 +39,7 @@ struct GemmSegK {
   int E, Mdim, N;
   int64_t R_cap;    // allocated rows of A and B
   float* colsum;    // optional [E][Mdim] fp32: sum over the segment's rows of A (bias gradient)
+  int max_ctas = 0;  // persistent grid cap (0: one CTA per SM)
 };
 
 dmoe_status simt_gemm_rows(const GemmRows& g, dmoe_dtype dt, cudaStream_t s);

@@ -177,7 +177,18 @@ __host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn) 
 // first 32 tiles: [role][tile] with role 0 = producer first TMA issued, 1 = producer last TMA
 // issued, 2 = MMA got first stage, 3 = MMA committed last stage, 4 = epilogue got the
 // accumulator, 5 = epilogue done
-__device__ unsigned long long g_tc_probe[8][6][32];  // [launch % 8][role][tile]
+// [launch % 8][role][tile]; roles 0 prod first load, 1 prod last load, 2 mma after the first
+// full-wait, 3 mma commit, 4 epilogue start, 5 epilogue done, 6 mma before the first full-wait,
+// 7 mma before issuing the last K block; role 8: [0] kernel id (BN<<8 | SEGK<<4 | EPI), [1] grid
+constexpr int TC_PROBE_ROLES = 9;
+__device__ unsigned long long g_tc_probe[8][TC_PROBE_ROLES][32];
+// DMOE_TC_DEBUG=64: clock64 cycles per pipeline phase summed over all CTAs, [launch % 8][counter]:
+// 0 producer empty-wait, 1 producer loop, 2 mma tempty-wait, 3 mma full-wait, 4 mma zeroing,
+// 5 mma issue+commit, 6 mma loop, 7 epi tfull-wait (warp 4), 8 epi store-read wait, 9 epi loop,
+// 10 mma tiles, 11 CTAs, 12 mma issue without the commits
+__device__ unsigned long long g_tc_wait[8][16];
+#define WT_T0(v) const long long v = (p.dbg & 64) ? clock64() : 0
+#define WT_ADD(acc_, v) do { if (p.dbg & 64) acc_ += clock64() - v; } while (0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -196,6 +207,7 @@ struct TcParams {
   void* C;
   int E, N, K, Mdim;
   int64_t rows_single;
+  int max_ctas;   // grid cap (0: all SMs)
   int stages;     // M-major engine: smem ring depth (runtime, <= TC_MAX_STAGES)
   int table_len;  // M-major engine: per-expert smem table entries (0: tables stay in global)
   int slot;  // probe slot (launch ordinal % 8)
@@ -210,8 +222,7 @@ constexpr int TC_TABLE_LEN = TC_TABLE_E + 4;      // entries per table (16-byte 
 
 constexpr int TC_MAX_STAGES = 8;
 
-template <int BN> struct TcCfg {
-  static constexpr int ONES_BYTES = 16 * 128;    // [16 N][64 K] bf16 ones (K-major B operand)
+template <int BN, bool SEGK = false> struct TcCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
   // epilogue warps: 8 (two column halves) for tiles >= 128 wide.  4 warps on 256-wide tiles buy
   // a 4th ring stage but the epilogue then trails the mainloop (measured: mnist FFN fwd 78 -> 92 us)
@@ -222,26 +233,35 @@ template <int BN> struct TcCfg {
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
   // fixed smem without the per-expert tables (those are sized at launch: 2 x table_len ints)
-  static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + ONES_BYTES + EPI_WARPS * TC_STAGE_WARP + BN * 4 * 2;
+  // weight-gradient tiles (~1 K block each): a 3rd accumulator (when TMEM has room) lets the
+  // MMA run two tiles ahead, and each warp double-buffers its 4 KB store box so the TMA
+  // engine's read of one box overlaps the staging of the next
+  static constexpr int NACC = (SEGK && BN <= 128) ? 3 : 2;
+  static constexpr int STG_WARP = SEGK ? 8 * 1024 : TC_STAGE_WARP;
+  static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + EPI_WARPS * STG_WARP + BN * 4 * 2;
   static int stages_for(int table_len) {
     const int st = (TC_SMEM_MAX - FIXED - 2 * table_len * 4) / STAGE_BYTES;
     return st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
   }
   static int smem_for(int table_len) { return stages_for(table_len) * STAGE_BYTES + FIXED + 2 * table_len * 4; }
   static constexpr int pow2cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
-  static constexpr int TMEM_COLS = pow2cols(2 * BN);            // 2 accumulators
-  static constexpr int TMEM_COLS_CS = pow2cols(2 * BN + 32);    // + 2 x 16 columns (SEGK column sums)
+  static constexpr int TMEM_COLS = pow2cols(NACC * BN);                 // NACC accumulators
+  static_assert(TMEM_COLS <= 512, "TMEM");
 };
+
+__device__ __forceinline__ float bf16lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w & 0xFFFF0000u); }
 
 // bf16 h > 0  <=>  sign bit clear and not +0
 __device__ __forceinline__ bool bf16_pos(uint32_t b) { return b != 0 && !(b & 0x8000u); }
 
 template <int BN, bool SEGK, bool B_MN, int EPI>
-__global__ void __launch_bounds__(TcCfg<BN>::THREADS, 1)
+__global__ void __launch_bounds__(TcCfg<BN, SEGK>::THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   DMOE_PDL_ENTRY();
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, SEGK>;
+  constexpr int NACC = Cfg::NACC;
   const int S = p.stages;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
   constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
@@ -252,11 +272,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* full = (uint64_t*)(smem + S * Cfg::STAGE_BYTES);
   uint64_t* empty = full + TC_MAX_STAGES;
   uint64_t* tfull = empty + TC_MAX_STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-  uint8_t* ones_s = smem + S * Cfg::STAGE_BYTES + 1024;       // 1 KB aligned constant tile
-  uint8_t* stage_base = ones_s + Cfg::ONES_BYTES;             // 1 KB aligned (128B-swizzled TMA stores)
-  float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * TC_STAGE_WARP);  // [2][BN]
+  uint64_t* tempty = tfull + 4;
+  uint64_t* ready = tempty + 4;  // SEGK: stage fixed up (tail rows zeroed) for the MMA
+  uint32_t* tmem_slot = (uint32_t*)(ready + TC_MAX_STAGES);
+  uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 1024;   // 1 KB aligned (128B-swizzled TMA stores)
+  float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * Cfg::STG_WARP);  // [2][BN]
   int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [table_len]
   int32_t* plan_s = off_s + p.table_len;                                    // [table_len]
 
@@ -309,12 +329,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     __syncthreads();
   }
 
-  if (SEGK && p.colsum) {
-    for (int i = threadIdx.x; i < Cfg::ONES_BYTES / 4; i += blockDim.x)
-      reinterpret_cast<uint32_t*>(ones_s)[i] = 0x3F803F80u;  // bf16 1.0 x 2
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-
   // ---- tile space (identical walk in every role)
   const int NT = (p.N + BN - 1) / BN;
   const int MT = SEGK ? p.Mdim / TC_BM : 0;
@@ -323,16 +337,31 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   else if (p.offsets) total = plan[p.E] * NT;
   else total = (int)((p.rows_single + TC_BM - 1) / TC_BM) * NT;
 
+  // tile walk: every role strides the grid.  (A contiguous chunk of SEGK tiles per CTA, which
+  // would let consecutive tiles share the expert's operand rows, measured 45% slower on the
+  // transformer dW2: the 148 CTAs then stream 148 experts' rows at once instead of sharing one
+  // expert's rows through L2.)
+  const int t_begin = (int)blockIdx.x, t_end = total, t_step = (int)gridDim.x;
+
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
+  if ((p.dbg & 8) && blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < TC_PROBE_ROLES * 32; i += blockDim.x) (&g_tc_probe[p.slot][0][0])[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      g_tc_probe[p.slot][8][0] = (unsigned long long)((BN << 8) | (SEGK << 4) | EPI);
+      g_tc_probe[p.slot][8][1] = gridDim.x;
+    }
+  }
   if (warp == 1 && lane == 0) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], Cfg::EPI_WARPS); }
+    // SEGK: a stage is released by the MMA commit and by the fix-up warp (column sums)
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], SEGK ? 2 : 1); mbar_init(&ready[i], 1); }
+    for (int i = 0; i < NACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], Cfg::EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t tmem_cols = (SEGK && p.colsum) ? Cfg::TMEM_COLS_CS : Cfg::TMEM_COLS;
+  const uint32_t tmem_cols = Cfg::TMEM_COLS;
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(tmem_cols));
@@ -343,15 +372,23 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  // decode a tile -> (group e, row0, row_end, m0, n0, number of K blocks)
+  // decode a tile -> (group e, row0, row_end, m0, n0, number of K blocks).  SEGK caches the
+  // expert's segment bounds per thread (tiles of one expert are consecutive in the walk).
+  int c_e = -1;
+  int64_t c_r0 = 0, c_r1 = 0;
   auto decode = [&](int tile, int& e, int64_t& row0, int64_t& row_end, int& m0, int& n0, int& nkb) {
     if (SEGK) {
       e = tile / (MT * NT);
       const int rem = tile - e * MT * NT;
       m0 = (rem / NT) * TC_BM;
       n0 = (rem % NT) * BN;
-      row0 = offs[e];
-      row_end = offs[e + 1];
+      if (e != c_e) {
+        c_e = e;
+        c_r0 = offs[e];
+        c_r1 = offs[e + 1];
+      }
+      row0 = c_r0;
+      row_end = c_r1;
       nkb = (int)((row_end - row0 + TC_BK - 1) / TC_BK);
     } else {
       const int rt = tile / NT;
@@ -378,17 +415,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // sequence, so the loads into the smem ring mostly hit L2 (weights stream from HBM once).
     if (lane == 0) {
       constexpr int PF = 16;
-      int ptile = blockIdx.x, pkb = 0, pe = 0, pm0 = 0, pn0 = 0, pnkb = 0;
+      int ptile = t_begin, pkb = 0, pe = 0, pm0 = 0, pn0 = 0, pnkb = 0;
       int64_t prow0 = 0, prow_end = 0;
       auto pnext_tile = [&]() {
         while (ptile < total) {
           decode(ptile, pe, prow0, prow_end, pm0, pn0, pnkb);
           if (pnkb > 0) return;
-          ptile += gridDim.x;
+          ptile += t_step;
         }
       };
       auto prefetch_one = [&]() {
-        if (ptile >= total || !(p.dbg & 16)) return;  // opt-in (DMOE_TC_DEBUG=16): measured slower
+        if (ptile >= t_end || !(p.dbg & 16)) return;  // opt-in (DMOE_TC_DEBUG=16): measured slower
         if (SEGK) {
           const int kr = (int)(prow0 + pkb * TC_BK);
 #pragma unroll
@@ -401,7 +438,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         if (++pkb == pnkb) {
           pkb = 0;
-          ptile += gridDim.x;
+          ptile += t_step;
           pnext_tile();
         }
       };
@@ -414,12 +451,16 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+      long long w_empty = 0, w_loop = 0;
+      WT_T0(t_loop);
+      for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         int e, m0, n0, nkb;
         int64_t row0, row_end;
         decode(tile, e, row0, row_end, m0, n0, nkb);
         for (int kb = 0; kb < nkb; ++kb) {
+          WT_T0(t_e);
           mbar_wait(&empty[stage], phase ^ 1);
+          WT_ADD(w_empty, t_e);
           if (kb == 0) PROBE(0, it);
           if (kb == nkb - 1) PROBE(1, it);
           prefetch_one();
@@ -446,66 +487,141 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
+      WT_ADD(w_loop, t_loop);
+      if (p.dbg & 64) {
+        atomicAdd(&g_tc_wait[p.slot][0], (unsigned long long)w_empty);
+        atomicAdd(&g_tc_wait[p.slot][1], (unsigned long long)w_loop);
+        atomicAdd(&g_tc_wait[p.slot][11], 1ull);
+      }
     }
   } else if (warp == 1) {
     // ======================= MMA issuer =======================
     constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN);
-    constexpr uint32_t idesc_ones = make_idesc(16, A_MN, false);  // colsum: A^T x ones[16]
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+    long long w_te = 0, w_full = 0, w_zero = 0, w_issue = 0, w_loop = 0, n_tiles = 0, w_mmaonly = 0;
+    WT_T0(t_loop);
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
       int e, m0, n0, nkb;
       int64_t row0, row_end;
       decode(tile, e, row0, row_end, m0, n0, nkb);
       if (nkb == 0) continue;  // empty segment: the epilogue writes zeros without TMEM
+      ++n_tiles;
+      WT_T0(t_te);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
+      WT_ADD(w_te, t_te);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
       for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
+        if (kb == 0 && lane == 0) PROBE(6, it);
+        WT_T0(t_f);
+        mbar_wait(SEGK ? &ready[stage] : &full[stage], phase);
+        WT_ADD(w_full, t_f);
         tc_fence_after();
+        WT_T0(t_z);
         if (kb == 0 && lane == 0) PROBE(2, it);
         uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
-        if (SEGK && kb == nkb - 1) {
-          // zero the K rows past the segment end in both operands (they hold other
-          // experts' rows or uninitialised capacity rows)
-          const int valid = (int)(row_end - row0 - (int64_t)kb * TC_BK);
-          if (valid < TC_BK) {
-            const int lines = (TC_BK - valid);
-            const int nchunk = 2 + BN / 64;  // 128-byte lines per K row across A and B chunks
-            for (int i = lane; i < lines * nchunk * 8; i += 32) {
-              const int piece = i & 7, rest = i >> 3;
-              const int c = rest % nchunk, r = valid + rest / nchunk;
-              uint8_t* base = c < 2 ? sa + c * 8192 : sb + (c - 2) * 8192;
-              *reinterpret_cast<uint4*>(base + r * 128 + piece * 16) = make_uint4(0, 0, 0, 0);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          }
-          __syncwarp();
-        }
+        // SEGK: the last K block issues only the 16-row MMA slices that hold segment rows (the
+        // fix-up warp has zeroed the rest of the last slice)
+        int nk16 = TC_BK / 16;
+        if (SEGK && kb == nkb - 1) nk16 = (int)((row_end - row0 - (int64_t)kb * TC_BK + 15) >> 4);
+        WT_ADD(w_zero, t_z);
+        WT_T0(t_i);
         if (lane == 0) {
+          if (kb == nkb - 1) PROBE(7, it);
           const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k) {
-            if (p.dbg & 4) break;
+            if ((p.dbg & 4) || k >= nk16) break;
             const uint64_t ad = A_MN ? make_desc(a0 + k * 2048, 8192, 1024) : make_desc(a0 + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(b0 + k * 2048, 8192, 1024) : make_desc(b0 + k * 32, 16, 1024);
             tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
-            if (SEGK && p.colsum && n0 == 0)
-              tc_mma(tmem_base + 2 * BN + acc * 16, ad, make_desc(smem_u32(ones_s) + k * 32, 16, 1024), idesc_ones,
-                     (kb | k) != 0);
           }
+          WT_ADD(w_mmaonly, t_i);
           tc_commit(&empty[stage]);
           if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
         }
         __syncwarp();
+        WT_ADD(w_issue, t_i);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
+    }
+    WT_ADD(w_loop, t_loop);
+    if ((p.dbg & 64) && lane == 0) {
+      atomicAdd(&g_tc_wait[p.slot][2], (unsigned long long)w_te);
+      atomicAdd(&g_tc_wait[p.slot][3], (unsigned long long)w_full);
+      atomicAdd(&g_tc_wait[p.slot][4], (unsigned long long)w_zero);
+      atomicAdd(&g_tc_wait[p.slot][5], (unsigned long long)w_issue);
+      atomicAdd(&g_tc_wait[p.slot][6], (unsigned long long)w_loop);
+      atomicAdd(&g_tc_wait[p.slot][10], (unsigned long long)n_tiles);
+      atomicAdd(&g_tc_wait[p.slot][12], (unsigned long long)w_mmaonly);
+    }
+  } else if (SEGK && warp == 3) {
+    // ======================= fix-up (SEGK) =======================
+    // Between the TMA landing a stage and the MMA reading it: zero the rows past the segment
+    // end inside the last 16-row MMA slice (other experts' rows or uninitialised capacity rows,
+    // <= 15 lines of every operand chunk), then release the stage to the MMA (ready).  On the
+    // n0 == 0 tiles also sum A's columns over the segment rows (the bias gradient: db = sum
+    // of the rows of dout / dh), in row order in fp32, before releasing the stage (empty).
+    // Lane l owns A columns m0 + 4l .. 4l+3: chunk l/16, 16-byte unit (l%16)/2, half l%2.
+    int stage = 0;
+    uint32_t phase = 0;
+    const int cchunk = lane >> 4, cunit = (lane & 15) >> 1, chalf = lane & 1;
+    for (int tile = t_begin; tile < t_end; tile += t_step) {
+      int e, m0, n0, nkb;
+      int64_t row0, row_end;
+      decode(tile, e, row0, row_end, m0, n0, nkb);
+      const bool sums = p.colsum && n0 == 0;
+      float cs[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
+        uint8_t* sb = sa + Cfg::A_BYTES;
+        const int64_t left = row_end - row0 - (int64_t)kb * TC_BK;
+        const int valid = left < TC_BK ? (int)left : TC_BK;
+        const int lines = ((valid + 15) & ~15) - valid;
+        if (lines > 0) {
+          constexpr int nchunk = 2 + BN / 64;  // 128-byte lines per K row across A and B chunks
+          for (int i = lane; i < lines * nchunk * 8; i += 32) {
+            const int piece = i & 7, rest = i >> 3;
+            const int c = rest % nchunk, r = valid + rest / nchunk;
+            uint8_t* base = c < 2 ? sa + c * 8192 : sb + (c - 2) * 8192;
+            *reinterpret_cast<uint4*>(base + r * 128 + piece * 16) = make_uint4(0, 0, 0, 0);
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ready[stage]);
+        if (sums) {
+          // 16 rows' loads in flight per batch (shared memory is busy with TMA / MMA / stores)
+          const uint8_t* col = sa + cchunk * 8192 + chalf * 8;
+          int r = 0;
+          for (; r + 16 <= valid; r += 16) {
+            uint2 v[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              v[j] = *reinterpret_cast<const uint2*>(col + (r + j) * 128 + ((cunit ^ (j & 7)) << 4));
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              cs[0] += bf16lo(v[j].x); cs[1] += bf16hi(v[j].x); cs[2] += bf16lo(v[j].y); cs[3] += bf16hi(v[j].y);
+            }
+          }
+          for (; r < valid; ++r) {
+            const uint2 v = *reinterpret_cast<const uint2*>(col + r * 128 + ((cunit ^ (r & 7)) << 4));
+            cs[0] += bf16lo(v.x); cs[1] += bf16hi(v.x); cs[2] += bf16lo(v.y); cs[3] += bf16hi(v.y);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (++stage == S) { stage = 0; phase ^= 1; }
+      }
+      if (sums)
+        *reinterpret_cast<float4*>(p.colsum + (int64_t)e * p.Mdim + m0 + 4 * lane) = make_float4(cs[0], cs[1], cs[2], cs[3]);
     }
   } else if (warp >= 4) {
     // ======================= epilogue =======================
@@ -516,12 +632,16 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int q = warp & 3;
     const int c_beg = (ew >> 2) * Cfg::EPI_COLS;
     const uint64_t pol_out = (p.dbg & 32) ? l2_policy_last() : l2_policy_first();  // dW: written once
-    uint8_t* stg = stage_base + ew * TC_STAGE_WARP;
+    uint8_t* const stg_warp = stage_base + ew * Cfg::STG_WARP;
+    uint8_t* stg = stg_warp;
+    int stg_buf = 0;  // SEGK: which of the warp's two 4 KB store boxes
     int acc = 0;
     uint32_t acc_phase = 0;
     int bias_buf = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
+    long long w_tf = 0, w_st = 0, w_loop = 0;
+    WT_T0(t_loop);
+    for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
       int e, m0, n0, nkb;
       int64_t row0, row_end;
       decode(tile, e, row0, row_end, m0, n0, nkb);
@@ -561,7 +681,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
       }
       if (has_acc) {
+        WT_T0(t_tf);
         mbar_wait(&tfull[acc], acc_phase);
+        WT_ADD(w_tf, t_tf);
         tc_fence_after();
       }
       if (ew == 0 && lane == 0) PROBE(4, it);
@@ -590,6 +712,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
           }
           __syncwarp();
+        }
+        if (SEGK && !OUT_F32) {
+          // this box was last stored two boxes ago: at most the newest store may still be reading
+          stg = stg_warp + stg_buf * 4096;
+          WT_T0(t_st);
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          WT_ADD(w_st, t_st);
         }
         // TMEM -> registers -> epilogue math -> staging (row = lane)
 #pragma unroll
@@ -647,8 +777,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
         if (SEGK && !OUT_F32) {
-          // full 32 x 64 box: one bulk tensor store; the staging buffer is reused only after
-          // the engine has read it (wait_group.read)
+          // full 32 x 64 box: one bulk tensor store (double-buffered box, see above)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0 && !(p.dbg & 1)) {
@@ -658,8 +787,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 "r"(smem_u32(stg)), "r"(n0 + cs), "r"((int)((int64_t)e * p.Mdim + qrow0)), "l"(pol_out)
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           }
+          stg_buf ^= 1;
           __syncwarp();
           continue;
         }
@@ -681,24 +810,19 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
       }
-      if (SEGK && p.colsum && n0 == 0 && c_beg == 0) {
-        // column sums of A over the segment's rows (bias gradient), from the ones-MMA
-        float v = 0.0f;
-        if (has_acc) {
-          uint32_t r[16];
-          TMEM_LD16(tmem_base + ((uint32_t)(q * 32) << 16) + 2 * BN + acc * 16, r);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          v = __uint_as_float(r[0]);
-        }
-        p.colsum[(int64_t)e * p.Mdim + m0 + q * 32 + lane] = v;
-      }
       if (ew == 0 && lane == 0) PROBE(5, it);
       if (has_acc) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
       }
+    }
+    WT_ADD(w_loop, t_loop);
+    if ((p.dbg & 64) && ew == 0 && lane == 0) {
+      atomicAdd(&g_tc_wait[p.slot][7], (unsigned long long)w_tf);
+      atomicAdd(&g_tc_wait[p.slot][8], (unsigned long long)w_st);
+      atomicAdd(&g_tc_wait[p.slot][9], (unsigned long long)w_loop);
     }
   }
 
@@ -1094,26 +1218,36 @@ static int debug_flags() {
   }
   return f;
 }
+// the same flags for the weight-gradient (SEGK) launches only (their outputs feed nothing else)
+static int debug_flags_segk() {
+  static int f = -1;
+  if (f < 0) {
+    const char* e = getenv("DMOE_TC_DEBUG_SEGK");
+    f = e ? atoi(e) : 0;
+  }
+  return f;
+}
 
 template <int BN, bool SEGK, bool B_MN, int EPI>
 static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcParams& p,
                           int64_t max_tiles, cudaStream_t s) {
   auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
   const int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
-  const int smem = TcCfg<BN>::smem_for(table_len);
+  const int smem = TcCfg<BN, SEGK>::smem_for(table_len);
   static int attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = smem;
   }
-  int64_t grid = max_tiles < num_sms() ? max_tiles : num_sms();
+  const int64_t ctas = (p.max_ctas > 0 && p.max_ctas < num_sms()) ? p.max_ctas : num_sms();
+  int64_t grid = max_tiles < ctas ? max_tiles : ctas;
   if (grid < 1) grid = 1;
   TcParams pp = p;
-  pp.dbg = debug_flags();
+  pp.dbg = debug_flags() | (SEGK ? debug_flags_segk() : 0);
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  pp.stages = TcCfg<BN>::stages_for(table_len);
+  pp.stages = TcCfg<BN, SEGK>::stages_for(table_len);
   pp.table_len = table_len;
-  launch_pdl(kern, (unsigned)grid, TcCfg<BN>::THREADS, smem, s, a, b, c, pp);
+  launch_pdl(kern, (unsigned)grid, TcCfg<BN, SEGK>::THREADS, smem, s, a, b, c, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
 }
@@ -1158,6 +1292,7 @@ static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
   TcParams p{};
   p.offsets = g.offsets; p.plan = g.plan; p.bias = g.bias; p.aux = (const __nv_bfloat16*)g.aux;
   p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
+  p.max_ctas = g.max_ctas;
   const int64_t tiles = g.max_tiles * ((g.N + BN - 1) / BN);
   switch (BN) {
     case 256: return rows_bn<256>(g, ta, tb, p, tiles, s);
@@ -1238,10 +1373,11 @@ dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
 }
 
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
-  // weight-gradient tiles have ~1 K block each: a 128-wide N tile keeps 5 tiles in the smem
-  // ring instead of 3 (measured 48 vs 56 us per call at 64 rows/expert)
-  int BN = getenv("DMOE_TC_BN") ? pick_bn(g.N, true) : (g.N % 128 == 0 ? 128 : pick_bn(g.N, true));
-  if (g.colsum && BN > 128) BN = 128;  // TMEM: 2 x BN + 2 x 16 columns
+  // weight-gradient tiles have ~1 K block each and are bound by shared-memory traffic (TMA
+  // in, MMA operand reads, staging, TMA store reads): a 256-wide tile reads its operands at
+  // 96 B/clk instead of 128 and halves the per-tile control work (measured: transformer dW
+  // 11.7 -> 8.3 ms per GEMM before the fix-up warp took the tail zeroing off the MMA path)
+  const int BN = pick_bn(g.N, true);
   CUtensorMap ta, tb;
   // K rows past a segment end (other experts' rows, or capacity rows past R) are zeroed
   // in smem before the MMA; rows past R_cap are zero-filled by TMA.
@@ -1256,6 +1392,7 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   DMOE_TRY(make_map(&tc, g.C, 2, cdims, 32));
   TcParams p{};
   p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim; p.colsum = g.colsum;
+  p.max_ctas = g.max_ctas;
   const int64_t tiles = (int64_t)g.E * (g.Mdim / TC_BM) * (g.N / BN);
   if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
   return launch<128, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
@@ -1263,8 +1400,17 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
 
 }  // namespace dmoe
 
+extern "C" int dmoe_debug_tc_wait(unsigned long long* host, int reset) {
+  cudaDeviceSynchronize();
+  int r = (int)cudaMemcpyFromSymbol(host, dmoe::g_tc_wait, sizeof(dmoe::g_tc_wait));
+  if (reset) {
+    static unsigned long long zero[8 * 16] = {};
+    r |= (int)cudaMemcpyToSymbol(dmoe::g_tc_wait, zero, sizeof(zero));
+  }
+  return r;
+}
 extern "C" int dmoe_debug_tc_probe(unsigned long long* host, int n) {
-  if (n > 8 * 6 * 32) n = 8 * 6 * 32;
+  if (n > 8 * dmoe::TC_PROBE_ROLES * 32) n = 8 * dmoe::TC_PROBE_ROLES * 32;
   cudaDeviceSynchronize();
   return (int)cudaMemcpyFromSymbol(host, dmoe::g_tc_probe, n * sizeof(unsigned long long));
 }

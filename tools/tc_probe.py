@@ -5,7 +5,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-os.environ["DMOE_TC_DEBUG"] = "8"
+os.environ["DMOE_TC_DEBUG"] = str(8 | int(os.environ.get("DBG", "0")))
 import torch  # noqa: E402
 
 import bench  # noqa: E402
@@ -17,24 +17,31 @@ lay, x, dy, alive, resp = bench.build_layer(cfg, 0, torch.device("cuda", 0), cfg
 for _ in range(2):
     bench.run_calls(lay, x, dy, alive, resp)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (8 * 192))()
+R = 9
+buf = (ctypes.c_ulonglong * (8 * R * 32))()
 f = L._L.dmoe_debug_tc_probe
-names = ["prod0", "prodN", "mma0", "mmaC", "epi0", "epiD"]
+names = ["prod0", "prodN", "mma0", "mmaC", "epi0", "epiD", "mmaW", "mmaL"]
+order = [0, 1, 6, 2, 7, 3, 4, 5]
 c0 = L.dmoe_launch_counters()[1]
 bench.run_calls(lay, x, dy, alive, resp)
 torch.cuda.synchronize()
 c1 = L.dmoe_launch_counters()[1]
-f(buf, 8 * 192)
-labels = ["gate", "GEMM1 h", "GEMM2 out", "GEMM3 dh", "GEMM4 dxd", "GEMM5 dW2", "GEMM6 dW1"]
-for j, launch in enumerate(range(c0, c1)):
+f(buf, 8 * R * 32)
+want = os.environ.get("KERNEL")  # e.g. "128,1,4": BN, SEGK, EPI
+for launch in range(c0, c1):
     slot = launch % 8
-    t = [[buf[slot * 192 + r * 32 + i] for i in range(32)] for r in range(6)]
-    vals = [v for row in t for v in row if v]
+    t = [[buf[(slot * R + r) * 32 + i] for i in range(32)] for r in range(R)]
+    kid, grid = t[8][0], t[8][1]
+    bn, segk, epi = kid >> 8, (kid >> 4) & 15, kid & 15
+    if want and want != f"{bn},{segk},{epi}":
+        continue
+    vals = [v for row in t[:8] for v in row if v]
     if not vals:
         continue
     t0 = min(vals)
-    print("==", labels[j] if j < len(labels) else j, "CTA 0, us since its first event")
-    for i in range(12):
-        if not any(t[r][i] for r in range(6)):
+    print(f"== launch {launch - c0}: k_tc_gemm<BN={bn}, SEGK={segk}, EPI={epi}> grid {grid}; CTA 0, us since its first event")
+    for i in range(int(os.environ.get("NT", "12"))):
+        if not any(t[r][i] for r in range(8)):
             continue
-        print(f"tile {i:2d} " + " ".join(f"{names[r]}={(t[r][i] - t0) / 1e3:6.2f}" if t[r][i] else f"{names[r]}=   -  " for r in range(6)))
+        print(f"tile {i:2d} " + " ".join(f"{names[r]}={(t[r][i] - t0) / 1e3:7.2f}" if t[r][i] else f"{names[r]}=    -  "
+                                         for r in order))
