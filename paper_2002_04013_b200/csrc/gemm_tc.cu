@@ -414,7 +414,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // An L2 prefetch cursor runs PF k-blocks ahead of the loads over the same (tile, kb)
     // sequence, so the loads into the smem ring mostly hit L2 (weights stream from HBM once).
     if (lane == 0) {
-      constexpr int PF = 16;
+      constexpr int PF = SEGK ? 4 : 16;
       int ptile = t_begin, pkb = 0, pe = 0, pm0 = 0, pn0 = 0, pnkb = 0;
       int64_t prow0 = 0, prow_end = 0;
       auto pnext_tile = [&]() {
@@ -428,6 +428,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (ptile >= t_end || !(p.dbg & 16)) return;  // opt-in (DMOE_TC_DEBUG=16): measured slower
         if (SEGK) {
           const int kr = (int)(prow0 + pkb * TC_BK);
+          tma_prefetch_2d(&tmA, pm0, kr);
+          tma_prefetch_2d(&tmA, pm0 + 64, kr);
 #pragma unroll
           for (int c = 0; c < BN / 64; ++c) tma_prefetch_2d(&tmB, pn0 + 64 * c, kr);
         } else if (B_MN) {
