@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import gen
-from harness import CONFIGS, TOL, check_routing, gpu_layer, make_inputs, np64, oracle_step, rel_err
+from harness import CONFIGS, TOL, check_routing, gpu_layer, make_inputs, np64, oracle_step, rel_err, to_torch
 
 pytestmark = pytest.mark.gpu
 
@@ -123,3 +123,34 @@ def test_step_host_matches_device_step():
     lay.step_host(hx, hdy, hy, hdx, alive, resp)
     torch.cuda.synchronize()
     assert np.array_equal(np64(hy), y_ref) and np.array_equal(np64(hdx), dx_ref)
+
+
+def test_host_pipeline_matches_device_steps():
+    """HostPipeline (double-buffered staging, graphs, overlapped copies) gives, for each of a
+    sequence of different batches, exactly the y and dX of a device step on that batch."""
+    import torch
+    from paper_2002_04013_b200.host_pipeline import HostPipeline
+    cfg = CONFIGS["mnist"]
+    T = 513
+    batches = [make_inputs(cfg, seed=20 + i, T=T) for i in range(5)]
+    lay = gpu_layer(cfg, batches[0])
+    _, _, alive, resp = lay._inputs
+    want, host = [], []
+    for inp in batches:
+        x = to_torch(inp["dev_X"], cfg.dtype, (T, cfg.D))
+        dy = to_torch(inp["dev_dY"], cfg.dtype, (T, cfg.D))
+        lay.step(x, dy, alive, resp)
+        torch.cuda.synchronize()
+        want.append((np64(lay.y[:T]).copy(), np64(lay.dx[:T]).copy()))
+        hx, hdy = x.cpu().pin_memory(), dy.cpu().pin_memory()
+        host.append((hx, hdy, torch.empty_like(hx).pin_memory(), torch.empty_like(hx).pin_memory()))
+    pipe = HostPipeline(lay, T, alive, resp)
+    for rep in range(2):  # a second pass reuses both staging slots
+        for hx, hdy, hy, hdx in host:
+            hy.zero_()
+            hdx.zero_()
+        for hx, hdy, hy, hdx in host:
+            pipe.submit(hx, hdy, hy, hdx)
+        pipe.synchronize()
+        for (y_ref, dx_ref), (_, _, hy, hdx) in zip(want, host):
+            assert np.array_equal(np64(hy), y_ref) and np.array_equal(np64(hdx), dx_ref)

@@ -13,7 +13,10 @@ for r in rows:
         d = dict(zip(hdr, r))
         if d.get("Metric Name") == "gpu__time_duration.sum":
             out.append((d["Kernel Name"].split("(")[0][:70], float(d["Metric Value"]) / 1000))
-starts = [i for i, o in enumerate(out) if first in o[0]]
+# a step starts at the gate's transpose, i.e. a k_transpose followed by a tcgen05 GEMM (the gate
+# backward's transpose is followed by k_gate_bwd_dx)
+starts = [i for i, o in enumerate(out) if first in o[0] and (first != "k_transpose" or
+                                                             (i + 1 < len(out) and "k_tc_gemm" in out[i + 1][0]))]
 i0 = starts[-2] if len(starts) > 1 else 0
 i1 = starts[-1] if len(starts) > 1 else len(out)
 tot = sum(o[1] for o in out[i0:i1])
