@@ -162,11 +162,12 @@ def run_calls(lay, x, dy, alive, resp, ev=None):
         lambda: L.dmoe_beam_topk(lay.G[:T], g, alive, lay.sel[:T], lay.sel_score[:T], lay.ws),
         lambda: L.dmoe_dispatch(x, g, lay.sel[:T], lay.sel_score[:T], resp, lay.w[:T], lay.valid[:T], lay.n_dropped,
                                 lay.counts, lay.offsets, lay.row_of_slot[:T], lay.token_of_row, lay.xd, lay.ws),
-        lambda: L.dmoe_expert_ffn_fwd(lay.xd, lay.offsets, lay.W1, lay.b1, lay.W2, lay.b2, lay.h, lay.out, lay.ws),
+        lambda: L.dmoe_expert_ffn_fwd(lay.xd, lay.offsets, lay.W1, lay.b1, lay.W2, lay.b2, lay.h, lay.out, lay.ws,
+                                      hmask=lay.hmask),
         lambda: L.dmoe_combine(lay.out, lay.row_of_slot[:T], lay.w[:T], lay.valid[:T], lay.y[:T]),
         lambda: L.dmoe_combine_bwd(dy, lay.out, lay.row_of_slot[:T], lay.w[:T], lay.dout, lay.dscore[:T]),
         lambda: L.dmoe_expert_ffn_bwd(lay.xd, lay.h, lay.dout, lay.offsets, lay.W1, lay.W2, lay.dxd, lay.dW1,
-                                      lay.db1, lay.dW2, lay.db2, lay.ws),
+                                      lay.db1, lay.dW2, lay.db2, lay.ws, hmask=lay.hmask),
         lambda: L.dmoe_gate_bwd(x, lay.Wg, lay.sel[:T], lay.dscore[:T], lay.dxd, lay.row_of_slot[:T], g,
                                 lay.dx[:T], lay.dWg, lay.dbg, lay.ws),
     ]

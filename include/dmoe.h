@@ -135,11 +135,15 @@ dmoe_status dmoe_dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, dm
  *   out[r] = W2[e] h[r] + b2[e]            (D outputs, dt)
  * xd [R_cap, D] dt; offsets [E_local+1] int32 device, non-decreasing, offsets[E_local] <= R_cap;
  * W1 [E_local, H, D] dt; b1 [E_local, H] fp32; W2 [E_local, D, H] dt; b2 [E_local, D] fp32;
- * h [R_cap, H] dt (out); out [R_cap, D] dt (out).  bf16 needs D % 64 == 0, H % 64 == 0. */
+ * h [R_cap, H] dt (out); out [R_cap, D] dt (out).  bf16 needs D % 64 == 0, H % 64 == 0.
+ * hmask: optional (NULL) packed ReLU record for the backward, [H/32][R_cap] uint32 (out):
+ *   bit c of hmask[w * R_cap + r] = (stored h[r, 32w + c] > 0) — the bit X13's derivative
+ *   needs — 1/16 of h's bytes; written for rows < offsets[E_local] when the bf16 tensor-core
+ *   path runs (left untouched otherwise, and then the backward reads h). */
 dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t E_local,
                                 int64_t R_cap, int32_t D, int32_t H, dmoe_dtype dt,
                                 const void* W1, const float* b1, const void* W2, const float* b2,
-                                void* h, void* out, void* ws, size_t ws_bytes,
+                                void* h, uint32_t* hmask, void* out, void* ws, size_t ws_bytes,
                                 dmoe_stream_t stream);
 
 /* S7 — combine, Eq. 3: y[t] = sum_{ok s} w[t,s] out[row_of_slot[t,s]]
@@ -162,8 +166,10 @@ dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row
  *   dW2[e] = sum_rows dout^T h;  db2[e] = sum_rows dout
  *   dW1[e] = sum_rows dh^T xd;   db1[e] = sum_rows dh      (0 for experts without rows)
  * dxd [R_cap, D] dt (out); dW1 [E_local, H, D] dt; dW2 [E_local, D, H] dt; db1 [E_local, H]
- * and db2 [E_local, D] fp32 (out). */
-dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
+ * and db2 [E_local, D] fp32 (out).  hmask: optional (NULL), the packed ReLU record the forward
+ * call wrote for these rows (same xd/offsets/h); when given, the dh GEMM reads its mask bits
+ * instead of h (the same decisions, 1/16 of the bytes). */
+dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
                                 const int32_t* offsets, int32_t E_local, int64_t R_cap,
                                 int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
                                 const void* W2, void* dxd, void* dW1, float* db1, void* dW2,

@@ -49,11 +49,11 @@ _SIGS = {
     "dmoe_beam_topk": ([_P, _I64, dmoe_grid, _P, _P, _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_dispatch": ([_P, _I32, _I64, _I32, dmoe_grid, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                        _SZ, _P], ctypes.c_int),
-    "dmoe_expert_ffn_fwd": ([_P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
+    "dmoe_expert_ffn_fwd": ([_P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _SZ, _P],
                             ctypes.c_int),
     "dmoe_combine": ([_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P], ctypes.c_int),
     "dmoe_combine_bwd": ([_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P], ctypes.c_int),
-    "dmoe_expert_ffn_bwd": ([_P, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
+    "dmoe_expert_ffn_bwd": ([_P, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                              _SZ, _P], ctypes.c_int),
     "dmoe_gate_bwd": ([_P, _P, _P, _P, _P, _P, _I64, _I32, dmoe_grid, _I32, _P, _P, _P, _P, _SZ, _P],
                       ctypes.c_int),
@@ -137,11 +137,11 @@ def dmoe_dispatch(x, g, sel, sel_score, responded_bits, w, valid, n_dropped, cou
         ws.numel() * ws.element_size(), _stream()))
 
 
-def dmoe_expert_ffn_fwd(xd, offsets, W1, b1, W2, b2, h, out, ws):
+def dmoe_expert_ffn_fwd(xd, offsets, W1, b1, W2, b2, h, out, ws, hmask=None):
     E_local, H, D = W1.shape
     _check("dmoe_expert_ffn_fwd", _L.dmoe_expert_ffn_fwd(
         _p(xd), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd), _p(W1), _p(b1), _p(W2), _p(b2), _p(h),
-        _p(out), _p(ws), ws.numel() * ws.element_size(), _stream()))
+        _p(hmask) if hmask is not None else None, _p(out), _p(ws), ws.numel() * ws.element_size(), _stream()))
 
 
 def dmoe_combine(out, row_of_slot, w, valid, y):
@@ -157,10 +157,10 @@ def dmoe_combine_bwd(dy, out, row_of_slot, w, dout, dscore):
                                                    _stream()))
 
 
-def dmoe_expert_ffn_bwd(xd, h, dout, offsets, W1, W2, dxd, dW1, db1, dW2, db2, ws):
+def dmoe_expert_ffn_bwd(xd, h, dout, offsets, W1, W2, dxd, dW1, db1, dW2, db2, ws, hmask=None):
     E_local, H, D = W1.shape
     _check("dmoe_expert_ffn_bwd", _L.dmoe_expert_ffn_bwd(
-        _p(xd), _p(h), _p(dout), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd), _p(W1), _p(W2), _p(dxd),
+        _p(xd), _p(h), _p(hmask) if hmask is not None else None, _p(dout), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd), _p(W1), _p(W2), _p(dxd),
         _p(dW1), _p(db1), _p(dW2), _p(db2), _p(ws), ws.numel() * ws.element_size(), _stream()))
 
 

@@ -120,6 +120,19 @@ static dmoe_status segk_gemm(const GemmSegK& g, dmoe_dtype dt, cudaStream_t s) {
 }
 constexpr int kPlanBM_SIMT = 64;
 
+// The packed ReLU record is produced by the forward's h GEMM and consumed by the backward's dh
+// GEMM only when both run on the M-major tcgen05 engine; both calls evaluate this same test.
+static bool hmask_path(dmoe_dtype dt, int32_t D, int32_t H, int32_t E, int64_t R_cap) {
+  static const bool off = getenv("DMOE_NO_HMASK") != nullptr;  // A/B experiments
+  if (off || dt != DMOE_BF16 || H % 32 != 0 || !tc_rows_mmajor()) return false;
+  GemmRows f{}, b{};
+  f.E = b.E = E; f.N = b.N = H; f.K = b.K = D; f.rows_cap = b.rows_cap = R_cap;
+  f.offsets = b.offsets = reinterpret_cast<const int32_t*>(16);  // grouped form (value unused)
+  f.b_mn = false; f.epi = EPI_BIAS_RELU;
+  b.b_mn = true; b.epi = EPI_RELU_MASK;
+  return tc_rows_supported(f) && tc_rows_supported(b);
+}
+
 static int num_sms_api() {
   static int n = 0;
   if (!n) {
@@ -290,7 +303,7 @@ dmoe_status dmoe_dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, dm
 dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t E_local,
                                 int64_t R_cap, int32_t D, int32_t H, dmoe_dtype dt,
                                 const void* W1, const float* b1, const void* W2, const float* b2,
-                                void* h, void* out, void* ws, size_t ws_bytes,
+                                void* h, uint32_t* hmask, void* out, void* ws, size_t ws_bytes,
                                 dmoe_stream_t stream) {
   DMOE_TRY(check_dt(dt, D));
   DMOE_TRY(check_dt(dt, H));
@@ -307,6 +320,7 @@ dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t 
   g1.E = E_local; g1.N = H; g1.K = D; g1.rows_cap = R_cap; g1.b_mn = false; g1.epi = EPI_BIAS_RELU;
   GemmRows g2 = g1;
   g2.A = h; g2.B = W2; g2.C = out; g2.bias = b2; g2.N = D; g2.K = H; g2.epi = EPI_BIAS;
+  if (hmask && hmask_path(dt, D, H, E_local, R_cap)) { g1.hmask = hmask; g1.hmask_ld = R_cap; }
   for (GemmRows* g : {&g1, &g2}) {
     const bool tc = dt == DMOE_BF16 && tc_rows_supported(*g);
     const int bm = tc ? tc_rows_tile(*g) : kPlanBM_SIMT;
@@ -336,7 +350,7 @@ dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row
   return combine_bwd(dy, out, row_of_slot, w, T, D, k, dt, dout, dscore, (cudaStream_t)stream);
 }
 
-dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
+dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
                                 const int32_t* offsets, int32_t E_local, int64_t R_cap,
                                 int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
                                 const void* W2, void* dxd, void* dW1, float* db1, void* dW2,
@@ -357,8 +371,10 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const void* dout,
   GemmRows g3{};
   g3.A = dout; g3.B = W2; g3.C = dh; g3.aux = h; g3.offsets = offsets;
   g3.E = E_local; g3.N = H; g3.K = D; g3.rows_cap = R_cap; g3.b_mn = true; g3.epi = EPI_RELU_MASK;
+  if (hmask && hmask_path(dt, D, H, E_local, R_cap)) { g3.hmask = const_cast<uint32_t*>(hmask); g3.hmask_ld = R_cap; }
   GemmRows g4 = g3;
   g4.A = dh; g4.B = W1; g4.C = dxd; g4.aux = nullptr; g4.N = D; g4.K = H; g4.epi = EPI_PLAIN;
+  g4.hmask = nullptr;
   for (GemmRows* g : {&g3, &g4}) {
     const bool tc = dt == DMOE_BF16 && tc_rows_supported(*g);
     const int bm = tc ? tc_rows_tile(*g) : kPlanBM_SIMT;

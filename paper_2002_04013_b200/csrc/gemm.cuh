@@ -28,6 +28,8 @@ struct GemmRows {
   bool b_mn;
   int epi;
   int max_ctas = 0;        // persistent grid cap (0: one CTA per SM); leaves SMs to a concurrent GEMM
+  uint32_t* hmask = nullptr;  // packed ReLU mask [N/32][hmask_ld]: EPI_BIAS_RELU writes, EPI_RELU_MASK reads
+  int64_t hmask_ld = 0;
 };
 
 // SEGK family: C_e[m, n] = sum_{r in seg e} A[r, m] B[r, n]  (K = segment rows)
@@ -54,7 +56,8 @@ dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s);
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s);
 bool tc_rows_supported(const GemmRows& g);
 int tc_rows_tile(const GemmRows& g);
-int tc_plan_in_kernel_max();  // experts up to which the M-major engine plans row tiles itself  // token rows per tile of the row engine (plan granularity)
+int tc_plan_in_kernel_max();
+bool tc_rows_mmajor();  // the M-major row engine (not the swap-AB experiment) runs the row GEMMs  // experts up to which the M-major engine plans row tiles itself  // token rows per tile of the row engine (plan granularity)
 bool tc_segk_supported(const GemmSegK& g);
 bool tc_segk_colsum_supported(const GemmSegK& g);  // the SEGK engine also writes colsum
 

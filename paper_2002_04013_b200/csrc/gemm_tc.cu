@@ -204,6 +204,9 @@ struct TcParams {
   const float* bias;
   float* colsum;             // SEGK: optional [E][Mdim] column sums of A (the bias gradient)
   const __nv_bfloat16* aux;  // ReLU mask source [rows, N]
+  uint32_t* hmask;           // packed ReLU mask [N/32][hmask_ld] (bit c of word (w,row) = h[row, 32w+c] > 0):
+                             // written by EPI_BIAS_RELU, read instead of aux by EPI_RELU_MASK
+  int64_t hmask_ld;
   void* C;
   int E, N, K, Mdim;
   int64_t rows_single;
@@ -348,11 +351,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
   if ((p.dbg & 8) && blockIdx.x == 0) {
+    const unsigned long long t_entry = gtimer();
     for (int i = threadIdx.x; i < TC_PROBE_ROLES * 32; i += blockDim.x) (&g_tc_probe[p.slot][0][0])[i] = 0;
     __syncthreads();
     if (threadIdx.x == 0) {
       g_tc_probe[p.slot][8][0] = (unsigned long long)((BN << 8) | (SEGK << 4) | EPI);
       g_tc_probe[p.slot][8][1] = gridDim.x;
+      g_tc_probe[p.slot][8][2] = t_entry;
     }
   }
   if (warp == 1 && lane == 0) {
@@ -371,6 +376,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if ((p.dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0) g_tc_probe[p.slot][8][3] = gtimer();
 
   // decode a tile -> (group e, row0, row_end, m0, n0, number of K blocks).  SEGK caches the
   // expert's segment bounds per thread (tiles of one expert are consecutive in the walk).
@@ -670,7 +676,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       // loads before waiting for the accumulator so their latency hides behind the MMA
       constexpr int NSUB = (Cfg::EPI_COLS + SUB - 1) / SUB;
       uint4 hreg[EPI == EPI_RELU_MASK ? NSUB : 1][8];
-      if (EPI == EPI_RELU_MASK) {
+      constexpr int NW = Cfg::EPI_COLS >= 32 ? Cfg::EPI_COLS / 32 : 1;  // packed mask words of this warp's columns
+      uint32_t mword[EPI == EPI_RELU_MASK ? NW : 1];
+      if (EPI == EPI_RELU_MASK && p.hmask) {
+        // one coalesced 4-byte load per 32 columns: lane = row (the TMEM row layout)
+#pragma unroll
+        for (int w = 0; w < NW; ++w)
+          mword[w] = lane < live_rows ? __ldg(p.hmask + (int64_t)((n0 + c_beg) / 32 + w) * p.hmask_ld + qrow0 + lane) : 0u;
+      } else if (EPI == EPI_RELU_MASK) {
 #pragma unroll
         for (int sb = 0; sb < NSUB; ++sb)
 #pragma unroll
@@ -694,7 +707,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int cs = c_beg + sb * SUB;
         const int ncols = (c_beg + Cfg::EPI_COLS - cs) < SUB ? (c_beg + Cfg::EPI_COLS - cs) : SUB;  // multiple of 16
         uint32_t hmask[SUB / 32] = {};
-        if (EPI == EPI_RELU_MASK) {
+        if (EPI == EPI_RELU_MASK && p.hmask) {
+#pragma unroll
+          for (int w = 0; w < SUB / 32; ++w) hmask[w] = mword[sb * (SUB / 32) + w];
+        } else if (EPI == EPI_RELU_MASK) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), piece = lane & 7;
@@ -724,6 +740,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           WT_ADD(w_st, t_st);
         }
         // TMEM -> registers -> epilogue math -> staging (row = lane)
+        uint32_t mw_lo = 0;  // EPI_BIAS_RELU: packed-mask bits of the first 16 columns of a word
+        (void)mw_lo;
 #pragma unroll
         for (int c16 = 0; c16 < SUB; c16 += 16) {
           if (c16 >= ncols) break;
@@ -745,6 +763,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           if (EPI == EPI_BIAS_RELU) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.0f);
+            if (p.hmask) {
+              // bit = (stored bf16 h > 0), the decision the backward would take from h: with
+              // round-to-nearest-even a non-negative fp32 v rounds to a nonzero bf16 iff
+              // v > 2^-134 (half the smallest bf16 subnormal; no flush-to-zero in this build)
+              uint32_t bits = 0;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) bits |= (v[j] > 0x1p-134f ? 1u : 0u) << j;
+              const int col = n0 + cs + c16;  // multiple of 16
+              if ((col & 31) == 0) mw_lo = bits;
+              else if (lane < live_rows && !(p.dbg & 1))
+                p.hmask[(int64_t)(col >> 5) * p.hmask_ld + qrow0 + lane] = mw_lo | (bits << 16);
+            }
           }
           if (EPI == EPI_RELU_MASK) {
 #pragma unroll
@@ -829,8 +859,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
 
   if (SEGK && warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if ((p.dbg & 8) && blockIdx.x == 0 && warp == 4 && lane == 0) g_tc_probe[p.slot][8][4] = gtimer();
   tc_fence_before();
   __syncthreads();
+  if ((p.dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0) g_tc_probe[p.slot][8][5] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
@@ -1175,6 +1207,7 @@ static int pick_bn_balanced(int N, bool b_mn, int64_t units) {
 
 static bool rows_swap();
 int tc_plan_in_kernel_max() { return rows_swap() ? 0 : TC_TABLE_E; }
+bool tc_rows_mmajor() { return !rows_swap(); }
 
 static bool rows_swap() {
   static int v = -1;
@@ -1295,6 +1328,7 @@ static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
   p.offsets = g.offsets; p.plan = g.plan; p.bias = g.bias; p.aux = (const __nv_bfloat16*)g.aux;
   p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
   p.max_ctas = g.max_ctas;
+  p.hmask = g.hmask; p.hmask_ld = g.hmask_ld;
   const int64_t tiles = g.max_tiles * ((g.N + BN - 1) / BN);
   switch (BN) {
     case 256: return rows_bn<256>(g, ta, tb, p, tiles, s);

@@ -51,6 +51,8 @@ class DMoELayer:
         self.token_of_row = e(max(T * k, 1), dt=torch.int32)
         self.xd = e(max(R, 1), D)
         self.h = e(max(R, 1), H)
+        # packed ReLU record [H/32, R_cap] (forward -> backward): 1/16 of h's bytes for dh's mask
+        self.hmask = e((H + 31) // 32, max(R, 1), dt=torch.int32)
         self.out = e(max(R, 1), D)
         self.y = e(T, D)
         self.dout = e(max(R, 1), D)
@@ -71,7 +73,7 @@ class DMoELayer:
                         self.n_dropped, self.counts, self.offsets, self.row_of_slot[:T], self.token_of_row,
                         self.xd, self.ws)
         L.dmoe_expert_ffn_fwd(self.xd, self.offsets, self.W1, self.b1, self.W2, self.b2, self.h, self.out,
-                              self.ws)
+                              self.ws, hmask=self.hmask)
         L.dmoe_combine(self.out, self.row_of_slot[:T], self.w[:T], self.valid[:T], self.y[:T])
         return self.y[:T]
 
@@ -81,7 +83,7 @@ class DMoELayer:
         T = x.shape[0]
         L.dmoe_combine_bwd(dy, self.out, self.row_of_slot[:T], self.w[:T], self.dout, self.dscore[:T])
         L.dmoe_expert_ffn_bwd(self.xd, self.h, self.dout, self.offsets, self.W1, self.W2, self.dxd,
-                              self.dW1, self.db1, self.dW2, self.db2, self.ws)
+                              self.dW1, self.db1, self.dW2, self.db2, self.ws, hmask=self.hmask)
         L.dmoe_gate_bwd(x, self.Wg, self.sel[:T], self.dscore[:T], self.dxd, self.row_of_slot[:T], self.g,
                         self.dx[:T], self.dWg, self.dbg, self.ws)
         return self.dx[:T]

@@ -48,7 +48,7 @@ class FakeLib:
         xd[: len(t)] = x[torch.from_numpy(t).long()]
 
     @staticmethod
-    def dmoe_expert_ffn_fwd(xd, offsets, W1, b1, W2, b2, h, out, ws):
+    def dmoe_expert_ffn_fwd(xd, offsets, W1, b1, W2, b2, h, out, ws, hmask=None):
         off = offsets.numpy()
         R = int(off[-1])
         a, o = O.ffn_fwd(xd[:R].numpy(), off, W1.numpy(), b1.numpy(), W2.numpy(), b2.numpy())
@@ -67,7 +67,7 @@ class FakeLib:
         dscore[:] = torch.from_numpy(ds)
 
     @staticmethod
-    def dmoe_expert_ffn_bwd(xd, h, dout, offsets, W1, W2, dxd, dW1, db1, dW2, db2, ws):
+    def dmoe_expert_ffn_bwd(xd, h, dout, offsets, W1, W2, dxd, dW1, db1, dW2, db2, ws, hmask=None):
         off = offsets.numpy()
         R = int(off[-1])
         dx, a, b, c, d = O.ffn_bwd(xd[:R].numpy(), h[:R].numpy(), dout[:R].numpy(), off, W1.numpy(), W2.numpy())

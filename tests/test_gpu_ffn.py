@@ -58,6 +58,17 @@ def _run(counts, D, H, dtype, seed=0, cap_extra=37):
                 dxd=rel_err(np64(dxd[:R]), dx_ref), dW1=rel_err(np64(dW1), dW1_ref),
                 db1=rel_err(np64(db1), db1_ref), dW2=rel_err(np64(dW2), dW2_ref), db2=rel_err(np64(db2), db2_ref))
     assert all(v <= tol for v in errs.values()), errs
+    # the packed ReLU record (forward -> backward) reproduces the h-read masks bit for bit
+    hm = torch.full(((H + 31) // 32, Rc), -1, dtype=torch.int32, device="cuda")
+    h2, out2 = torch.empty_like(h), torch.empty_like(out)
+    P.dmoe_expert_ffn_fwd(xd, off, W1, b1, W2, b2, h2, out2, ws, hmask=hm)
+    dxd2, dW12, dW22 = torch.empty_like(dxd), torch.empty_like(dW1), torch.empty_like(dW2)
+    db12, db22 = torch.empty_like(db1), torch.empty_like(db2)
+    P.dmoe_expert_ffn_bwd(xd, h2, dout, off, W1, W2, dxd2, dW12, db12, dW22, db22, ws, hmask=hm)
+    torch.cuda.synchronize()
+    for a, b in [(h[:R], h2[:R]), (out[:R], out2[:R]), (dxd[:R], dxd2[:R]), (dW1, dW12), (dW2, dW22), (db1, db12),
+                 (db2, db22)]:
+        assert torch.equal(a, b)
     for i in np.nonzero(counts == 0)[0]:
         assert (np64(dW1[i]) == 0).all() and (np64(dW2[i]) == 0).all() and (np64(db1[i]) == 0).all()
     return errs

@@ -35,11 +35,15 @@ for launch in range(c0, c1):
     bn, segk, epi = kid >> 8, (kid >> 4) & 15, kid & 15
     if want and want != f"{bn},{segk},{epi}":
         continue
-    vals = [v for row in t[:8] for v in row if v]
+    vals = [v for row in t[:8] for v in row if v] + [v for v in t[8][2:6] if v]
     if not vals:
         continue
     t0 = min(vals)
     print(f"== launch {launch - c0}: k_tc_gemm<BN={bn}, SEGK={segk}, EPI={epi}> grid {grid}; CTA 0, us since its first event")
+    ent, setup, epi_end, ext = t[8][2], t[8][3], t[8][4], t[8][5]
+    if ent:
+        us = lambda v: f"{(v - t0) / 1e3:7.2f}" if v else "   -   "
+        print(f"   entry(after PDL wait) {us(ent)}  setup done {us(setup)}  epilogue-warp-0 done {us(epi_end)}  exit {us(ext)}")
     for i in range(int(os.environ.get("NT", "12"))):
         if not any(t[r][i] for r in range(8)):
             continue
