@@ -262,8 +262,28 @@ template <int BN, bool SEGK, bool B_MN, int EPI>
 __global__ void __launch_bounds__(TcCfg<BN, SEGK>::THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const TcParams p) {
-  DMOE_PDL_ENTRY();
   using Cfg = TcCfg<BN, SEGK>;
+  // Before waiting for the previous kernel (programmatic dependent launch: this CTA may already
+  // sit on an SM the previous grid freed while its last CTAs finish): pull the expert weights of
+  // this CTA's first tile into L2.  Weights are parameters no kernel of the step writes, and a
+  // prefetch never changes what the loads after the wait see, so this needs no ordering.  The
+  // tile's expert is guessed as its row tile (one 128-row tile per expert); a wrong guess only
+  // warms another expert's weights.
+  if (!SEGK && p.offsets && (p.dbg & 128) == 0 && threadIdx.x == 0) {
+    const int nt = (p.N + BN - 1) / BN;
+    const int rt = (int)blockIdx.x / nt, n0 = ((int)blockIdx.x % nt) * BN;
+    const int e = rt < p.E ? rt : p.E - 1;
+    const int nkb = p.K / TC_BK;
+    const int npf = nkb < 8 ? nkb : 8;
+    for (int kb = 0; kb < npf; ++kb) {
+      if (B_MN) {
+        for (int c = 0; c < BN / 64; ++c) tma_prefetch_3d(&tmB, n0 + 64 * c, kb * TC_BK, e);
+      } else {
+        tma_prefetch_3d(&tmB, kb * TC_BK, n0, e);
+      }
+    }
+  }
+  DMOE_PDL_ENTRY();
   constexpr int NACC = Cfg::NACC;
   const int S = p.stages;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
