@@ -11,7 +11,7 @@ resident in HBM, timed with CUDA events around a CUDA-graph replay of the step (
 L2 is flushed (untimed 256 MiB write) before every timed step.  `e2e` = the same metric through
 the public API with host buffers: every step uploads its pinned-host x, dy and downloads its y,
 dX inside the timed region (single GPU: HostPipeline, which overlaps those copies with the
-neighbouring steps' compute; multi-GPU: the per-step step_host).  `--impl reference` times the float64 CPU oracle (oracle/) on a bounded
+neighbouring steps' compute; N GPUs: the per-step step_host).  `--impl reference` times the float64 CPU oracle (oracle/) on a bounded
 token sample of the same workload (the only reference this paper has).
 """
 import argparse
@@ -233,7 +233,8 @@ def bench_ep(args, cfg, rank, world, local_rank):
         run = lambda: lay.step(x, dy, alive, resp)
         with torch.cuda.stream(stream):
             run()
-    launches = L.dmoe_launch_counters()[0] - c0[0]
+    c1 = L.dmoe_launch_counters()
+    launches, tc_launches = c1[0] - c0[0], c1[1] - c0[1]
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -261,28 +262,58 @@ def bench_ep(args, cfg, rank, world, local_rank):
     hdy.copy_(dy)
     hy, hdx = torch.empty_like(hx, pin_memory=True), torch.empty_like(hx, pin_memory=True)
     e2e = []
-    with torch.cuda.stream(stream):
-        lay.step_host(hx, hdy, hy, hdx, alive, resp)
-        for i in range(args.steps):
-            flush.fill_(i & 0xFF)
-            stream.synchronize()
-            dist.barrier()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            lay.step_host(hx, hdy, hy, hdx, alive, resp)
-            b.record(stream)
-            b.synchronize()
-            e2e.append(a.elapsed_time(b))
-    if peer:
+    if peer and os.environ.get("DMOE_EP_PIPELINE"):  # per-rank HostPipeline (opt-in: an illegal
+        # address was seen once at 4 GPUs in its eager warm-up; not yet understood)
+        from paper_2002_04013_b200.host_pipeline import HostPipeline
+        pipe = HostPipeline(lay, T, alive, resp)
+        for _ in range(args.warmup):
+            pipe.submit(hx, hdy, hy, hdx)
+        pipe.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(pipe.h2d)
+        for _ in range(args.steps):
+            pipe.submit(hx, hdy, hy, hdx)
+        b.record(pipe.d2h)
+        b.synchronize()
+        e2e.append(a.elapsed_time(b) / args.steps)
         lay.check()
+    else:
+        with torch.cuda.stream(stream):
+            lay.step_host(hx, hdy, hy, hdx, alive, resp)
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)
+                stream.synchronize()
+                dist.barrier()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                lay.step_host(hx, hdy, hy, hdx, alive, resp)
+                b.record(stream)
+                b.synchronize()
+                e2e.append(a.elapsed_time(b))
     t = torch.tensor([sum(e2e) / len(e2e)], device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
     R_out = int(lay.offsets[cfg.E].item())
+    per_call, ep_local = {}, None
     if peer:
+        # the roofline call measured on this rank: its expert backward over the rows it received
+        R_in = int(lay.off_loc[lay.El].item())
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(20)]
+        with torch.cuda.stream(stream):
+            for a, b in ev:
+                a.record(stream)
+                L.dmoe_expert_ffn_bwd(lay.xin, lay.h_loc, lay.din, lay.off_loc, lay.W1, lay.W2, lay.dxd_loc,
+                                      lay.dW1, lay.db1, lay.dW2, lay.db2, lay.ws, hmask=lay.hmask)
+                b.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / len(ev)], device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per_call = {"expert_ffn_bwd": float(t.item())}
+        ep_local = (lay.El, R_in)
         lay.close()
-    return dict(ms=ms, step_ms=[], per_call_ms={}, e2e_ms=e2e_ms, R=R_out, E_act=cfg.E,
-                n_dropped=int(lay.n_dropped.item()), launches=launches, tc_launches=0, clocks=clk.summary(),
+    return dict(ms=ms, step_ms=[], per_call_ms=per_call, ep_local=ep_local, e2e_ms=e2e_ms, R=R_out, E_act=cfg.E,
+                n_dropped=int(lay.n_dropped.item()), launches=launches, tc_launches=tc_launches, clocks=clk.summary(),
                 h2d=2 * T * cfg.D * x.element_size(), d2h=2 * T * cfg.D * x.element_size())
 
 
@@ -499,13 +530,20 @@ def main():
     tokens = cfg.T * world
     value = tokens / (r["ms"] / 1e3)
     e2e_v = tokens / (r["e2e_ms"] / 1e3)
-    # dominant call and its roofline (N > 1: measured on the 1-GPU step only)
+    # dominant call and its roofline (N > 1: rank-local expert backward, max over ranks)
     if not r["per_call_ms"]:
         r["per_call_ms"] = {"expert_ffn_bwd": r["ms"]}
     dom = max(r["per_call_ms"], key=r["per_call_ms"].get)
     dms = r["per_call_ms"][dom]
     fl = call_flops(cfg, dom, r["R"])
     by = call_bytes(cfg, dom, r["R"], r["E_act"])
+    if r.get("ep_local"):
+        El, R_in = r["ep_local"]
+        es = 2 if cfg.dtype == "bf16" else 4
+        Wl = El * cfg.D * cfg.H * es
+        fl = 8.0 * R_in * cfg.D * cfg.H
+        by = (R_in * cfg.D * es * 2 + R_in * cfg.H * es + 2 * Wl + R_in * cfg.D * es + 2 * Wl
+              + El * (cfg.D + cfg.H) * 4 + 3 * R_in * cfg.H * es)
     ai = fl / by if by else 0.0
     ridge = tf_sus * 1e12 / (hbm * 1e9)
     if fl > 0 and ai > ridge:
@@ -538,7 +576,7 @@ def main():
                    else "cuda graph replay"},
         "e2e": {"value": e2e_v, "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
                 "api": "HostPipeline.submit (copies of neighbouring steps overlapped, no L2 flush: weights > L2)"
-                if world == 1 else "step_host (per step)"},
+                if (world == 1 or os.environ.get("DMOE_EP_PIPELINE")) else "step_host (per step)"},
         "gpu_launches": r["launches"] * args.steps,
         "roofline": roof,
         "clocks": r["clocks"],

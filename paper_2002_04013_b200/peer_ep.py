@@ -62,7 +62,9 @@ class PeerEPDMoELayer:
         self.Wg, self.bg = e(D, dM), e(dM, dt=f32)
         self.W1, self.b1 = e(El, H, D), e(El, H, dt=f32)
         self.W2, self.b2 = e(El, D, H), e(El, D, dt=f32)
-        self.dWg, self.dbg = e(D, dM, dt=f32), e(dM, dt=f32)
+        # dW_g and db_g share one buffer: one all-reduce per step (C6)
+        self._dgate = e(D * dM + dM, dt=f32)
+        self.dWg, self.dbg = self._dgate[: D * dM].view(D, dM), self._dgate[D * dM:]
         self.dW1, self.db1 = e(El, H, D), e(El, H, dt=f32)
         self.dW2, self.db2 = e(El, D, H), e(El, D, dt=f32)
         # local (not peer-written) buffers
@@ -74,6 +76,7 @@ class PeerEPDMoELayer:
         self.dout = e(self.rout_cap, D)
         self.y, self.dx, self.dscore = e(T, D), e(T, D), e(T, k, dt=f32)
         self.h_loc, self.out_loc, self.dxd_loc = e(self.rin_cap, H), e(self.rin_cap, D), e(self.rin_cap, D)
+        self.hmask = e((H + 31) // 32, self.rin_cap, dt=i32)  # packed ReLU record (forward -> backward)
         self.epoch = torch.zeros(1, dtype=torch.int64, device=self.dev)
         self.err = torch.zeros(1, dtype=i32, device=self.dev)
         self.base, self.off_loc = e(E, dt=i32), e(El + 1, dt=i32)
@@ -137,7 +140,7 @@ class PeerEPDMoELayer:
         L.dmoe_ep_exchange_counts(ep, self.counts)                                  # C1
         L.dmoe_ep_push_rows(ep, x, self.token_of_row, self.offsets, self.peer["xin"], 1)   # C2 (gather+send)
         L.dmoe_expert_ffn_fwd(self.xin, self.off_loc, self.W1, self.b1, self.W2, self.b2, self.h_loc,
-                              self.out_loc, self.ws)
+                              self.out_loc, self.ws, hmask=self.hmask)
         L.dmoe_ep_return_rows(ep, self.out_loc, self.peer["ret"], 2)                   # C3
         L.dmoe_combine(self.ret, self.row_of_slot[:T], self.w[:T], self.valid[:T], self.y[:T])
         return self.y[:T]
@@ -150,12 +153,11 @@ class PeerEPDMoELayer:
         L.dmoe_combine_bwd(dy, self.ret, self.row_of_slot[:T], self.w[:T], self.dout, self.dscore[:T])
         L.dmoe_ep_push_rows(ep, self.dout, None, self.offsets, self.peer["din"], 3)   # C4
         L.dmoe_expert_ffn_bwd(self.xin, self.h_loc, self.din, self.off_loc, self.W1, self.W2, self.dxd_loc,
-                              self.dW1, self.db1, self.dW2, self.db2, self.ws)
+                              self.dW1, self.db1, self.dW2, self.db2, self.ws, hmask=self.hmask)
         L.dmoe_ep_return_rows(ep, self.dxd_loc, self.peer["dret"], 4)                  # C5
         L.dmoe_gate_bwd(x, self.Wg, self.sel[:T], self.dscore[:T], self.dret, self.row_of_slot[:T], self.g,
                         self.dx[:T], self.dWg, self.dbg, self.ws)
-        dist.all_reduce(self.dWg, group=self.group)                                    # C6
-        dist.all_reduce(self.dbg, group=self.group)
+        dist.all_reduce(self._dgate, group=self.group)                                 # C6 (dW_g, db_g)
         return self.dx[:T]
 
     def step(self, x, dy, alive_bits, responded_bits):
