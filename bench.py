@@ -11,7 +11,8 @@ resident in HBM, timed with CUDA events around a CUDA-graph replay of the step (
 L2 is flushed (untimed 256 MiB write) before every timed step.  `e2e` = the same metric through
 the public API with host buffers: every step uploads its pinned-host x, dy and downloads its y,
 dX inside the timed region (single GPU: HostPipeline, which overlaps those copies with the
-neighbouring steps' compute; N GPUs: the per-step step_host).  `--impl reference` times the float64 CPU oracle (oracle/) on a bounded
+neighbouring steps' compute, per rank under the peer-memory exchange; the NCCL-exchange
+variant: the per-step step_host).  `--impl reference` times the float64 CPU oracle (oracle/) on a bounded
 token sample of the same workload (the only reference this paper has).
 """
 import argparse
@@ -262,8 +263,7 @@ def bench_ep(args, cfg, rank, world, local_rank):
     hdy.copy_(dy)
     hy, hdx = torch.empty_like(hx, pin_memory=True), torch.empty_like(hx, pin_memory=True)
     e2e = []
-    if peer and os.environ.get("DMOE_EP_PIPELINE"):  # per-rank HostPipeline (opt-in: an illegal
-        # address was seen once at 4 GPUs in its eager warm-up; not yet understood)
+    if peer:  # graph-capturable: the same HostPipeline as one GPU, per rank
         from paper_2002_04013_b200.host_pipeline import HostPipeline
         pipe = HostPipeline(lay, T, alive, resp)
         for _ in range(args.warmup):
@@ -576,7 +576,7 @@ def main():
                    else "cuda graph replay"},
         "e2e": {"value": e2e_v, "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
                 "api": "HostPipeline.submit (copies of neighbouring steps overlapped, no L2 flush: weights > L2)"
-                if (world == 1 or os.environ.get("DMOE_EP_PIPELINE")) else "step_host (per step)"},
+                if (world == 1 or os.environ.get("DMOE_EP", "peer") != "nccl") else "step_host (per step)"},
         "gpu_launches": r["launches"] * args.steps,
         "roofline": roof,
         "clocks": r["clocks"],

@@ -110,7 +110,9 @@ k_ep_plan(const int32_t* __restrict__ cnt, int G, int rank, int E, int El, int64
       if (i0 + lane < El) {
         base[e] = ex + mine;
         if (j == rank) {
-          off_loc[i0 + lane] = ex;
+          // clamped to the receive capacity: on overflow (err & 2) the expert GEMMs stay inside
+          // the buffers (the step's results are then invalid and check() reports it)
+          off_loc[i0 + lane] = ex < rin_cap ? ex : (int32_t)rin_cap;
           int32_t d = ex;
           for (int s = 0; s < G; ++s) {
             dst_off[s * El + i0 + lane] = d;
@@ -121,7 +123,7 @@ k_ep_plan(const int32_t* __restrict__ cnt, int G, int rank, int E, int El, int64
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
     if (lane == 0) {
-      if (j == rank) off_loc[El] = carry;
+      if (j == rank) off_loc[El] = carry < rin_cap ? carry : (int32_t)rin_cap;
       if (carry > rin_cap) atomicOr(err, 2);
     }
   }

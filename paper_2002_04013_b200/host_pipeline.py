@@ -33,8 +33,7 @@ class HostPipeline:
         self.ev_up, self.ev_fwd, self.ev_bwd, self.ev_down = mk(), mk(), mk(), mk()
         self.n = 0
         self.graphs = None
-        if use_graphs:
-            self._capture()
+        self.use_graphs = use_graphs
 
     # one half-step body per slot: the layer pass plus the copy into the slot's output staging
     def _fwd(self, s):
@@ -45,7 +44,13 @@ class HostPipeline:
         dx = self.lay.backward(self.dyin[s])
         self.dxout[s].copy_(dx)
 
-    def _capture(self):
+    def _capture(self, hx, hdy):
+        # warm-up and capture on the first batch's data (routing on uninitialised staging could
+        # send every token to a few experts, beyond an expert-parallel receive capacity)
+        for s in (0, 1):
+            self.xin[s].copy_(hx)
+            self.dyin[s].copy_(hdy)
+        torch.cuda.synchronize(self.xin[0].device)
         with torch.cuda.stream(self.compute):
             for s in (0, 1):  # warm-up through the eager path (also builds library side streams)
                 self._fwd(s)
@@ -63,6 +68,8 @@ class HostPipeline:
 
     def submit(self, hx, hdy, hy, hdx):
         """Enqueue one step: pinned host x, dy in; y, dX out (valid after synchronize())."""
+        if self.use_graphs and self.graphs is None:
+            self._capture(hx, hdy)
         i, s = self.n, self.n % 2
         cur = self.compute
         with torch.cuda.stream(self.h2d):
