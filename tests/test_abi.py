@@ -44,3 +44,29 @@ def test_validation_errors_without_gpu():
     assert L._L.dmoe_gate_scores(None, 1, 8, 64, None, None, g, None, None, 0, None) == -1                  # null
     assert b"null pointer" in L._L.dmoe_last_error()
     assert P.dmoe_workspace_bytes(4096, 256, 1024, g, 16, 16384) > 16384 * 1024 * 2
+
+
+def _prototypes():
+    """name -> parameter count of every function prototype in include/dmoe.h."""
+    src = open(os.path.join(ROOT, "include", "dmoe.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    out = {}
+    for m in re.finditer(r"(?:const char\*|int32_t|size_t|dmoe_status|void)\s+(dmoe_\w+)\s*\(([^;{]*?)\)\s*;", src):
+        params = m.group(2).strip()
+        out[m.group(1)] = 0 if params in ("", "void") else params.count(",") + 1
+    return out
+
+
+def test_binding_signatures_match_the_header():
+    """The ctypes argtypes of every bound call have the header's parameter count (ABI drift check)."""
+    from paper_2002_04013_b200 import _lib as L
+    protos = _prototypes()
+    assert "dmoe_expert_ffn_fwd" in protos and "dmoe_expert_ffn_bwd" in protos
+    checked = 0
+    for name, n in protos.items():
+        f = getattr(L._L, name, None)
+        if f is None or f.argtypes is None:
+            continue
+        assert len(f.argtypes) == n, (name, len(f.argtypes), n)
+        checked += 1
+    assert checked >= 10
