@@ -109,11 +109,104 @@ k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
 }
 
 // partial[split][c][col] = sum_{t in split} X[t][c] dG[t][col]; pb[split][col] = sum dG[t][col]
-// Tile: 64 columns of X (c) x 32 columns of dG (col) per CTA, 32 tokens per smem pass, each
-// thread 8 outputs; X and dG rows are read with 16-byte vector loads.
+// Tile: 128 columns of X (c) x 32 columns of dG (col) per CTA, 32 tokens per smem pass; thread
+// (tc, tg) owns c = 4 tc .. 4 tc + 3 and col = 4 tg .. 4 tg + 3 (16 fp32 accumulators, two
+// 16-byte shared loads per 16 FMAs), summing tokens in order.
+constexpr int kDwgC = 128, kDwgCol = 32, kDwgTok = 32;
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn, int32_t D, int dM,
+              int64_t tok_per_split, float* __restrict__ partial, float* __restrict__ pb) {
+  DMOE_PDL_ENTRY();
+  __shared__ __align__(16) float xs[kDwgTok][kDwgC];
+  __shared__ __align__(16) float gs[kDwgTok][kDwgCol];
+  constexpr int V = Vec16<T>::N;
+  const int tc = threadIdx.x & 31, tg = threadIdx.x >> 5;  // 32 x 8
+  const int c0 = blockIdx.x * kDwgC, col0 = blockIdx.y * kDwgCol;
+  const int64_t split = blockIdx.z;
+  const int64_t t_begin = split * tok_per_split;
+  int64_t t_end = t_begin + tok_per_split;
+  if (t_end > Tn) t_end = Tn;
+  float acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+  float bsum[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool xvec = (c0 + kDwgC <= D);
+  const bool gvec = (col0 + kDwgCol <= dM) && (dM % 4 == 0);
+  for (int64_t tb = t_begin; tb < t_end; tb += kDwgTok) {
+    // X tile: 32 tokens x 128 columns (fp32 in smem)
+    for (int i = threadIdx.x; i < kDwgTok * (kDwgC / V); i += 256) {
+      const int r = i / (kDwgC / V), cv = (i % (kDwgC / V)) * V;
+      const int64_t t = tb + r;
+      float f[V];
+      if (t < t_end && xvec) {
+        unpack16(ld_nc_v4(X + t * D + c0 + cv), f, (const T*)nullptr);
+      } else {
+#pragma unroll
+        for (int q = 0; q < V; ++q) f[q] = (t < t_end && c0 + cv + q < D) ? Elem<T>::load(X + t * D + c0 + cv + q) : 0.0f;
+      }
+#pragma unroll
+      for (int q = 0; q < V; ++q) xs[r][cv + q] = f[q];
+    }
+    // dG tile: 32 tokens x 32 columns
+    {
+      const int r = threadIdx.x >> 3, cv = (threadIdx.x & 7) * 4;
+      const int64_t t = tb + r;
+      float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (t < t_end) {
+        if (gvec) g = __ldg(reinterpret_cast<const float4*>(dG + t * dM + col0 + cv));
+        else {
+          g.x = col0 + cv + 0 < dM ? dG[t * dM + col0 + cv + 0] : 0.f;
+          g.y = col0 + cv + 1 < dM ? dG[t * dM + col0 + cv + 1] : 0.f;
+          g.z = col0 + cv + 2 < dM ? dG[t * dM + col0 + cv + 2] : 0.f;
+          g.w = col0 + cv + 3 < dM ? dG[t * dM + col0 + cv + 3] : 0.f;
+        }
+      }
+      *reinterpret_cast<float4*>(&gs[r][cv]) = g;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int r = 0; r < kDwgTok; ++r) {
+      const float4 xa = *reinterpret_cast<const float4*>(&xs[r][tc * 4]);
+      const float4 gb = *reinterpret_cast<const float4*>(&gs[r][tg * 4]);
+      const float xv[4] = {xa.x, xa.y, xa.z, xa.w}, gv[4] = {gb.x, gb.y, gb.z, gb.w};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xv[a], gv[b], acc[a][b]);
+      if (tc == 0) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) bsum[b] += gv[b];
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int c = c0 + tc * 4 + a;
+    if (c >= D) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int col = col0 + tg * 4 + b;
+      if (col < dM) partial[(split * D + c) * dM + col] = acc[a][b];
+    }
+  }
+  if (blockIdx.x == 0 && tc == 0)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int col = col0 + tg * 4 + b;
+      if (col < dM) pb[split * dM + col] = bsum[b];
+    }
+}
+
+// partial[split][c][col] = sum_{t in split} X[t][c] dG[t][col]; pb[split][col] = sum dG[t][col]
+// Small gates (D * dM < 64K, e.g. 256 x 32): 64 columns of X (c) x 32 columns of dG (col) per
+// CTA, 32 tokens per smem pass, each thread 8 outputs: more, shorter CTAs for a latency-bound size.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_dwg_partial_small(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn, int32_t D, int dM,
               int64_t tok_per_split, float* __restrict__ partial, float* __restrict__ pb) {
   DMOE_PDL_ENTRY();
   __shared__ float xs[32][65];
@@ -220,10 +313,11 @@ k_dwg_reduce(const float* __restrict__ partial, const float* __restrict__ pb, in
 }
 
 // split-K over tokens: >= 64 tokens per split, partial sums capped at 8M floats
+// split-K over tokens: one 32-token pass per split where the partial sums (capped at 8M floats)
+// allow, so the CTAs stay short and many
 static int64_t dwg_splits(int64_t T, int32_t D, int dM) {
-  int64_t smax = ((int64_t)8 << 20) / ((int64_t)D * dM);
-  if (smax < 1) smax = 1;
-  int64_t s = ceil_div(T, 32);
+  int64_t s = ceil_div(T, kDwgTok);
+  const int64_t smax = ((int64_t)8 << 20) / ((int64_t)D * dM);
   if (s > smax) s = smax;
   return s < 1 ? 1 : s;
 }
@@ -270,11 +364,20 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
     DMOE_TRY(check_launch("gate_bwd.dx"));
   }
   const int64_t tps = T > 0 ? ceil_div(T, S) : 1;
-  dim3 pg((unsigned)ceil_div(D, 64), (unsigned)ceil_div(dM, 32), (unsigned)S);
-  if (dt == DMOE_BF16)
-    launch_pdl(k_dwg_partial<__nv_bfloat16>, pg, 256, 0, s, (const __nv_bfloat16*)x, dG, T, D, dM, tps, part, pb);
-  else
-    launch_pdl(k_dwg_partial<float>, pg, 256, 0, s, (const float*)x, dG, T, D, dM, tps, part, pb);
+  if ((int64_t)D * dM < 65536) {
+    dim3 pg((unsigned)ceil_div(D, 64), (unsigned)ceil_div(dM, 32), (unsigned)S);
+    if (dt == DMOE_BF16)
+      launch_pdl(k_dwg_partial_small<__nv_bfloat16>, pg, 256, 0, s, (const __nv_bfloat16*)x, dG, T, D, dM, tps,
+                 part, pb);
+    else
+      launch_pdl(k_dwg_partial_small<float>, pg, 256, 0, s, (const float*)x, dG, T, D, dM, tps, part, pb);
+  } else {
+    dim3 pg((unsigned)ceil_div(D, kDwgC), (unsigned)ceil_div(dM, kDwgCol), (unsigned)S);
+    if (dt == DMOE_BF16)
+      launch_pdl(k_dwg_partial<__nv_bfloat16>, pg, 256, 0, s, (const __nv_bfloat16*)x, dG, T, D, dM, tps, part, pb);
+    else
+      launch_pdl(k_dwg_partial<float>, pg, 256, 0, s, (const float*)x, dG, T, D, dM, tps, part, pb);
+  }
   DMOE_TRY(check_launch("gate_bwd.dwg_partial"));
   launch_pdl(k_dwg_reduce, (unsigned)ceil_div((int64_t)D * dM + dM, 32), 256, 0, s, part, pb, S, D, dM, dWg, dbg);
   return check_launch("gate_bwd.dwg_reduce");
