@@ -427,15 +427,15 @@ def oracle_sample_tokens(cfg):
     return ts
 
 
-def time_oracle(cfg, seed, steps=1):
+def time_oracle(cfg, seed, steps=1, Ts=None, sampled=False):
     """The float64 oracle on the first Ts tokens of the step.  Small workloads: the whole layer
     step with every expert (oracle.layer_step).  Large ones (the full expert set cannot be held in
     float64): oracle.layer_step_tokens on the sample, weights regenerated for the experts it
     touches (generation excluded from the timed region)."""
     from gen.inputs import make_inputs  # generator only (no method arithmetic)
     from oracle import oracle as O
-    Ts = oracle_sample_tokens(cfg)
-    full = cfg.E * cfg.D * cfg.H <= (1 << 28)
+    Ts = oracle_sample_tokens(cfg) if Ts is None else Ts
+    full = cfg.E * cfg.D * cfg.H <= (1 << 28) and not sampled
     times = []
     if full:
         inp = make_inputs(cfg, seed=seed, T=Ts)
@@ -481,11 +481,25 @@ def time_oracle(cfg, seed, steps=1):
 
 
 def bench_reference(args, cfg):
+    """The oracle as it stands, timed for exactly --steps K steps after --warmup W, each step a
+    token sample of the workload sized so that the whole run takes about DMOE_REF_BUDGET_S
+    (default 150) seconds: the sample is the default one when that fits, else the per-token cost
+    of a 64-token probe step sets it (sampled path: only the touched experts' weights)."""
     os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))
-    steps = max(1, min(args.steps, 3))
-    for _ in range(min(args.warmup, 1)):
-        time_oracle(cfg, args.seed, 1)
-    Ts, times, cores, sample = time_oracle(cfg, args.seed, steps)
+    steps, warm = args.steps, args.warmup
+    budget = float(os.environ.get("DMOE_REF_BUDGET_S", "150"))
+    per_step = budget / (steps + warm)
+    Ts0 = oracle_sample_tokens(cfg)
+    _, t0, _, _ = time_oracle(cfg, args.seed, 1)
+    Ts, sampled = Ts0, False
+    if t0[0] > per_step:
+        probe = min(64, cfg.T)
+        _, tp, _, _ = time_oracle(cfg, args.seed, 2, Ts=probe, sampled=True)
+        Ts = int(max(16, min(Ts0, probe * per_step / max(min(tp), 1e-6))))
+        sampled = True
+    for _ in range(warm):
+        time_oracle(cfg, args.seed, 1, Ts=Ts, sampled=sampled)
+    Ts, times, cores, sample = time_oracle(cfg, args.seed, steps, Ts=Ts, sampled=sampled)
     sec = sum(times) / len(times)
     v = Ts / sec
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus,
