@@ -402,6 +402,17 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
     if (only & 8) DMOE_TRY(segk_gemm(g6, dt, s));
     return DMOE_OK;
   }
+  // Both weight-gradient GEMMs in one persistent launch (one ramp / drain) once dh exists, on a
+  // forked library stream next to the dxd GEMM.  DMOE_SEGK_SPLIT=1: the two-launch form below.
+  static const bool segk_split = getenv("DMOE_SEGK_SPLIT") != nullptr;
+  if (!segk_split && fused && tc_segk2_supported(g5, g6)) {
+    DMOE_TRY(rows_gemm(g3, dt, s));
+    cudaStream_t side2 = fork_stream(s);
+    DMOE_TRY(tc_gemm_segk2(g5, g6, side2 ? side2 : s));
+    DMOE_TRY(rows_gemm(g4, dt, s));
+    if (side2) DMOE_TRY(join_stream(s, side2));
+    return DMOE_OK;
+  }
   cudaStream_t side = fork_stream(s);
   if (side) {
     // SM split between the chains: the weight-gradient GEMMs are bound by HBM writes (dW), the

@@ -55,10 +55,12 @@ dmoe_status tile_plan(const int32_t* offsets, int64_t E, int bm, int32_t* plan, 
 dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s);
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s);
 bool tc_rows_supported(const GemmRows& g);
-int tc_rows_tile(const GemmRows& g);
-int tc_plan_in_kernel_max();
-bool tc_rows_mmajor();  // the M-major row engine (not the swap-AB experiment) runs the row GEMMs  // experts up to which the M-major engine plans row tiles itself  // token rows per tile of the row engine (plan granularity)
+int tc_rows_tile(const GemmRows& g);       // token rows per tile of the row engine (plan granularity)
+int tc_plan_in_kernel_max();               // experts up to which the M-major engine plans row tiles itself
+bool tc_rows_mmajor();                     // the M-major row engine (not the swap-AB experiment) runs them
 bool tc_segk_supported(const GemmSegK& g);
 bool tc_segk_colsum_supported(const GemmSegK& g);  // the SEGK engine also writes colsum
+bool tc_segk2_supported(const GemmSegK& a, const GemmSegK& b);
+dmoe_status tc_gemm_segk2(const GemmSegK& a, const GemmSegK& b, cudaStream_t s);  // both in one launch
 
 }  // namespace dmoe

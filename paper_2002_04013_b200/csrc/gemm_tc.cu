@@ -207,6 +207,10 @@ struct TcParams {
   uint32_t* hmask;           // packed ReLU mask [N/32][hmask_ld] (bit c of word (w,row) = h[row, 32w+c] > 0):
                              // written by EPI_BIAS_RELU, read instead of aux by EPI_RELU_MASK
   int64_t hmask_ld;
+  // SEGK: an optional second problem over the same segments (offsets), tiles after the first's
+  // (its A / B / C tensor maps are the kernel's tmA2 / tmB2 / tmC2)
+  int Mdim2, N2;          // Mdim2 == 0: one problem
+  float* colsum2;
   void* C;
   int E, N, K, Mdim;
   int64_t rows_single;
@@ -261,7 +265,8 @@ __device__ __forceinline__ bool bf16_pos(uint32_t b) { return b != 0 && !(b & 0x
 template <int BN, bool SEGK, bool B_MN, int EPI>
 __global__ void __launch_bounds__(TcCfg<BN, SEGK>::THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-          const __grid_constant__ CUtensorMap tmC, const TcParams p) {
+          const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
+          const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC2, const TcParams p) {
   using Cfg = TcCfg<BN, SEGK>;
   // Before waiting for the previous kernel (programmatic dependent launch: this CTA may already
   // sit on an SM the previous grid freed while its last CTAs finish): pull the expert weights of
@@ -355,8 +360,12 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   // ---- tile space (identical walk in every role)
   const int NT = (p.N + BN - 1) / BN;
   const int MT = SEGK ? p.Mdim / TC_BM : 0;
+  const bool two = SEGK && p.Mdim2 > 0;
+  const int NT2 = two ? (p.N2 + BN - 1) / BN : 1;
+  const int MT2 = two ? p.Mdim2 / TC_BM : 1;
+  const int total0 = SEGK ? p.E * MT * NT : 0;
   int total;
-  if (SEGK) total = p.E * MT * NT;
+  if (SEGK) total = total0 + (two ? p.E * MT2 * NT2 : 0);
   else if (p.offsets) total = plan[p.E] * NT;
   else total = (int)((p.rows_single + TC_BM - 1) / TC_BM) * NT;
 
@@ -402,12 +411,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   // expert's segment bounds per thread (tiles of one expert are consecutive in the walk).
   int c_e = -1;
   int64_t c_r0 = 0, c_r1 = 0;
-  auto decode = [&](int tile, int& e, int64_t& row0, int64_t& row_end, int& m0, int& n0, int& nkb) {
+  auto decode = [&](int tile, int& e, int64_t& row0, int64_t& row_end, int& m0, int& n0, int& nkb) -> int {
+    int prob = 0;
     if (SEGK) {
-      e = tile / (MT * NT);
-      const int rem = tile - e * MT * NT;
-      m0 = (rem / NT) * TC_BM;
-      n0 = (rem % NT) * BN;
+      int mt = MT, nt = NT;
+      if (tile >= total0) { prob = 1; tile -= total0; mt = MT2; nt = NT2; }
+      e = tile / (mt * nt);
+      const int rem = tile - e * mt * nt;
+      m0 = (rem / nt) * TC_BM;
+      n0 = (rem % nt) * BN;
       if (e != c_e) {
         c_e = e;
         c_r0 = offs[e];
@@ -433,6 +445,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
       nkb = p.K / TC_BK;
     }
+    return prob;
   };
 
   if (warp == 0) {
@@ -484,7 +497,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
         int e, m0, n0, nkb;
         int64_t row0, row_end;
-        decode(tile, e, row0, row_end, m0, n0, nkb);
+        const int prob = decode(tile, e, row0, row_end, m0, n0, nkb);
+        (void)prob;
         for (int kb = 0; kb < nkb; ++kb) {
           WT_T0(t_e);
           mbar_wait(&empty[stage], phase ^ 1);
@@ -497,11 +511,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           if (SEGK) {
             const int kr = (int)(row0 + kb * TC_BK);
-            tma_load_2d_h(sa, &tmA, &full[stage], m0, kr, pol_keep);
-            tma_load_2d_h(sa + 8192, &tmA, &full[stage], m0 + 64, kr, pol_keep);
+            const CUtensorMap* mA = prob ? &tmA2 : &tmA;
+            const CUtensorMap* mB = prob ? &tmB2 : &tmB;
+            tma_load_2d_h(sa, mA, &full[stage], m0, kr, pol_keep);
+            tma_load_2d_h(sa + 8192, mA, &full[stage], m0 + 64, kr, pol_keep);
 #pragma unroll
             for (int c = 0; c < BN / 64; ++c)
-              tma_load_2d_h(sb + c * 8192, &tmB, &full[stage], n0 + 64 * c, kr, pol_keep);
+              tma_load_2d_h(sb + c * 8192, mB, &full[stage], n0 + 64 * c, kr, pol_keep);
           } else {
             tma_load_2d_h(sa, &tmA, &full[stage], kb * TC_BK, (int)row0, pol_keep);
             if (B_MN) {
@@ -603,8 +619,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int tile = t_begin; tile < t_end; tile += t_step) {
       int e, m0, n0, nkb;
       int64_t row0, row_end;
-      decode(tile, e, row0, row_end, m0, n0, nkb);
-      const bool sums = p.colsum && n0 == 0;
+      const int prob = decode(tile, e, row0, row_end, m0, n0, nkb);
+      float* const colsum = prob ? p.colsum2 : p.colsum;
+      const int mdim = prob ? p.Mdim2 : p.Mdim;
+      const bool sums = colsum && n0 == 0;
       float cs[4] = {0.f, 0.f, 0.f, 0.f};
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
@@ -649,7 +667,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
       if (sums)
-        *reinterpret_cast<float4*>(p.colsum + (int64_t)e * p.Mdim + m0 + 4 * lane) = make_float4(cs[0], cs[1], cs[2], cs[3]);
+        *reinterpret_cast<float4*>(colsum + (int64_t)e * mdim + m0 + 4 * lane) = make_float4(cs[0], cs[1], cs[2], cs[3]);
     }
   } else if (warp >= 4) {
     // ======================= epilogue =======================
@@ -672,7 +690,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
       int e, m0, n0, nkb;
       int64_t row0, row_end;
-      decode(tile, e, row0, row_end, m0, n0, nkb);
+      const int prob = decode(tile, e, row0, row_end, m0, n0, nkb);
+      const CUtensorMap* mC = prob ? &tmC2 : &tmC;
+      const int mdim = prob ? p.Mdim2 : p.Mdim;
       const bool has_acc = !(SEGK && nkb == 0);
       // stage this tile's bias slice (double-buffered across tiles; one named barrier)
       constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
@@ -835,8 +855,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           if (lane == 0 && !(p.dbg & 1)) {
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
-                    &tmC),
-                "r"(smem_u32(stg)), "r"(n0 + cs), "r"((int)((int64_t)e * p.Mdim + qrow0)), "l"(pol_out)
+                    mC),
+                "r"(smem_u32(stg)), "r"(n0 + cs), "r"((int)((int64_t)e * mdim + qrow0)), "l"(pol_out)
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
@@ -1284,8 +1304,9 @@ static int debug_flags_segk() {
 }
 
 template <int BN, bool SEGK, bool B_MN, int EPI>
-static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcParams& p,
-                          int64_t max_tiles, cudaStream_t s) {
+static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                               const CUtensorMap& a2, const CUtensorMap& b2, const CUtensorMap& c2,
+                               const TcParams& p, int64_t max_tiles, cudaStream_t s) {
   auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
   const int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
   const int smem = TcCfg<BN, SEGK>::smem_for(table_len);
@@ -1302,9 +1323,14 @@ static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUte
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
   pp.stages = TcCfg<BN, SEGK>::stages_for(table_len);
   pp.table_len = table_len;
-  launch_pdl(kern, (unsigned)grid, TcCfg<BN, SEGK>::THREADS, smem, s, a, b, c, pp);
+  launch_pdl(kern, (unsigned)grid, TcCfg<BN, SEGK>::THREADS, smem, s, a, b, c, a2, b2, c2, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
+}
+template <int BN, bool SEGK, bool B_MN, int EPI>
+static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcParams& p,
+                          int64_t max_tiles, cudaStream_t s) {
+  return launch_maps<BN, SEGK, B_MN, EPI>(a, b, c, a, b, c, p, max_tiles, s);
 }
 
 template <int BN>
@@ -1452,6 +1478,33 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   const int64_t tiles = (int64_t)g.E * (g.Mdim / TC_BM) * (g.N / BN);
   if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
   return launch<128, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
+}
+
+// two weight-gradient GEMMs over the same segments in one persistent launch (the expert
+// backward's dW2 and dW1): one ramp / drain instead of two
+bool tc_segk2_supported(const GemmSegK& a, const GemmSegK& b) {
+  return tc_segk_supported(a) && tc_segk_supported(b) && a.offsets == b.offsets && a.E == b.E &&
+         pick_bn(a.N, true) == 256 && pick_bn(b.N, true) == 256 && a.max_ctas == b.max_ctas;
+}
+dmoe_status tc_gemm_segk2(const GemmSegK& g, const GemmSegK& h, cudaStream_t s) {
+  CUtensorMap m[6];
+  const GemmSegK* gs[2] = {&g, &h};
+  for (int i = 0; i < 2; ++i) {
+    const GemmSegK& x = *gs[i];
+    const uint64_t rc = (uint64_t)(x.R_cap > 0 ? x.R_cap : 1);
+    uint64_t adims[2] = {(uint64_t)x.Mdim, rc};
+    uint64_t bdims[2] = {(uint64_t)x.N, rc};
+    uint64_t cdims[2] = {(uint64_t)x.N, (uint64_t)x.E * x.Mdim};
+    DMOE_TRY(make_map(&m[3 * i + 0], x.A, 2, adims, 64));
+    DMOE_TRY(make_map(&m[3 * i + 1], x.B, 2, bdims, 64));
+    DMOE_TRY(make_map(&m[3 * i + 2], x.C, 2, cdims, 32));
+  }
+  TcParams p{};
+  p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim; p.colsum = g.colsum;
+  p.N2 = h.N; p.Mdim2 = h.Mdim; p.colsum2 = h.colsum;
+  p.max_ctas = g.max_ctas;
+  const int64_t tiles = (int64_t)g.E * ((g.Mdim / TC_BM) * (g.N / 256) + (h.Mdim / TC_BM) * (h.N / 256));
+  return launch_maps<256, true, true, EPI_PLAIN>(m[0], m[1], m[2], m[3], m[4], m[5], p, tiles, s);
 }
 
 }  // namespace dmoe
