@@ -36,8 +36,8 @@
  * Conventions for every call:
  *   - All pointers are caller-owned DEVICE memory unless marked (host); row-major,
  *     contiguous; 16-byte aligned (the caller's cudaMalloc / torch allocations are).
- *   - Work is enqueued on `stream` (dmoe_expert_ffn_bwd forks two of its GEMMs onto a library
- *     stream with events and joins back before returning; CUDA-graph capturable); no call
+ *   - Work is enqueued on `stream` (dmoe_expert_ffn_bwd forks its weight-gradient GEMMs onto a
+ *     library stream with events and joins back before returning; CUDA-graph capturable); no call
  *     synchronises the host or allocates device memory.
  *     Scratch comes from the caller's workspace `ws` of at least
  *     dmoe_workspace_bytes(...) bytes (re-usable across calls on one stream).

@@ -49,8 +49,9 @@ def _run(counts, D, H, dtype, seed=0, cap_extra=37):
     P.dmoe_expert_ffn_bwd(xd, h, dout, off, W1, W2, dxd, dW1, db1, dW2, db2, ws)
     torch.cuda.synchronize()
     c1 = P.dmoe_launch_counters()
-    if dtype == "bf16":   # the bf16 path must run on the tensor cores (6 tcgen05 GEMMs, no SIMT GEMM)
-        assert c1[1] - c0[1] == 6 and c1[2] == c0[2], (c0, c1)
+    if dtype == "bf16":   # the bf16 path must run on the tensor cores (h, out, dh, dxd and the two
+        # weight-gradient GEMMs: 6 tcgen05 launches, 5 when dW2 and dW1 share one), no SIMT GEMM
+        assert c1[1] - c0[1] in (5, 6) and c1[2] == c0[2], (c0, c1)
     a_ref, out_ref = O.ffn_fwd(xd64[:R], offsets, W164, np64(b1), W264, np64(b2))
     dx_ref, dW1_ref, db1_ref, dW2_ref, db2_ref = O.ffn_bwd(xd64[:R], a_ref, dout64[:R], offsets, W164, W264)
     tol = TOL[dtype]
