@@ -406,6 +406,11 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
   // forked library stream next to the dxd GEMM.  DMOE_SEGK_SPLIT=1: the two-launch form below.
   static const bool segk_split = getenv("DMOE_SEGK_SPLIT") != nullptr;
   if (!segk_split && fused && tc_segk2_supported(g5, g6)) {
+    const int seg_ctas = bwd_segk_ctas();  // optional SM split with the dxd GEMM (experiments)
+    if (seg_ctas > 0) {
+      g5.max_ctas = g6.max_ctas = seg_ctas;
+      g4.max_ctas = num_sms_api() - seg_ctas;
+    }
     DMOE_TRY(rows_gemm(g3, dt, s));
     cudaStream_t side2 = fork_stream(s);
     DMOE_TRY(tc_gemm_segk2(g5, g6, side2 ? side2 : s));
