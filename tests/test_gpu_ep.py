@@ -52,7 +52,18 @@ def _worker(rank, G, port, q, kind="nccl", graph=False):
     dy = to_torch(inp["dev_dY"], "bf16", (cfg.T, D))[rank * T:(rank + 1) * T].contiguous()
     alive = torch.from_numpy(inp["alive_bits"].view(np.int32)).cuda()
     resp = torch.from_numpy(inp["responded_bits"].view(np.int32)).cuda()
-    if graph:
+    if graph == "pipe":
+        # the host-buffer pipeline (per-slot CUDA graphs, overlapped copies), three steps
+        from paper_2002_04013_b200.host_pipeline import HostPipeline
+        hx, hdy = x.cpu().pin_memory(), dy.cpu().pin_memory()
+        hy, hdx = torch.empty_like(hx).pin_memory(), torch.empty_like(hx).pin_memory()
+        pipe = HostPipeline(lay, T, alive, resp)
+        for _ in range(3):
+            pipe.submit(hx, hdy, hy, hdx)
+        pipe.synchronize()
+        y, dx = hy.cuda(), hdx.cuda()
+        del pipe
+    elif graph:
         # capture one step in a CUDA graph (peer exchange needs no host sync), replay it twice
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
@@ -86,7 +97,8 @@ def _worker(rank, G, port, q, kind="nccl", graph=False):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("G,kind,graph", [(2, "nccl", False), (2, "peer", False), (2, "peer", True)])
+@pytest.mark.parametrize("G,kind,graph", [(2, "nccl", False), (2, "peer", False), (2, "peer", True),
+                                          (2, "peer", "pipe")])
 def test_ep_equals_single_gpu(G, kind, graph):
     if torch.cuda.device_count() < G:
         pytest.skip(f"needs {G} GPUs")
