@@ -239,24 +239,18 @@ template <int BN, bool SEGK = false> struct TcCfg {
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;       // 16 KB
   static constexpr int B_BYTES = BN * TC_BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
+  // fixed smem without the per-expert tables (those are sized at launch: 2 x table_len ints)
   // weight-gradient tiles (~1 K block each): a 3rd accumulator (when TMEM has room) lets the
-  // MMA run two tiles ahead.  Their stage ring is latency bound (TMA -> fix-up -> MMA -> release
-  // per 1-K-block tile), so the SEGK layout is trimmed to fit a 4th 48 KB stage at BN = 256:
-  // one 4 KB store box per warp, no bias slice, one table (offsets), no alignment slack (the
-  // dynamic smem is declared 1024-aligned; the kernel traps if it is not).
+  // MMA run two tiles ahead, and each warp double-buffers its 4 KB store box so the TMA
+  // engine's read of one box overlaps the staging of the next
   static constexpr int NACC = (SEGK && BN <= 128) ? 3 : 2;
-  static constexpr int STG_WARP = SEGK ? 4 * 1024 : TC_STAGE_WARP;
-  static constexpr int BIAS_BYTES = SEGK ? 0 : BN * 4 * 2;
-  static constexpr int TABLES = SEGK ? 1 : 2;
-  static constexpr int SLACK = SEGK ? 0 : 1024;
-  static constexpr int FIXED = SLACK + 512 /*barriers*/ + EPI_WARPS * STG_WARP + BIAS_BYTES;
-  static int stages_for(int table_len, int budget) {
-    const int st = (budget - FIXED - TABLES * table_len * 4) / STAGE_BYTES;
+  static constexpr int STG_WARP = SEGK ? 8 * 1024 : TC_STAGE_WARP;
+  static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + EPI_WARPS * STG_WARP + BN * 4 * 2;
+  static int stages_for(int table_len) {
+    const int st = (TC_SMEM_MAX - FIXED - 2 * table_len * 4) / STAGE_BYTES;
     return st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
   }
-  static int smem_for(int table_len, int budget) {
-    return stages_for(table_len, budget) * STAGE_BYTES + FIXED + TABLES * table_len * 4;
-  }
+  static int smem_for(int table_len) { return stages_for(table_len) * STAGE_BYTES + FIXED + 2 * table_len * 4; }
   static constexpr int pow2cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
   static constexpr int TMEM_COLS = pow2cols(NACC * BN);                 // NACC accumulators
   static_assert(TMEM_COLS <= 512, "TMEM");
@@ -301,20 +295,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
   constexpr int OUT_ES = OUT_F32 ? 4 : 2;
   constexpr int SUB = 128 / OUT_ES;  // columns per staged sub-tile (128 bytes per row)
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  if (SEGK && smem != smem_raw) __trap();  // the SEGK budget has no alignment slack
-  // [stage ring][store staging (1 KB aligned: 128B-swizzled TMA stores)][barriers][bias][tables]
-  uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES;
-  uint64_t* full = (uint64_t*)(stage_base + Cfg::EPI_WARPS * Cfg::STG_WARP);
+  uint64_t* full = (uint64_t*)(smem + S * Cfg::STAGE_BYTES);
   uint64_t* empty = full + TC_MAX_STAGES;
   uint64_t* tfull = empty + TC_MAX_STAGES;
   uint64_t* tempty = tfull + 4;
   uint64_t* ready = tempty + 4;  // SEGK: stage fixed up (tail rows zeroed) for the MMA
   uint32_t* tmem_slot = (uint32_t*)(ready + TC_MAX_STAGES);
-  float* bias_s = (float*)((uint8_t*)full + 512);                               // [2][BN] (ROWS)
-  int32_t* off_s = (int32_t*)((uint8_t*)bias_s + Cfg::BIAS_BYTES);              // [table_len]
-  int32_t* plan_s = off_s + p.table_len;                                        // [table_len] (ROWS)
+  uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 1024;   // 1 KB aligned (128B-swizzled TMA stores)
+  float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * Cfg::STG_WARP);  // [2][BN]
+  int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [table_len]
+  int32_t* plan_s = off_s + p.table_len;                                    // [table_len]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -688,6 +680,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const uint64_t pol_out = (p.dbg & 32) ? l2_policy_last() : l2_policy_first();  // dW: written once
     uint8_t* const stg_warp = stage_base + ew * Cfg::STG_WARP;
     uint8_t* stg = stg_warp;
+    int stg_buf = 0;  // SEGK: which of the warp's two 4 KB store boxes
     int acc = 0;
     uint32_t acc_phase = 0;
     int bias_buf = 0;
@@ -779,10 +772,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           __syncwarp();
         }
         if (SEGK && !OUT_F32) {
-          // the warp's single box: its previous store must have been read out
-          stg = stg_warp;
+          // this box was last stored two boxes ago: at most the newest store may still be reading
+          stg = stg_warp + stg_buf * 4096;
           WT_T0(t_st);
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           __syncwarp();
           WT_ADD(w_st, t_st);
         }
@@ -856,7 +849,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
         if (SEGK && !OUT_F32) {
-          // full 32 x 64 box: one bulk tensor store
+          // full 32 x 64 box: one bulk tensor store (double-buffered box, see above)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0 && !(p.dbg & 1)) {
@@ -867,6 +860,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
+          stg_buf ^= 1;
           __syncwarp();
           continue;
         }
@@ -1314,20 +1308,8 @@ static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const
                                const CUtensorMap& a2, const CUtensorMap& b2, const CUtensorMap& c2,
                                const TcParams& p, int64_t max_tiles, cudaStream_t s) {
   auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
-  static int budget = 0;  // opt-in dynamic smem of this kernel: device maximum less its static smem
-  if (!budget) {
-    int dev = 0, optin = 0;
-    cudaFuncAttributes fa{};
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncGetAttributes(&fa, kern);
-    budget = optin - (int)fa.sharedSizeBytes;
-    if (budget <= 0 || budget > TC_SMEM_MAX + 2048) budget = TC_SMEM_MAX;
-  }
-  int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
-  if (SEGK && TcCfg<BN, SEGK>::stages_for(table_len, budget) < TcCfg<BN, SEGK>::stages_for(0, budget))
-    table_len = 0;  // SEGK: ring depth first (offsets then come from global, cached per expert)
-  const int smem = TcCfg<BN, SEGK>::smem_for(table_len, budget);
+  const int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
+  const int smem = TcCfg<BN, SEGK>::smem_for(table_len);
   static int attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1339,7 +1321,7 @@ static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const
   TcParams pp = p;
   pp.dbg = debug_flags() | (SEGK ? debug_flags_segk() : 0);
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  pp.stages = TcCfg<BN, SEGK>::stages_for(table_len, budget);
+  pp.stages = TcCfg<BN, SEGK>::stages_for(table_len);
   pp.table_len = table_len;
   launch_pdl(kern, (unsigned)grid, TcCfg<BN, SEGK>::THREADS, smem, s, a, b, c, a2, b2, c2, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
