@@ -67,7 +67,7 @@ __device__ __forceinline__ void insert_sorted(uint64_t (&top)[WMAX], uint64_t ke
   }
 }
 
-constexpr int kBeamWarps = 8;
+constexpr int kBeamWarps = 4;
 
 // smem per warp: G row (dM floats) + beam (WMAX x {p, s})
 constexpr int kSmemPAWords = 2048;  // prefix bitmaps up to 64K bits live in smem
