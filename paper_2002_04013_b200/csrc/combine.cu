@@ -7,7 +7,7 @@
 
 namespace dmoe {
 
-constexpr int kCombWarps = 8;
+constexpr int kCombWarps = 4;
 
 template <typename T, int kMaxK>
 __global__ void __launch_bounds__(kCombWarps * 32)

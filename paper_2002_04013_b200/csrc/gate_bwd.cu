@@ -39,7 +39,7 @@ dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt
   return check_launch("transpose");
 }
 
-constexpr int kGbWarps = 8;
+constexpr int kGbWarps = 4;
 
 template <typename T, int kGbMaxK>
 __global__ void __launch_bounds__(kGbWarps * 32)
