@@ -2,6 +2,10 @@
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+# `make EXPERIMENTS=1`: a library with the A/B switches and probes (env DMOE_*); never the product
+ifdef EXPERIMENTS
+NVFLAGS   += -DDMOE_EXPERIMENTS
+endif
 CFLAGS    := -O2 -fPIC -fopenmp -Wall -std=c11
 
 PKG       := paper_2002_04013_b200
@@ -19,10 +23,16 @@ gen/libgen_device.so: gen/gen_device.cu gen/counter_gen.h
 oracle/liboracle.so: oracle/dmoe_oracle.c
 	gcc $(CFLAGS) -shared -o $@ oracle/dmoe_oracle.c -lm
 
-$(PKG)/libdmoe.so: $(CSRC) $(CHDR)
-	$(NVCC) $(NVFLAGS) -Iinclude -shared -o $@ $(CSRC) -lcuda
+COBJ      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CSRC))
+
+build/%.o: $(PKG)/csrc/%.cu $(CHDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -Iinclude -c -o $@ $<
+
+$(PKG)/libdmoe.so: $(COBJ)
+	$(NVCC) $(ARCH) -shared -o $@ $(COBJ) -lcuda
 
 clean:
-	rm -f gen/*.so oracle/*.so $(PKG)/*.so
+	rm -f gen/*.so oracle/*.so $(PKG)/*.so build/*.o
 
 .PHONY: all clean

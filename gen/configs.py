@@ -26,6 +26,7 @@ class Config:
     dead_frac: float = 0.0   # P(expert dead before selection) -> `alive`
     beam: int = 0            # beam width B (0 -> k, the paper's Alg. 1)
     exact_grid: bool = False
+    pool: int = 0            # parameter slots of the tied-weight pool (0 -> E, no tying; X20)
 
     @property
     def E(self):
@@ -34,6 +35,15 @@ class Config:
     @property
     def dM(self):
         return self.d * self.M
+
+    @property
+    def P(self):
+        """Expert parameter slots: expert e computes with slot e // tie (reading X20)."""
+        return self.pool if self.pool else self.E
+
+    @property
+    def tie(self):
+        return self.E // self.P
 
     @property
     def B(self):

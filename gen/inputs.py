@@ -29,7 +29,7 @@ def make_inputs(cfg, seed=0, T=None, experts=None):
     out["X"] = param("X", gen.X, T * D).reshape(T, D)
     out["Wg"] = param("Wg", gen.WG, D * dM).reshape(D, dM)
     out["bg"] = param("bg", gen.BG, dM, force_f32=True)
-    ex = range(E) if experts is None else experts
+    ex = range(cfg.P) if experts is None else experts   # parameter slots (== experts unless tied)
     W1, b1, W2, b2 = [], [], [], []
     dev = {k: [] for k in ("W1", "b1", "W2", "b2")}
     for e in ex:

@@ -112,6 +112,17 @@ dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_
                            int32_t* sel, float* sel_score, void* ws, size_t ws_bytes,
                            dmoe_stream_t stream);
 
+/* S1+S2+S3 fused — gate scores (Eq. 2) and SelectExperts (Alg. 1 + FilterAlive) in one call:
+ * exactly dmoe_gate_scores followed by dmoe_beam_topk (same definitions, same results bit for
+ * bit), but on the bf16 tensor-core path (d*M <= 128 and a multiple of 16, beam <= 8, prefix
+ * bitmaps <= 64K bits) the search runs in the gate GEMM's epilogue on each 128-token tile, so
+ * G never round-trips through HBM.  G [T, d*M] fp32 is optional (NULL: not written; the
+ * two-launch form then keeps it in `ws`).  sel / sel_score as dmoe_beam_topk. */
+dmoe_status dmoe_gate_topk(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg,
+                           const float* bg, dmoe_grid g, const uint32_t* alive_bits, float* G,
+                           int32_t* sel, float* sel_score, void* ws, size_t ws_bytes,
+                           dmoe_stream_t stream);
+
 /* S4+S5 — renormalised Eq. 3 weights and per-expert dispatch:
  *   ok[t,s]  = sel[t,s] >= 0 && responded(sel[t,s])                  (X8)
  *   w[t,s]   = exp(sel_score[t,s] - m_t) / sum_{ok r} exp(sel_score[t,r] - m_t), 0 if !ok
@@ -168,7 +179,10 @@ dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row
  * dxd [R_cap, D] dt (out); dW1 [E_local, H, D] dt; dW2 [E_local, D, H] dt; db1 [E_local, H]
  * and db2 [E_local, D] fp32 (out).  hmask: optional (NULL), the packed ReLU record the forward
  * call wrote for these rows (same xd/offsets/h); when given, the dh GEMM reads its mask bits
- * instead of h (the same decisions, 1/16 of the bytes). */
+ * instead of h (the same decisions, 1/16 of the bytes).  Contract: hmask is either NULL or the
+ * buffer the last dmoe_expert_ffn_fwd call wrote for exactly these rows (same xd, offsets,
+ * E_local, R_cap, D, H, dtype, with a non-NULL hmask); the library cannot check that the bits
+ * are current, so a stale record gives a wrong dh mask without an error. */
 dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
                                 const int32_t* offsets, int32_t E_local, int64_t R_cap,
                                 int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
@@ -185,6 +199,16 @@ dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, con
                           dmoe_grid g, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
                           size_t ws_bytes, dmoe_stream_t stream);
 
+/* Tied-weight pool (reading X20): experts [s*group, (s+1)*group) share parameter
+ * slot s, so the FFN calls run with E_local = E / group slots over the slot segments
+ *   seg[s] = offsets[s * group],  s = 0 .. E/group        (seg [E/group + 1] int32, out)
+ * Rows of tied experts are contiguous in the expert-major dispatch order, so a slot's rows are
+ * one segment and its weight gradient (dW of the FFN backward) is the sum over its experts'
+ * rows: the gradient of the tied parameters.  group = 1 copies offsets.
+ * Fails with DMOE_ERR_SHAPE unless E % group == 0. */
+dmoe_status dmoe_segment_offsets(const int32_t* offsets, int32_t E, int32_t group, int32_t* seg,
+                                 dmoe_stream_t stream);
+
 /* S11 — expert-parallel exchange, receive side ("send inputs to those workers
  * and collect outputs"; §3.3 the runtime batches requests per expert).  With experts sharded
  * over G ranks by contiguous flat index, a rank receives its experts' rows source-rank-major;
@@ -192,6 +216,9 @@ dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, con
  *   offsets [E_local+1] (out): expert-major segment starts (expert e: source 0's rows, then
  *     source 1's, ... — the single-GPU token order when sources hold increasing token blocks);
  *   src_of_dst [R_cap] (out): source-major row index of every expert-major row.
+ * Capacity: if sum(recv_counts) > R_cap the segments are clamped to R_cap (offsets[E_local] =
+ * R_cap < sum(recv_counts) reports the overflow; rows past R_cap are never placed), so no kernel
+ * downstream can run past the caller's buffers.
  * ws >= 8 * G * E_local bytes.  Fails with DMOE_ERR_SHAPE on G < 1 or E_local < 1. */
 dmoe_status dmoe_exchange_layout(const int32_t* recv_counts, int32_t G, int32_t E_local, int64_t R_cap,
                                  int32_t* offsets, int32_t* src_of_dst, void* ws, size_t ws_bytes,

@@ -181,14 +181,20 @@ def gate_bwd(X, Wg, sel, dscore, dx_rows, row_of_slot, d, M):
     return dX, dWg, dbg
 
 
-def layer_step(X, Wg, bg, W1, b1, W2, b2, dY, alive, responded, d, M, k, B, sel_override=None):
+def layer_step(X, Wg, bg, W1, b1, W2, b2, dY, alive, responded, d, M, k, B, sel_override=None, tie=1):
     """One DMoE layer step, forward + backward, composed from S1..S10 in the paper's order.
 
-    W1/b1/W2/b2 cover all E experts.  `sel_override` (optional [T,k] int32) replaces the
+    W1/b1/W2/b2 cover all E experts, or E / tie parameter slots when `tie` > 1: the declared
+    tied-weight pool of the stress workload (reading X20), where expert e computes with
+    slot e // tie.  Rows are dispatched per expert exactly as without tying (S5); the FFN then runs
+    each slot over the rows of its tied experts, which are contiguous in the expert-major order,
+    so the slot segments are offsets[::tie] and dW of a slot is the gradient of the tied weights
+    (the sum over its experts' rows).  `sel_override` (optional [T,k] int32) replaces the
     oracle's own routing downstream of S3 (stage-wise parity with forced routing).
     Returns a dict of every intermediate and gradient.
     """
     E = M ** d
+    assert E % tie == 0 and W1.shape[0] == E // tie
     G = gate_scores(X, Wg, bg)
     sel, sc, gap = select_experts(G, d, M, k, B, alive)
     if sel_override is not None:
@@ -196,11 +202,12 @@ def layer_step(X, Wg, bg, W1, b1, W2, b2, dY, alive, responded, d, M, k, B, sel_
         sc = np.where(sel >= 0, _scores_of(G, sel, d, M), -np.inf)
     w, ok, valid, nd = weights(sel, sc, responded)
     counts, offsets, ros, tor = dispatch(sel, ok, E)
+    seg = np.ascontiguousarray(offsets[::tie])
     x_rows = np.asarray(X, np.float64)[tor]
-    a, out = ffn_fwd(x_rows, offsets, W1, b1, W2, b2)
+    a, out = ffn_fwd(x_rows, seg, W1, b1, W2, b2)
     y = combine(out, ros, w)
     g, dscore = combine_bwd(dY, out, ros, w)
-    dx_rows, dW1, db1, dW2, db2 = ffn_bwd(x_rows, a, g, offsets, W1, W2)
+    dx_rows, dW1, db1, dW2, db2 = ffn_bwd(x_rows, a, g, seg, W1, W2)
     dX, dWg, dbg = gate_bwd(X, Wg, sel, dscore, dx_rows, ros, d, M)
     return dict(G=G, sel=sel, sel_score=sc, gap=gap, w=w, ok=ok, valid=valid, n_dropped=nd,
                 counts=counts, offsets=offsets, row_of_slot=ros, token_of_row=tor, a=a, out=out,

@@ -46,6 +46,7 @@ _SIGS = {
     "dmoe_launch_counters": ([_P, _I32], ctypes.c_int32),
     "dmoe_workspace_bytes": ([_I64, _I32, _I32, dmoe_grid, _I32, _I64], ctypes.c_size_t),
     "dmoe_gate_scores": ([_P, _I32, _I64, _I32, _P, _P, dmoe_grid, _P, _P, _SZ, _P], ctypes.c_int),
+    "dmoe_gate_topk": ([_P, _I32, _I64, _I32, _P, _P, dmoe_grid, _P, _P, _P, _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_beam_topk": ([_P, _I64, dmoe_grid, _P, _P, _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_dispatch": ([_P, _I32, _I64, _I32, dmoe_grid, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
                        _SZ, _P], ctypes.c_int),
@@ -57,6 +58,7 @@ _SIGS = {
                              _SZ, _P], ctypes.c_int),
     "dmoe_gate_bwd": ([_P, _P, _P, _P, _P, _P, _I64, _I32, dmoe_grid, _I32, _P, _P, _P, _P, _SZ, _P],
                       ctypes.c_int),
+    "dmoe_segment_offsets": ([_P, _I32, _I32, _P, _P], ctypes.c_int),
     "dmoe_exchange_layout": ([_P, _I32, _I32, _I64, _P, _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_ep_begin": ([_P, _P], ctypes.c_int),
     "dmoe_ep_exchange_counts": ([_P, _P, _P], ctypes.c_int),
@@ -123,6 +125,14 @@ def dmoe_gate_scores(x, Wg, bg, g, G, ws):
                                                    ws.numel() * ws.element_size(), _stream()))
 
 
+def dmoe_gate_topk(x, Wg, bg, g, alive_bits, G, sel, sel_score, ws):
+    """G may be None (not written)."""
+    T, D = x.shape
+    _check("dmoe_gate_topk", _L.dmoe_gate_topk(_p(x), _dt(x), T, D, _p(Wg), _p(bg), g, _p(alive_bits), _p(G),
+                                               _p(sel), _p(sel_score), _p(ws), ws.numel() * ws.element_size(),
+                                               _stream()))
+
+
 def dmoe_beam_topk(G, g, alive_bits, sel, sel_score, ws):
     _check("dmoe_beam_topk", _L.dmoe_beam_topk(_p(G), G.shape[0], g, _p(alive_bits), _p(sel), _p(sel_score),
                                                _p(ws), ws.numel() * ws.element_size(), _stream()))
@@ -169,6 +179,11 @@ def dmoe_gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, g, dx, dWg, dbg, ws):
     _check("dmoe_gate_bwd", _L.dmoe_gate_bwd(
         _p(x), _p(Wg), _p(sel), _p(dscore), _p(dxd), _p(row_of_slot), T, D, g, _dt(x), _p(dx), _p(dWg),
         _p(dbg), _p(ws), ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_segment_offsets(offsets, group, seg):
+    E = offsets.shape[0] - 1
+    _check("dmoe_segment_offsets", _L.dmoe_segment_offsets(_p(offsets), E, group, _p(seg), _stream()))
 
 
 def dmoe_exchange_layout(recv_counts, G, E_local, offsets, src_of_dst, ws):

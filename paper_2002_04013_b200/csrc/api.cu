@@ -6,6 +6,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -65,6 +69,7 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
                      int k, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
                      size_t ws_bytes, cudaStream_t s);
 
+dmoe_status segment_offsets(const int32_t* offsets, int64_t E, int group, int32_t* seg, cudaStream_t s);
 dmoe_status exchange_layout(const int32_t* counts, int G, int El, int32_t* offsets,
                             int32_t* src_of_dst, int64_t R_cap, void* ws, size_t ws_bytes, cudaStream_t s);
 dmoe_status permute_rows(const void* src, const int32_t* idx, const int32_t* n_rows, int32_t D,
@@ -123,7 +128,7 @@ constexpr int kPlanBM_SIMT = 64;
 // The packed ReLU record is produced by the forward's h GEMM and consumed by the backward's dh
 // GEMM only when both run on the M-major tcgen05 engine; both calls evaluate this same test.
 static bool hmask_path(dmoe_dtype dt, int32_t D, int32_t H, int32_t E, int64_t R_cap) {
-  static const bool off = getenv("DMOE_NO_HMASK") != nullptr;  // A/B experiments
+  static const bool off = dmoe_env("DMOE_NO_HMASK") != nullptr;  // A/B experiments
   if (off || dt != DMOE_BF16 || H % 32 != 0 || !tc_rows_mmajor()) return false;
   GemmRows f{}, b{};
   f.E = b.E = E; f.N = b.N = H; f.K = b.K = D; f.rows_cap = b.rows_cap = R_cap;
@@ -147,7 +152,7 @@ static int num_sms_api() {
 static int bwd_segk_ctas() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("DMOE_BWD_SEGK_CTAS");
+    const char* e = dmoe_env("DMOE_BWD_SEGK_CTAS");
     v = e ? atoi(e) : 0;
     if (v >= num_sms_api()) v = 0;
   }
@@ -155,43 +160,49 @@ static int bwd_segk_ctas() {
 }
 
 // ------------------------------------------------------- library side stream (fork / join)
-// One non-blocking stream + event pool per device, created on first use (setup, not hot path).
-// fork_stream(s): the side stream waits for everything enqueued on s so far; join_stream: s
-// waits for the side stream.  Event record / wait are captured into CUDA graphs as edges.
-// DMOE_SERIAL=1 disables the fork (everything on the caller's stream).
+// One non-blocking side stream + 3 events per (device, caller stream), created on first use
+// (setup, not hot path) and kept for the process: two host threads calling on different
+// streams never share a side stream or an event, so one call can never wait on another call's
+// fork point.  fork_stream(s): the side stream waits for everything enqueued on s so far;
+// join_stream: s waits for the side stream.  Event record / wait are captured into CUDA graphs
+// as edges.  DMOE_SERIAL=1 (experiment builds) disables the fork.
 struct SideStream {
   cudaStream_t st = nullptr;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
 };
-static SideStream g_side[64];
+static std::mutex g_side_mu;
+static std::map<std::pair<int, cudaStream_t>, SideStream> g_side;
 
-static cudaStream_t fork_stream(cudaStream_t s) {
-  static const bool serial = getenv("DMOE_SERIAL") != nullptr;
-  if (serial) return nullptr;
+static SideStream* side_for(cudaStream_t s) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  SideStream& ss = g_side[dev];
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStream& ss = g_side[{dev, s}];
   if (!ss.st) {
     if (cudaStreamCreateWithFlags(&ss.st, cudaStreamNonBlocking) != cudaSuccess) { ss.st = nullptr; return nullptr; }
     for (auto& e : ss.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
   }
-  if (cudaEventRecord(ss.ev[0], s) != cudaSuccess || cudaStreamWaitEvent(ss.st, ss.ev[0], 0) != cudaSuccess)
-    return nullptr;
-  return ss.st;
+  return &ss;
 }
-static dmoe_status fork_point(cudaStream_t s, cudaStream_t side) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaEvent_t e = g_side[dev].ev[1];
-  if (cudaEventRecord(e, s) != cudaSuccess || cudaStreamWaitEvent(side, e, 0) != cudaSuccess)
+
+static cudaStream_t fork_stream(cudaStream_t s, SideStream** out) {
+  static const bool serial = dmoe_env("DMOE_SERIAL") != nullptr;
+  *out = nullptr;
+  if (serial) return nullptr;
+  SideStream* ss = side_for(s);
+  if (!ss) return nullptr;
+  if (cudaEventRecord(ss->ev[0], s) != cudaSuccess || cudaStreamWaitEvent(ss->st, ss->ev[0], 0) != cudaSuccess)
+    return nullptr;
+  *out = ss;
+  return ss->st;
+}
+static dmoe_status fork_point(cudaStream_t s, SideStream* ss) {
+  if (cudaEventRecord(ss->ev[1], s) != cudaSuccess || cudaStreamWaitEvent(ss->st, ss->ev[1], 0) != cudaSuccess)
     return set_error(DMOE_ERR_CUDA, "fork_point: %s", cudaGetErrorString(cudaGetLastError()));
   return DMOE_OK;
 }
-static dmoe_status join_stream(cudaStream_t s, cudaStream_t side) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  cudaEvent_t e = g_side[dev].ev[2];
-  if (cudaEventRecord(e, side) != cudaSuccess || cudaStreamWaitEvent(s, e, 0) != cudaSuccess)
+static dmoe_status join_stream(cudaStream_t s, SideStream* ss) {
+  if (cudaEventRecord(ss->ev[2], ss->st) != cudaSuccess || cudaStreamWaitEvent(s, ss->ev[2], 0) != cudaSuccess)
     return set_error(DMOE_ERR_CUDA, "join_stream: %s", cudaGetErrorString(cudaGetLastError()));
   return DMOE_OK;
 }
@@ -229,7 +240,9 @@ size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_
                             int64_t R_cap) {
   int64_t E = 1;
   for (int i = 0; i < g.d; ++i) E *= g.M;
-  size_t beam = prefix_words(g.d, g.M) * 4 + (size_t)g.d * g.M * D * 2 + 256;
+  // gate / beam (dmoe_gate_topk's unfused form keeps G in the workspace when the caller passes none)
+  size_t beam = align_up(prefix_words(g.d, g.M) * 4, 256) + align_up((size_t)g.d * g.M * D * 2, 256) +
+                (size_t)T * g.d * g.M * 4 + 1024;
   size_t disp = dispatch_ws_bytes(T, E);
   size_t ffn = 2 * align_up((size_t)(E_local + 1) * 4, 256) + align_up((size_t)R_cap * H * 4, 256) + 1024;
   size_t gate = gate_bwd_ws_bytes(T, D, g.d * g.M);
@@ -269,6 +282,42 @@ dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D,
   r.b_mn = true;
   r.max_tiles = ceil_div(T, kPlanBM_SIMT);
   return simt_gemm_rows(r, dt, s);
+}
+
+dmoe_status dmoe_gate_topk(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg, const float* bg,
+                           dmoe_grid g, const uint32_t* alive_bits, float* G, int32_t* sel, float* sel_score,
+                           void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  int64_t E = 0;
+  DMOE_TRY(check_grid(&g, &E));
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
+  NN(alive_bits); NN(ws); NN(Wg); NN(bg);
+  if (T == 0) return DMOE_OK;
+  NN(x); NN(sel); NN(sel_score);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int dM = g.d * g.M;
+  if (dt == DMOE_BF16 && tc_gate_topk_supported(dM, D, g.d, g.M, g.beam)) {
+    // one launch: tcgen05 gate GEMM, Alg. 1 on each 128-token tile in the epilogue
+    DMOE_REQUIRE(ws_bytes >= (size_t)dM * D * 2, DMOE_ERR_ARG, "gate_topk: workspace too small");
+    DMOE_TRY(transpose(Wg, D, dM, dt, ws, s));
+    GemmRows r{};
+    r.A = x; r.B = ws; r.C = G; r.bias = bg; r.aux = nullptr;
+    r.offsets = nullptr; r.plan = nullptr;
+    r.E = 1; r.N = dM; r.K = D; r.rows_single = T; r.rows_cap = T;
+    r.b_mn = false; r.epi = EPI_GATE_TOPK;
+    r.topk.sel = sel; r.topk.sel_score = sel_score; r.topk.alive = alive_bits;
+    r.topk.d = g.d; r.topk.M = g.M; r.topk.k = g.k; r.topk.B = g.beam;
+    r.max_tiles = ceil_div(T, tc_rows_tile(r));
+    return tc_gemm_rows(r, s);
+  }
+  // two launches: gate scores into G (the caller's, else the workspace), then the search
+  Carver cv(ws, ws_bytes);
+  uint32_t* pa = cv.take<uint32_t>(prefix_words(g.d, g.M));
+  void* wgt = cv.take<char>((size_t)dM * D * 2);
+  float* Gw = G ? G : cv.take<float>((size_t)T * dM);
+  DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "gate_topk: workspace too small (%zu < %zu)", ws_bytes, cv.used);
+  DMOE_TRY(dmoe_gate_scores(x, dt, T, D, Wg, bg, g, Gw, wgt, (size_t)dM * D * 2, stream));
+  return beam_topk(Gw, T, g, alive_bits, sel, sel_score, pa, s);
 }
 
 dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive_bits,
@@ -386,25 +435,15 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
   // tensor-core path: an extra ones-MMA inside the same GEMMs)
   GemmSegK g5{dout, h, dW2, offsets, E_local, D, H, R_cap, db2};
   GemmSegK g6{dh, xd, dW1, offsets, E_local, H, D, R_cap, db1};
-  static const bool no_fuse = getenv("DMOE_NO_COLSUM_FUSE") != nullptr;  // A/B experiments
+  static const bool no_fuse = dmoe_env("DMOE_NO_COLSUM_FUSE") != nullptr;  // A/B experiments
   const bool fused = !no_fuse && dt == DMOE_BF16 && tc_segk_colsum_supported(g5) && tc_segk_colsum_supported(g6);
   if (!fused) g5.colsum = g6.colsum = nullptr;
   // Dependency graph: dh (g3) -> dxd (g4); dh -> dW1 (g6); dW2 (g5) independent.  g5 and g6 run
   // on a library stream forked/joined with events (graph-capturable), so each persistent GEMM's
   // tail is filled by the other chain's tiles instead of idling SMs.
-  // DMOE_BWD_ONLY=<mask> (timing experiments only; results are then incomplete): run only the
-  // GEMMs whose bit is set: 1 dh, 2 dxd, 4 dW2, 8 dW1
-  static const int only = getenv("DMOE_BWD_ONLY") ? atoi(getenv("DMOE_BWD_ONLY")) : 15;
-  if (only != 15) {
-    if (only & 1) DMOE_TRY(rows_gemm(g3, dt, s));
-    if (only & 2) DMOE_TRY(rows_gemm(g4, dt, s));
-    if (only & 4) DMOE_TRY(segk_gemm(g5, dt, s));
-    if (only & 8) DMOE_TRY(segk_gemm(g6, dt, s));
-    return DMOE_OK;
-  }
   // Both weight-gradient GEMMs in one persistent launch (one ramp / drain) once dh exists, on a
   // forked library stream next to the dxd GEMM.  DMOE_SEGK_SPLIT=1: the two-launch form below.
-  static const bool segk_split = getenv("DMOE_SEGK_SPLIT") != nullptr;
+  static const bool segk_split = dmoe_env("DMOE_SEGK_SPLIT") != nullptr;
   if (!segk_split && fused && tc_segk2_supported(g5, g6)) {
     const int seg_ctas = bwd_segk_ctas();  // optional SM split with the dxd GEMM (experiments)
     if (seg_ctas > 0) {
@@ -412,13 +451,15 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
       g4.max_ctas = num_sms_api() - seg_ctas;
     }
     DMOE_TRY(rows_gemm(g3, dt, s));
-    cudaStream_t side2 = fork_stream(s);
+    SideStream* ss2 = nullptr;
+    cudaStream_t side2 = fork_stream(s, &ss2);
     DMOE_TRY(tc_gemm_segk2(g5, g6, side2 ? side2 : s));
     DMOE_TRY(rows_gemm(g4, dt, s));
-    if (side2) DMOE_TRY(join_stream(s, side2));
+    if (side2) DMOE_TRY(join_stream(s, ss2));
     return DMOE_OK;
   }
-  cudaStream_t side = fork_stream(s);
+  SideStream* ss = nullptr;
+  cudaStream_t side = fork_stream(s, &ss);
   if (side) {
     // SM split between the chains: the weight-gradient GEMMs are bound by HBM writes (dW), the
     // row GEMMs by HBM reads (W); run side by side on disjoint SMs the two mix into copy-like
@@ -430,12 +471,12 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
   }
   DMOE_TRY(rows_gemm(g3, dt, s));
   if (side) {
-    DMOE_TRY(fork_point(s, side));  // side waits for dh
+    DMOE_TRY(fork_point(s, ss));  // side waits for dh
     DMOE_TRY(segk_gemm(g6, dt, side));
   }
   DMOE_TRY(rows_gemm(g4, dt, s));
   if (side) {
-    DMOE_TRY(join_stream(s, side));
+    DMOE_TRY(join_stream(s, ss));
   } else {
     DMOE_TRY(segk_gemm(g5, dt, s));
     DMOE_TRY(segk_gemm(g6, dt, s));
@@ -457,6 +498,13 @@ dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, con
   if (T > 0) { NN(x); NN(sel); NN(dscore); NN(row_of_slot); NN(dx); }
   return gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, T, D, g.d, g.M, g.k, dt, dx, dWg, dbg, ws,
                   ws_bytes, (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_segment_offsets(const int32_t* offsets, int32_t E, int32_t group, int32_t* seg,
+                                 dmoe_stream_t stream) {
+  DMOE_REQUIRE(E >= 1 && group >= 1 && E % group == 0, DMOE_ERR_SHAPE, "segment_offsets: E=%d group=%d", E, group);
+  NN(offsets); NN(seg);
+  return segment_offsets(offsets, E, group, seg, (cudaStream_t)stream);
 }
 
 dmoe_status dmoe_exchange_layout(const int32_t* recv_counts, int32_t G, int32_t E_local, int64_t R_cap,

@@ -1,0 +1,149 @@
+// beam.cuh — S3 SelectExperts (Alg. 1) for ONE token by ONE thread.
+//
+// Alg. 1 per token: beam := [()]; for every grid dimension i: expand each prefix p of the beam
+// by j in [0, M) with score s_p + g_i(x, j) (Eq. 2's additive score), drop the candidates whose
+// prefix has no alive expert (FilterAlive; reading X5), keep the best B
+// (k at the last level) under the total order of reading X4 (score descending, then flat index
+// ascending; -0.0 == +0.0).
+//
+// B200 design: a thread owns a token.  Its row of gate scores sits in shared memory (staged by
+// coalesced loads, or written there by the gate GEMM's epilogue), the beam and the level's
+// running top-W list live in registers as 64-bit keys  (order-preserving score bits << 32) |
+// (2^32 - 1 - flat prefix index)  so "larger key" == "higher score, then lower index", and each
+// candidate costs one fp32 add and one fp32 compare against the list's current W-th score; only
+// the rare candidates that reach the list pay the unrolled compare-select insertion.  No warp
+// shuffles, no divergence-bound merge rounds: the search is a short ALU loop per token, so a
+// 128-token tile of the gate GEMM finishes it in its own epilogue.
+#pragma once
+#include <math.h>
+#include <stdint.h>
+
+namespace dmoe {
+
+__device__ __forceinline__ uint32_t beam_ord(float s) {
+  uint32_t u = __float_as_uint(s == 0.0f ? 0.0f : s);  // canonicalise -0.0 (reading X4)
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float beam_unord(uint32_t o) {
+  uint32_t u = (o & 0x80000000u) ? (o & 0x7fffffffu) : ~o;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ uint64_t beam_key(float s, uint32_t p) {
+  return ((uint64_t)beam_ord(s) << 32) | (uint64_t)(0xffffffffu - p);
+}
+
+// keep `top` sorted descending; the smallest entry falls off
+template <int WMAX>
+__device__ __forceinline__ void beam_insert(uint64_t (&top)[WMAX], uint64_t key) {
+#pragma unroll
+  for (int i = WMAX - 1; i >= 0; --i) {
+    const uint64_t prev = (i > 0) ? top[i - 1] : ~0ull;
+    if (key > top[i]) top[i] = (key > prev) ? prev : key;
+  }
+}
+
+template <int WMAX>
+__device__ __forceinline__ uint64_t beam_at(const uint64_t (&top)[WMAX], int i) {
+  uint64_t v = 0;
+#pragma unroll
+  for (int q = 0; q < WMAX; ++q)
+    if (q == i) v = top[q];
+  return v;
+}
+
+// One token.  grow: its d*M gate scores G[t, i*M + j] (any memory, stride `gstride` floats
+// between consecutive j — 1 for a contiguous row).  PA: prefix-alive bitmaps, level i at word
+// offset pa_off[i] (level d-1 = the alive mask); read only when MASKED.  Writes sel[0..k) and
+// score[0..k) (flat expert index / Eq. 2 score sum, best first; -1 / -inf pad, reading X6).
+template <int WMAX, bool MASKED>
+__device__ __forceinline__ void beam_search_row(const float* grow, int gstride, int d, int M, int k, int B,
+                                                const uint32_t* PA, const int (&pa_off)[4], int32_t* sel,
+                                                float* score) {
+  uint64_t beam[WMAX];
+#pragma unroll
+  for (int q = 0; q < WMAX; ++q) beam[q] = 0ull;
+  beam[0] = beam_key(0.0f, 0u);  // the empty prefix, score 0
+  int nb = 1;
+  for (int i = 0; i < d; ++i) {
+    const int W = (i < d - 1) ? B : k;
+    uint64_t top[WMAX];
+#pragma unroll
+    for (int q = 0; q < WMAX; ++q) top[q] = 0ull;
+    uint64_t thr = 0ull;        // key of the W-th entry (0: fewer than W so far)
+    float thr_s = -INFINITY;    // its score: a candidate below it cannot enter the list
+    const float* gi = grow + (int64_t)i * M * gstride;
+    const uint32_t* pa = nullptr;
+    if (MASKED) pa = PA + (i == 0 ? pa_off[0] : i == 1 ? pa_off[1] : i == 2 ? pa_off[2] : pa_off[3]);
+#pragma unroll
+    for (int b = 0; b < WMAX; ++b) {
+      if (b < nb) {
+        const uint32_t p0 = (0xffffffffu - (uint32_t)beam[b]) * (uint32_t)M;
+        const float sp = beam_unord((uint32_t)(beam[b] >> 32));
+        for (int j = 0; j < M; ++j) {
+          const float s = sp + gi[j * gstride];
+          if (!(s >= thr_s)) continue;  // also drops NaN scores (undefined, reading X4)
+          const uint32_t p = p0 + (uint32_t)j;
+          if (MASKED && !((pa[p >> 5] >> (p & 31)) & 1u)) continue;  // FilterAlive
+          const uint64_t key = beam_key(s, p);
+          if (key > thr) {
+            beam_insert<WMAX>(top, key);
+            thr = beam_at<WMAX>(top, W - 1);
+            if (thr) thr_s = beam_unord((uint32_t)(thr >> 32));
+          }
+        }
+      }
+    }
+    nb = 0;
+#pragma unroll
+    for (int q = 0; q < WMAX; ++q) {
+      const bool keep = q < W && top[q] != 0ull;
+      beam[q] = keep ? top[q] : 0ull;
+      nb += keep ? 1 : 0;
+    }
+  }
+  for (int s = 0; s < k; ++s) {
+    const uint64_t v = beam_at<WMAX>(beam, s);
+    sel[s] = s < nb ? (int32_t)(0xffffffffu - (uint32_t)v) : -1;
+    score[s] = s < nb ? beam_unord((uint32_t)(v >> 32)) : -INFINITY;
+  }
+}
+
+// any alive expert in [e0, e0 + span)
+__device__ __forceinline__ bool span_any(const uint32_t* __restrict__ alive, int64_t e0, int64_t span) {
+  const int64_t e1 = e0 + span;
+  for (int64_t e = e0; e < e1;) {
+    const uint32_t word = alive[e >> 5];
+    const int sh = (int)(e & 31);
+    int64_t take = 32 - sh;
+    if (take > e1 - e) take = e1 - e;
+    const uint32_t mask = (take == 32) ? 0xffffffffu : (((1u << take) - 1u) << sh);
+    if (word & mask) return true;
+    e += take;
+  }
+  return false;
+}
+
+// prefix bitmaps into `PA` (smem or global) by the whole CTA, one thread per prefix and a
+// warp ballot per 32-bit word; the last level is the alive mask itself.  Same definition as
+// k_prefix_alive (reading X5).
+__device__ __forceinline__ void prefix_alive_block(const uint32_t* __restrict__ alive, int d, int M, int64_t E, uint32_t* PA) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t wo = 0, n = M;
+  for (int i = 0; i < d; ++i) {
+    const int64_t words = (n + 31) / 32, span = E / n;
+    if (i == d - 1) {
+      for (int64_t w = threadIdx.x; w < words; w += blockDim.x) PA[wo + w] = alive[w];
+    } else {
+      for (int64_t w = warp; w < words; w += nw) {
+        const int64_t p = w * 32 + lane;
+        const bool any = p < n && span_any(alive, p * span, span);
+        const uint32_t bits = __ballot_sync(0xffffffffu, any);
+        if (lane == 0) PA[wo + w] = bits;
+      }
+    }
+    wo += words;
+    n *= M;
+  }
+}
+
+}  // namespace dmoe

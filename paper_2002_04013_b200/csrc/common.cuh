@@ -15,6 +15,18 @@ dmoe_status check_launch(const char* what);
 extern int64_t g_counters[4];
 int num_sms();
 
+// Experiment switches (A/B timing runs, probes, stores / MMAs skipped) exist only in builds
+// compiled with -DDMOE_EXPERIMENTS (`make EXPERIMENTS=1`).  In the product library every switch
+// reads as unset and every probe branch is compiled out, so no environment variable can change
+// what the library computes.
+#ifdef DMOE_EXPERIMENTS
+#define dmoe_env(name) getenv(name)
+#define DMOE_DBG(p) ((p).dbg)
+#else
+#define dmoe_env(name) ((const char*)nullptr)
+#define DMOE_DBG(p) 0
+#endif
+
 #define DMOE_REQUIRE(cond, st, ...)                          \
   do {                                                       \
     if (!(cond)) return ::dmoe::set_error((st), __VA_ARGS__); \

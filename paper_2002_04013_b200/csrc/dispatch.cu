@@ -301,3 +301,21 @@ dmoe_status tile_plan(const int32_t* offsets, int64_t E, int bm, int32_t* plan, 
 }
 
 }  // namespace dmoe
+
+namespace dmoe {
+// seg[s] = offsets[s * group], s = 0..E/group (reading X20: the tied-weight pool's slot segments)
+__global__ void k_segment_offsets(const int32_t* __restrict__ offsets, int64_t n, int group,
+                                  int32_t* __restrict__ seg) {
+  DMOE_PDL_ENTRY();
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s <= n; s += (int64_t)gridDim.x * blockDim.x)
+    seg[s] = offsets[s * group];
+}
+
+dmoe_status segment_offsets(const int32_t* offsets, int64_t E, int group, int32_t* seg, cudaStream_t s) {
+  const int64_t n = E / group;
+  int64_t blocks = ceil_div(n + 1, 256);
+  if (blocks > 1024) blocks = 1024;
+  launch_pdl(k_segment_offsets, (unsigned)blocks, 256, 0, s, offsets, n, group, seg);
+  return check_launch("segment_offsets");
+}
+}  // namespace dmoe

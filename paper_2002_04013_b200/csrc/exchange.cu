@@ -43,7 +43,7 @@ __device__ int32_t xblock_excl_scan(int32_t v, int32_t* sh, int32_t* total) {
 // offsets[e] (expert-major segment starts, El+1) and dst_off[s][e] = offsets[e] +
 // sum_{s'<s} counts[s'][e]
 __global__ void __launch_bounds__(1024)
-k_exchange_tables(const int32_t* __restrict__ counts, int G, int El, int32_t* __restrict__ offsets,
+k_exchange_tables(const int32_t* __restrict__ counts, int G, int El, int64_t R_cap, int32_t* __restrict__ offsets,
                   int32_t* __restrict__ src_off, int32_t* __restrict__ dst_off) {
   DMOE_PDL_ENTRY();
   __shared__ int32_t sh[32];
@@ -64,16 +64,17 @@ k_exchange_tables(const int32_t* __restrict__ counts, int G, int El, int32_t* __
     const int32_t ex = xblock_excl_scan(v, sh, &tot);
     if (e < El) {
       int32_t d = carry + ex;
-      offsets[e] = d;
+      // capacity clamp: segments never extend past R_cap (offsets[El] < sum(counts) reports it)
+      offsets[e] = (int64_t)d < R_cap ? d : (int32_t)R_cap;
       for (int s = 0; s < G; ++s) { dst_off[s * El + e] = d; d += counts[s * El + e]; }
     }
     carry += tot;
   }
-  if (threadIdx.x == 0) offsets[El] = carry;
+  if (threadIdx.x == 0) offsets[El] = (int64_t)carry < R_cap ? carry : (int32_t)R_cap;
 }
 
-// src_of_dst[r] for every expert-major row r: expert by binary search over offsets, source by
-// a scan over the <= G blocks of that expert
+// src_of_dst[r] for every expert-major row r < offsets[El] (<= R_cap): expert by binary search
+// over offsets, source by a scan over the <= G blocks of that expert
 __global__ void k_exchange_index(const int32_t* __restrict__ counts, int G, int El,
                                  const int32_t* __restrict__ offsets, const int32_t* __restrict__ src_off,
                                  const int32_t* __restrict__ dst_off, int32_t* __restrict__ src_of_dst) {
@@ -114,7 +115,7 @@ dmoe_status exchange_layout(const int32_t* counts, int G, int El, int32_t* offse
   int32_t* src_off = cv.take<int32_t>((size_t)G * El);
   int32_t* dst_off = cv.take<int32_t>((size_t)G * El);
   DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "exchange_layout: workspace too small");
-  launch_pdl(k_exchange_tables, 1, 1024, 0, s, counts, G, El, offsets, src_off, dst_off);
+  launch_pdl(k_exchange_tables, 1, 1024, 0, s, counts, G, El, R_cap, offsets, src_off, dst_off);
   DMOE_TRY(check_launch("exchange_tables"));
   int64_t blocks = ceil_div(R_cap > 0 ? R_cap : 1, 256);
   const int64_t cap = (int64_t)num_sms() * 8;

@@ -23,6 +23,7 @@
 #include <cuda.h>
 #include <stdlib.h>
 
+#include "beam.cuh"
 #include "gemm.cuh"
 
 namespace dmoe {
@@ -187,15 +188,15 @@ __device__ unsigned long long g_tc_probe[8][TC_PROBE_ROLES][32];
 // 5 mma issue+commit, 6 mma loop, 7 epi tfull-wait (warp 4), 8 epi store-read wait, 9 epi loop,
 // 10 mma tiles, 11 CTAs, 12 mma issue without the commits
 __device__ unsigned long long g_tc_wait[8][16];
-#define WT_T0(v) const long long v = (p.dbg & 64) ? clock64() : 0
-#define WT_ADD(acc_, v) do { if (p.dbg & 64) acc_ += clock64() - v; } while (0)
+#define WT_T0(v) const long long v = (DMOE_DBG(p) & 64) ? clock64() : 0
+#define WT_ADD(acc_, v) do { if (DMOE_DBG(p) & 64) acc_ += clock64() - v; } while (0)
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
 #define PROBE(role, i) \
-  do { if ((p.dbg & 8) && blockIdx.x == 0 && (i) < 32) g_tc_probe[p.slot][role][i] = gtimer(); } while (0)
+  do { if ((DMOE_DBG(p) & 8) && blockIdx.x == 0 && (i) < 32) g_tc_probe[p.slot][role][i] = gtimer(); } while (0)
 
 // ------------------------------------------------------------------------- kernel
 struct TcParams {
@@ -217,17 +218,23 @@ struct TcParams {
   int max_ctas;   // grid cap (0: all SMs)
   int stages;     // M-major engine: smem ring depth (runtime, <= TC_MAX_STAGES)
   int table_len;  // M-major engine: per-expert smem table entries (0: tables stay in global)
+  GateTopk topk;   // EPI_GATE_TOPK: Alg. 1 in the epilogue
+  int topk_bytes;  // EPI_GATE_TOPK: smem of the G tile [128][N+1] fp32 + prefix-alive bitmaps
+  int pa_words;    // EPI_GATE_TOPK: words of the prefix-alive bitmaps (<= kTopkPAWords)
   int slot;  // probe slot (launch ordinal % 8)
-  int dbg;  // experiment switches (env DMOE_TC_DEBUG): 1 skip stores, 2 skip TMEM loads, 4 skip MMAs
+  int dbg;  // experiment switches (DMOE_EXPERIMENTS builds only, env DMOE_TC_DEBUG): 1 skip stores,
+            // 2 skip TMEM loads, 4 skip MMAs, 8 timeline probe, 16 L2 prefetch cursor, 32 no L2 hints,
+            // 64 phase cycle counters, 128 no first-tile weight prefetch
 };
 
 constexpr int TC_SMEM_MAX = 227 * 1024 - 2048;   // opt-in maximum less the kernels' static smem (<= 2 KB)
 constexpr int TC_STAGE_ROW = 144;              // staging row pitch: 128 B of data + 16 B pad
 constexpr int TC_STAGE_WARP = 5 * 1024;           // one warp's 32-row staging tile (1 KB aligned)
 constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan live in smem
-constexpr int TC_TABLE_LEN = TC_TABLE_E + 4;      // entries per table (16-byte multiple)
 
 constexpr int TC_MAX_STAGES = 8;
+constexpr int kTopkPAWords = 2048;  // fused gate + top-k: prefix bitmaps up to 64K bits (in smem)
+constexpr int kTopkWMAX = 8;        // fused gate + top-k: beam widths up to 8
 
 template <int BN, bool SEGK = false> struct TcCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
@@ -246,11 +253,13 @@ template <int BN, bool SEGK = false> struct TcCfg {
   static constexpr int NACC = (SEGK && BN <= 128) ? 3 : 2;
   static constexpr int STG_WARP = SEGK ? 8 * 1024 : TC_STAGE_WARP;
   static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + EPI_WARPS * STG_WARP + BN * 4 * 2;
-  static int stages_for(int table_len) {
-    const int st = (TC_SMEM_MAX - FIXED - 2 * table_len * 4) / STAGE_BYTES;
+  static int stages_for(int table_len, int extra = 0) {
+    const int st = (TC_SMEM_MAX - FIXED - 2 * table_len * 4 - extra) / STAGE_BYTES;
     return st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
   }
-  static int smem_for(int table_len) { return stages_for(table_len) * STAGE_BYTES + FIXED + 2 * table_len * 4; }
+  static int smem_for(int table_len, int extra = 0) {
+    return stages_for(table_len, extra) * STAGE_BYTES + FIXED + 2 * table_len * 4 + extra;
+  }
   static constexpr int pow2cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
   static constexpr int TMEM_COLS = pow2cols(NACC * BN);                 // NACC accumulators
   static_assert(TMEM_COLS <= 512, "TMEM");
@@ -274,7 +283,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   // prefetch never changes what the loads after the wait see, so this needs no ordering.  The
   // tile's expert is guessed as its row tile (one 128-row tile per expert); a wrong guess only
   // warms another expert's weights.
-  if (!SEGK && p.offsets && (p.dbg & 128) == 0 && threadIdx.x == 0) {
+  if (!SEGK && p.offsets && (DMOE_DBG(p) & 128) == 0 && threadIdx.x == 0) {
     const int nt = (p.N + BN - 1) / BN;
     const int rt = (int)blockIdx.x / nt, n0 = ((int)blockIdx.x % nt) * BN;
     const int e = rt < p.E ? rt : p.E - 1;
@@ -292,7 +301,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   constexpr int NACC = Cfg::NACC;
   const int S = p.stages;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
-  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
+  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS || EPI == EPI_GATE_TOPK);
+  constexpr bool TOPK = (EPI == EPI_GATE_TOPK);
   constexpr int OUT_ES = OUT_F32 ? 4 : 2;
   constexpr int SUB = 128 / OUT_ES;  // columns per staged sub-tile (128 bytes per row)
   extern __shared__ uint8_t smem_raw[];
@@ -307,6 +317,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * Cfg::STG_WARP);  // [2][BN]
   int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [table_len]
   int32_t* plan_s = off_s + p.table_len;                                    // [table_len]
+  // EPI_GATE_TOPK: G tile [128][N + 1] fp32 (row pitch N + 1: a thread's row walk and the
+  // epilogue's column writes both hit 32 distinct banks) and the prefix-alive bitmaps
+  float* gtile = reinterpret_cast<float*>(plan_s + p.table_len);
+  uint32_t* pa_s = reinterpret_cast<uint32_t*>(gtile + TC_BM * (p.N + 1));
+  __shared__ int topk_masked;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -357,6 +372,27 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     __syncthreads();
   }
 
+  // ---- EPI_GATE_TOPK: FilterAlive bitmaps (reading X5) in smem, unless every expert is alive
+  int pa_off[4] = {0, 0, 0, 0};
+  if (TOPK) {
+    int64_t E = 1;
+    for (int i = 0; i < p.topk.d; ++i) E *= p.topk.M;
+    {
+      int64_t wo = 0, n = p.topk.M;
+      for (int i = 0; i < p.topk.d; ++i) { pa_off[i] = (int)wo; wo += (n + 31) / 32; n *= p.topk.M; }
+    }
+    bool dead = false;
+    const int64_t aw = (E + 31) / 32;
+    for (int64_t w = threadIdx.x; w < aw; w += blockDim.x) {
+      const uint32_t want = (w == aw - 1 && (E & 31)) ? ((1u << (E & 31)) - 1u) : 0xffffffffu;
+      dead |= (p.topk.alive[w] & want) != want;
+    }
+    const int masked = __syncthreads_or(dead);
+    if (threadIdx.x == 0) topk_masked = masked;
+    if (masked) prefix_alive_block(p.topk.alive, p.topk.d, p.topk.M, E, pa_s);
+    __syncthreads();
+  }
+
   // ---- tile space (identical walk in every role)
   const int NT = (p.N + BN - 1) / BN;
   const int MT = SEGK ? p.Mdim / TC_BM : 0;
@@ -379,7 +415,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
-  if ((p.dbg & 8) && blockIdx.x == 0) {
+  if ((DMOE_DBG(p) & 8) && blockIdx.x == 0) {
     const unsigned long long t_entry = gtimer();
     for (int i = threadIdx.x; i < TC_PROBE_ROLES * 32; i += blockDim.x) (&g_tc_probe[p.slot][0][0])[i] = 0;
     __syncthreads();
@@ -405,7 +441,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if ((p.dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0) g_tc_probe[p.slot][8][3] = gtimer();
+  if ((DMOE_DBG(p) & 8) && blockIdx.x == 0 && threadIdx.x == 0) g_tc_probe[p.slot][8][3] = gtimer();
 
   // decode a tile -> (group e, row0, row_end, m0, n0, number of K blocks).  SEGK caches the
   // expert's segment bounds per thread (tiles of one expert are consecutive in the walk).
@@ -464,7 +500,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
       };
       auto prefetch_one = [&]() {
-        if (ptile >= t_end || !(p.dbg & 16)) return;  // opt-in (DMOE_TC_DEBUG=16): measured slower
+        if (ptile >= t_end || !(DMOE_DBG(p) & 16)) return;  // opt-in (DMOE_TC_DEBUG=16): measured slower
         if (SEGK) {
           const int kr = (int)(prow0 + pkb * TC_BK);
           tma_prefetch_2d(&tmA, pm0, kr);
@@ -487,7 +523,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       for (int i = 0; i < PF; ++i) prefetch_one();
       // expert weights stream through once (evict first); token / activation tiles are re-read
       // across N tiles (evict last).  DMOE_TC_DEBUG=32 disables the hints.
-      const uint64_t pol_stream = (p.dbg & 32) ? l2_policy_last() : l2_policy_first();
+      const uint64_t pol_stream = (DMOE_DBG(p) & 32) ? l2_policy_last() : l2_policy_first();
       const uint64_t pol_keep = l2_policy_last();
       int stage = 0;
       uint32_t phase = 0;
@@ -532,7 +568,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
       }
       WT_ADD(w_loop, t_loop);
-      if (p.dbg & 64) {
+      if (DMOE_DBG(p) & 64) {
         atomicAdd(&g_tc_wait[p.slot][0], (unsigned long long)w_empty);
         atomicAdd(&g_tc_wait[p.slot][1], (unsigned long long)w_loop);
         atomicAdd(&g_tc_wait[p.slot][11], 1ull);
@@ -580,7 +616,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           const uint32_t a0 = smem_u32(sa), b0 = smem_u32(sb);
 #pragma unroll
           for (int k = 0; k < TC_BK / 16; ++k) {
-            if ((p.dbg & 4) || k >= nk16) break;
+            if ((DMOE_DBG(p) & 4) || k >= nk16) break;
             const uint64_t ad = A_MN ? make_desc(a0 + k * 2048, 8192, 1024) : make_desc(a0 + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(b0 + k * 2048, 8192, 1024) : make_desc(b0 + k * 32, 16, 1024);
             tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
@@ -596,7 +632,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
     }
     WT_ADD(w_loop, t_loop);
-    if ((p.dbg & 64) && lane == 0) {
+    if ((DMOE_DBG(p) & 64) && lane == 0) {
       atomicAdd(&g_tc_wait[p.slot][2], (unsigned long long)w_te);
       atomicAdd(&g_tc_wait[p.slot][3], (unsigned long long)w_full);
       atomicAdd(&g_tc_wait[p.slot][4], (unsigned long long)w_zero);
@@ -677,7 +713,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int ew = warp - 4;
     const int q = warp & 3;
     const int c_beg = (ew >> 2) * Cfg::EPI_COLS;
-    const uint64_t pol_out = (p.dbg & 32) ? l2_policy_last() : l2_policy_first();  // dW: written once
+    const uint64_t pol_out = (DMOE_DBG(p) & 32) ? l2_policy_last() : l2_policy_first();  // dW: written once
     uint8_t* const stg_warp = stage_base + ew * Cfg::STG_WARP;
     uint8_t* stg = stg_warp;
     int stg_buf = 0;  // SEGK: which of the warp's two 4 KB store boxes
@@ -695,7 +731,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       const int mdim = prob ? p.Mdim2 : p.Mdim;
       const bool has_acc = !(SEGK && nkb == 0);
       // stage this tile's bias slice (double-buffered across tiles; one named barrier)
-      constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
+      constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_GATE_TOPK || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
       float* bias_t = bias_s + bias_buf * BN;
       if (HAS_BIAS) {
         for (int c = threadIdx.x - 128; c < BN; c += 32 * Cfg::EPI_WARPS)
@@ -786,7 +822,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         for (int c16 = 0; c16 < SUB; c16 += 16) {
           if (c16 >= ncols) break;
           float v[16];
-          if (has_acc && !(p.dbg & 2)) {
+          if (has_acc && !(DMOE_DBG(p) & 2)) {
             uint32_t r[16];
             TMEM_LD16(tq + cs + c16, r);
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -812,7 +848,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               for (int j = 0; j < 16; ++j) bits |= (v[j] > 0x1p-134f ? 1u : 0u) << j;
               const int col = n0 + cs + c16;  // multiple of 16
               if ((col & 31) == 0) mw_lo = bits;
-              else if (lane < live_rows && !(p.dbg & 1))
+              else if (lane < live_rows && !(DMOE_DBG(p) & 1))
                 p.hmask[(int64_t)(col >> 5) * p.hmask_ld + qrow0 + lane] = mw_lo | (bits << 16);
             }
           }
@@ -822,6 +858,12 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               const int col = c16 + j;
               if (!((hmask[col >> 5] >> (col & 31)) & 1u)) v[j] = 0.0f;
             }
+          }
+          if (TOPK) {
+            float* grow_s = gtile + (q * 32 + lane) * (p.N + 1) + cs + c16;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) grow_s[j] = v[j];
+            continue;
           }
           if (SEGK && !OUT_F32) {
             // 128B-swizzled box row (the TMA store layout): 16-byte chunk q of row `lane`
@@ -848,11 +890,12 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                              pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
           }
         }
+        if (TOPK) continue;
         if (SEGK && !OUT_F32) {
           // full 32 x 64 box: one bulk tensor store (double-buffered box, see above)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
-          if (lane == 0 && !(p.dbg & 1)) {
+          if (lane == 0 && !(DMOE_DBG(p) & 1)) {
             asm volatile(
                 "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
                     mC),
@@ -870,7 +913,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + (lane >> 3), piece = lane & 7;
-          if (r < live_rows && piece * 16 < row_bytes && !(p.dbg & 1)) {
+          if (r < live_rows && piece * 16 < row_bytes && !(DMOE_DBG(p) & 1)) {
             const uint4 v = *reinterpret_cast<const uint4*>(stg + r * TC_STAGE_ROW + piece * 16);
             uint8_t* gdst;
             if (SEGK)
@@ -882,6 +925,38 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
       }
+      if (TOPK) {
+        // the accumulator is in registers / smem now: hand TMEM back to the MMA first
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * Cfg::EPI_WARPS) : "memory");  // whole G tile staged
+        const int tid = threadIdx.x - 128;
+        if (p.C) {  // G (optional output): coalesced 16-byte rows
+          const int q4 = p.N / 4;
+          for (int i = tid; i < TC_BM * q4; i += 32 * Cfg::EPI_WARPS) {
+            const int r = i / q4, c = (i - r * q4) * 4;
+            if (row0 + r < row_end) {
+              const float* src = gtile + r * (p.N + 1) + c;
+              *reinterpret_cast<float4*>((float*)p.C + (row0 + r) * p.N + c) = make_float4(src[0], src[1], src[2], src[3]);
+            }
+          }
+        }
+        if (ew < 4 && lane < live_rows) {  // Alg. 1, one thread per token
+          const int64_t t = qrow0 + lane;
+          const float* grow_s = gtile + (ew * 32 + lane) * (p.N + 1);
+          const GateTopk& tk = p.topk;
+          if (topk_masked)
+            beam_search_row<kTopkWMAX, true>(grow_s, 1, tk.d, tk.M, tk.k, tk.B, pa_s, pa_off, tk.sel + t * tk.k,
+                                             tk.sel_score + t * tk.k);
+          else
+            beam_search_row<kTopkWMAX, false>(grow_s, 1, tk.d, tk.M, tk.k, tk.B, pa_s, pa_off, tk.sel + t * tk.k,
+                                              tk.sel_score + t * tk.k);
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * Cfg::EPI_WARPS) : "memory");  // G tile free again
+        continue;
+      }
       if (ew == 0 && lane == 0) PROBE(5, it);
       if (has_acc) {
         tc_fence_before();
@@ -891,7 +966,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
     }
     WT_ADD(w_loop, t_loop);
-    if ((p.dbg & 64) && ew == 0 && lane == 0) {
+    if ((DMOE_DBG(p) & 64) && ew == 0 && lane == 0) {
       atomicAdd(&g_tc_wait[p.slot][7], (unsigned long long)w_tf);
       atomicAdd(&g_tc_wait[p.slot][8], (unsigned long long)w_st);
       atomicAdd(&g_tc_wait[p.slot][9], (unsigned long long)w_loop);
@@ -899,286 +974,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   }
 
   if (SEGK && warp >= 4 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-  if ((p.dbg & 8) && blockIdx.x == 0 && warp == 4 && lane == 0) g_tc_probe[p.slot][8][4] = gtimer();
+  if ((DMOE_DBG(p) & 8) && blockIdx.x == 0 && warp == 4 && lane == 0) g_tc_probe[p.slot][8][4] = gtimer();
   tc_fence_before();
   __syncthreads();
-  if ((p.dbg & 8) && blockIdx.x == 0 && threadIdx.x == 0) g_tc_probe[p.slot][8][5] = gtimer();
+  if ((DMOE_DBG(p) & 8) && blockIdx.x == 0 && threadIdx.x == 0) g_tc_probe[p.slot][8][5] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
-  }
-}
-
-// --------------------------------------------------------- ROWS engine (swap-AB form)
-// For the row GEMMs C[r, n] = epi(sum_k X[r, k] W_e(n, k)) the expert weights are the MMA
-// M operand (128 output features per tile) and the dispatched tokens the N operand
-// (NT = 64/128/256 token rows per tile).  Each expert's rows are padded only to NT, a
-// stage is 16 KB of weights + NT*128 B of tokens, so 8+ stages keep >= 128 KB of weights in
-// flight per SM: the weight-streaming regime of small expert batches (rows/expert ~ 64)
-// needs that depth.  TMEM lane = output feature, column = token: the epilogue thread owns
-// one feature, so bias is one register and every store instruction writes 32 consecutive
-// features of one token row (coalesced) with rows masked to the expert's segment.
-constexpr int SW_FEAT = 128;  // MMA M (output features per tile)
-
-template <int NT, bool OUT_F32 = false> struct SwCfg {
-  static_assert(NT == 64 || NT == 128 || NT == 256, "token tile");
-  static constexpr int EPI_WARPS = 8;
-  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
-  static constexpr int W_BYTES = SW_FEAT * TC_BK * 2;   // 16 KB
-  static constexpr int X_BYTES = NT * TC_BK * 2;
-  static constexpr int STAGE_BYTES = W_BYTES + X_BYTES;
-  static constexpr int STG_PITCH = SW_FEAT * (OUT_F32 ? 4 : 2) + 16;  // one staged token row of 128 features
-  static constexpr int STG_BYTES = 2 * 32 * STG_PITCH;   // [token half][32 tokens][128 features]
-  static constexpr int FIXED = 1024 + 512 + 2 * TC_TABLE_LEN * 4 + STG_BYTES;
-  static constexpr int ST = (TC_SMEM_MAX - FIXED) / STAGE_BYTES;
-  static constexpr int STAGES = ST > 12 ? 12 : ST;
-  static constexpr int ACC = NT == 256 ? 2 : 4;         // accumulator buffers in TMEM
-  static constexpr int TMEM_COLS = ACC * NT <= 256 ? 256 : 512;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + FIXED;
-};
-
-template <int NT, bool W_MN, int EPI>
-__global__ void __launch_bounds__(SwCfg<NT>::THREADS, 1)
-k_tc_rows(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-          const TcParams p) {
-  DMOE_PDL_ENTRY();
-  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS);
-  using Cfg = SwCfg<NT, OUT_F32>;
-  constexpr int S = Cfg::STAGES;
-  constexpr int ACC = Cfg::ACC;
-  constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = (uint64_t*)(smem + S * Cfg::STAGE_BYTES);
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
-  uint64_t* tempty = tfull + ACC;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + ACC);
-  int32_t* off_s = (int32_t*)(smem + S * Cfg::STAGE_BYTES + 512);
-  int32_t* plan_s = off_s + TC_TABLE_LEN;
-  uint8_t* stg_all = (uint8_t*)(plan_s + TC_TABLE_LEN);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  const int32_t* offs = p.offsets;
-  const int32_t* plan = p.plan;
-  if (p.offsets && p.E <= TC_TABLE_E) {
-    for (int i = threadIdx.x; i <= p.E; i += blockDim.x) {
-      off_s[i] = p.offsets[i];
-      plan_s[i] = p.plan[i];
-    }
-    offs = off_s;
-    plan = plan_s;
-  }
-  const int NFB = (p.N + SW_FEAT - 1) / SW_FEAT;
-  const int total = (p.offsets ? p.plan[p.E] : (int)((p.rows_single + NT - 1) / NT)) * NFB;
-
-  if (warp == 0 && lane == 0) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmW) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
-  }
-  if (warp == 1 && lane == 0) {
-    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < ACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], Cfg::EPI_WARPS); }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(Cfg::TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  // tile -> (expert e, token rows [row0, row_end), feature block f0)
-  auto decode = [&](int tile, int& e, int64_t& row0, int64_t& row_end, int& f0) {
-    const int rt = tile / NFB;
-    f0 = (tile - rt * NFB) * SW_FEAT;
-    if (p.offsets) {
-      int lo = 0, hi = p.E;
-      while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (plan[mid] <= rt) lo = mid; else hi = mid; }
-      e = lo;
-      row0 = offs[e] + (int64_t)(rt - plan[e]) * NT;
-      row_end = offs[e + 1];
-    } else {
-      e = 0;
-      row0 = (int64_t)rt * NT;
-      row_end = p.rows_single;
-    }
-  };
-  const int nkb = p.K / TC_BK;
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-        int e, f0;
-        int64_t row0, row_end;
-        decode(tile, e, row0, row_end, f0);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          if (kb == 0) PROBE(0, it);
-          uint8_t* sw = smem + stage * Cfg::STAGE_BYTES;
-          uint8_t* sx = sw + Cfg::W_BYTES;
-          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          if (W_MN) {
-            tma_load_3d(sw, &tmW, &full[stage], f0, kb * TC_BK, e);
-            tma_load_3d(sw + 8192, &tmW, &full[stage], f0 + 64, kb * TC_BK, e);
-          } else {
-            tma_load_3d(sw, &tmW, &full[stage], kb * TC_BK, f0, e);
-          }
-          tma_load_2d(sx, &tmX, &full[stage], kb * TC_BK, (int)row0);
-          if (++stage == S) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
-  } else if (warp == 1) {  // ---------------- MMA issuer
-    constexpr uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((W_MN ? 1u : 0u) << 15) |
-                               ((uint32_t)(NT >> 3) << 17) | ((uint32_t)(SW_FEAT >> 4) << 24);
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t tmem_d = tmem_base + acc * NT;
-      for (int kb = 0; kb < nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
-        tc_fence_after();
-        if (kb == 0 && lane == 0) PROBE(2, it);
-        if (lane == 0) {
-          const uint32_t w0 = smem_u32(smem + stage * Cfg::STAGE_BYTES);
-          const uint32_t x0 = w0 + Cfg::W_BYTES;
-#pragma unroll
-          for (int k = 0; k < TC_BK / 16; ++k) {
-            if (p.dbg & 4) break;
-            const uint64_t ad = W_MN ? make_desc(w0 + k * 2048, 8192, 1024) : make_desc(w0 + k * 32, 16, 1024);
-            const uint64_t bd = make_desc(x0 + k * 32, 16, 1024);
-            tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
-          }
-          tc_commit(&empty[stage]);
-          if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
-        }
-        __syncwarp();
-        if (++stage == S) { stage = 0; phase ^= 1; }
-      }
-      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
-    }
-  } else if (warp >= 4) {  // ---------------- epilogue
-    // warp (q = warp % 4) owns TMEM lanes 32q..32q+31 = features f0+32q+lane; the two warp
-    // quartets split the tile's tokens.  Per 32-token chunk the quartet stages a
-    // [32 tokens][128 features] block in smem (lane -> one feature column), then each warp
-    // stores 8 token rows as 256-/512-byte contiguous runs, rows masked to the segment.
-    constexpr int OUT_ES = OUT_F32 ? 4 : 2;
-    constexpr int ROWB = SW_FEAT * OUT_ES;     // bytes of one staged token row
-    constexpr int TH = NT / 2;                 // tokens per quartet
-    const int ew = warp - 4;
-    const int q = warp & 3;
-    const int half = ew >> 2;
-    const int t_beg = half * TH;
-    uint8_t* stg = stg_all + half * 32 * Cfg::STG_PITCH;
-    const uint32_t bar_id = 1 + half;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    int it = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x, ++it) {
-      int e, f0;
-      int64_t row0, row_end;
-      decode(tile, e, row0, row_end, f0);
-      const int f = f0 + q * 32 + lane;
-      const bool fvalid = f < p.N;
-      const int nf = p.N - f0 < SW_FEAT ? p.N - f0 : SW_FEAT;   // valid features in the tile
-      int64_t nrows = row_end - (row0 + t_beg);
-      nrows = nrows < 0 ? 0 : (nrows > TH ? TH : nrows);
-      float b = 0.0f;
-      if (HAS_BIAS && fvalid) b = __ldg(p.bias + (int64_t)e * p.N + f);
-      // ReLU-mask source rows h[row][f0 .. f0+127] of the first chunk, prefetched (coalesced)
-      uint4 hreg[4];
-      auto load_h = [&](int c) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = q * 8 + i * 2 + (lane >> 4), piece = lane & 15;
-          hreg[i] = make_uint4(0, 0, 0, 0);
-          if (c + r < nrows && piece * 8 < nf)
-            hreg[i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (row0 + t_beg + c + r) * p.N + f0) + piece);
-        }
-      };
-      if (EPI == EPI_RELU_MASK) load_h(0);
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      if (ew == 0 && lane == 0) PROBE(4, it);
-      const uint32_t tq = tmem_base + ((uint32_t)(q * 32) << 16) + acc * NT + t_beg;
-#pragma unroll 1
-      for (int c = 0; c < TH; c += 32) {
-        if (c >= nrows) break;  // uniform across the quartet (same nrows)
-        uint32_t hm = 0xffffffffu;  // bit j: h[row c+j][f] > 0
-        if (EPI == EPI_RELU_MASK) {
-          if (c > 0) load_h(c);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int r = q * 8 + i * 2 + (lane >> 4), piece = lane & 15;
-            *reinterpret_cast<uint4*>(stg + r * Cfg::STG_PITCH + piece * 16) = hreg[i];
-          }
-          asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-          hm = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const uint16_t hv = *reinterpret_cast<const uint16_t*>(stg + j * Cfg::STG_PITCH + (q * 32 + lane) * 2);
-            hm |= (bf16_pos(hv) ? 1u : 0u) << j;
-          }
-          asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-        }
-        // TMEM -> registers -> epilogue math -> staging column (this lane's feature)
-#pragma unroll
-        for (int c16 = 0; c16 < 32; c16 += 16) {
-          uint32_t r[16];
-          TMEM_LD16(tq + c + c16, r);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float v = __uint_as_float(r[j]);
-            if (HAS_BIAS) v += b;
-            if (EPI == EPI_BIAS_RELU) v = fmaxf(v, 0.0f);
-            if (EPI == EPI_RELU_MASK) v = ((hm >> (c16 + j)) & 1u) ? v : 0.0f;
-            uint8_t* dst = stg + (c16 + j) * Cfg::STG_PITCH + (q * 32 + lane) * OUT_ES;
-            if (OUT_F32) *reinterpret_cast<float*>(dst) = v;
-            else *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(v);
-          }
-        }
-        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-        // staging -> global: warp q stores token rows 8q .. 8q+7
-        if (!(p.dbg & 1)) {
-          constexpr int LPR = ROWB / 16;           // 16-byte pieces per row (16 or 32)
-          constexpr int RPI = 32 / LPR;            // rows per instruction (2 or 1)
-#pragma unroll
-          for (int i = 0; i < 8 / RPI; ++i) {
-            const int r = q * 8 + i * RPI + lane / LPR, piece = lane % LPR;
-            if (c + r < nrows && piece * 16 < nf * OUT_ES) {
-              const uint4 v = *reinterpret_cast<const uint4*>(stg + r * Cfg::STG_PITCH + piece * 16);
-              uint8_t* g = (uint8_t*)p.C + ((row0 + t_beg + c + r) * p.N + f0) * OUT_ES + piece * 16;
-              *reinterpret_cast<uint4*>(g) = v;
-            }
-          }
-        }
-        asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-      }
-      if (ew == 0 && lane == 0) PROBE(5, it);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == ACC) { acc = 0; acc_phase ^= 1; }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS));
   }
 }
 
@@ -1221,7 +1023,7 @@ static dmoe_status make_map(CUtensorMap* m, const void* ptr, int rank, const uin
 static int pick_bn(int N, bool b_mn) {
   static int force = -1;
   if (force < 0) {
-    const char* e = getenv("DMOE_TC_BN");  // experiment override: 128 / 256
+    const char* e = dmoe_env("DMOE_TC_BN");  // experiment override: 128 / 256
     force = e ? atoi(e) : 0;
   }
   if ((force == 128 || force == 256) && N % force == 0) return force;
@@ -1235,7 +1037,7 @@ static int pick_bn(int N, bool b_mn) {
 // 128 balances the persistent grid markedly better (tiles per SM rounded up to whole waves)
 static int pick_bn_balanced(int N, bool b_mn, int64_t units) {
   const int bn = pick_bn(N, b_mn);
-  if (bn != 256 || getenv("DMOE_TC_BN")) return bn;
+  if (bn != 256 || dmoe_env("DMOE_TC_BN")) return bn;
   const int64_t sms = num_sms();
   auto eff = [&](int b) {
     const int64_t tiles = units * (N / b);
@@ -1245,41 +1047,29 @@ static int pick_bn_balanced(int N, bool b_mn, int64_t units) {
   return eff(128) > eff(256) + 0.08 ? 128 : 256;
 }
 
-static bool rows_swap();
-int tc_plan_in_kernel_max() { return rows_swap() ? 0 : TC_TABLE_E; }
-bool tc_rows_mmajor() { return !rows_swap(); }
+int tc_plan_in_kernel_max() { return TC_TABLE_E; }
+bool tc_rows_mmajor() { return true; }
 
-static bool rows_swap() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DMOE_TC_ROWS");  // "swap": swap-AB row kernel (experiment)
-    v = (e && e[0] == 's') ? 1 : 0;
-  }
-  return v == 1;
-}
-
-// token tile of the row GEMMs from the expected rows per expert (capacity / experts)
-int tc_rows_tile(const GemmRows& g) {
-  if (!rows_swap()) return TC_BM;  // M-major kernel: 128-row token tiles
-  if (!g.offsets) return 64;
-  static int force = -1;
-  if (force < 0) {
-    const char* e = getenv("DMOE_TC_NT");  // experiment override: 64 / 128 / 256
-    force = e ? atoi(e) : 0;
-  }
-  if (force == 64 || force == 128 || force == 256) return force;
-  const int64_t avg = g.rows_cap / (g.E > 0 ? g.E : 1);
-  return avg <= 32 ? 64 : (avg <= 160 ? 128 : 256);
-}
+// token rows per tile of the row GEMMs (the plan granularity)
+int tc_rows_tile(const GemmRows&) { return TC_BM; }
 
 bool tc_rows_supported(const GemmRows& g) {
   if (g.K % TC_BK != 0 || g.K <= 0 || g.N % 16 != 0) return false;
   if (g.b_mn && g.N % 64 != 0) return false;
-  if (!rows_swap() && pick_bn(g.N, g.b_mn) == 0) return false;
+  if (pick_bn(g.N, g.b_mn) == 0) return false;
   if (g.epi == EPI_F32_BIAS && g.offsets != nullptr) return false;
   if (encode_fn() == nullptr) return false;
   return true;
 }
+// the fused gate + SelectExperts epilogue: one N tile of K-major W_g^T (d*M <= 128 columns,
+// a multiple of 16), beam widths <= 8, prefix bitmaps that fit in smem
+bool tc_gate_topk_supported(int dM, int D, int d, int M, int beam) {
+  int64_t words = 0, n = M;
+  for (int i = 0; i < d; ++i) { words += (n + 31) / 32; n *= M; }
+  return dM % 16 == 0 && dM <= 128 && D % TC_BK == 0 && beam <= kTopkWMAX && words <= kTopkPAWords &&
+         encode_fn() != nullptr;
+}
+
 bool tc_segk_supported(const GemmSegK& g) {
   return g.Mdim % TC_BM == 0 && g.N % 128 == 0 && encode_fn() != nullptr;
 }
@@ -1288,7 +1078,7 @@ bool tc_segk_colsum_supported(const GemmSegK& g) { return tc_segk_supported(g); 
 static int debug_flags() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("DMOE_TC_DEBUG");
+    const char* e = dmoe_env("DMOE_TC_DEBUG");
     f = e ? atoi(e) : 0;
   }
   return f;
@@ -1297,7 +1087,7 @@ static int debug_flags() {
 static int debug_flags_segk() {
   static int f = -1;
   if (f < 0) {
-    const char* e = getenv("DMOE_TC_DEBUG_SEGK");
+    const char* e = dmoe_env("DMOE_TC_DEBUG_SEGK");
     f = e ? atoi(e) : 0;
   }
   return f;
@@ -1309,7 +1099,8 @@ static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const
                                const TcParams& p, int64_t max_tiles, cudaStream_t s) {
   auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
   const int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
-  const int smem = TcCfg<BN, SEGK>::smem_for(table_len);
+  const int extra = EPI == EPI_GATE_TOPK ? p.topk_bytes : 0;
+  const int smem = TcCfg<BN, SEGK>::smem_for(table_len, extra);
   static int attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1321,7 +1112,7 @@ static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const
   TcParams pp = p;
   pp.dbg = debug_flags() | (SEGK ? debug_flags_segk() : 0);
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  pp.stages = TcCfg<BN, SEGK>::stages_for(table_len);
+  pp.stages = TcCfg<BN, SEGK>::stages_for(table_len, extra);
   pp.table_len = table_len;
   launch_pdl(kern, (unsigned)grid, TcCfg<BN, SEGK>::THREADS, smem, s, a, b, c, a2, b2, c2, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
@@ -1340,6 +1131,9 @@ static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtens
 #define DMOE_TC_EPI(BMN)                                   \
   switch (g.epi) {                                         \
     case EPI_F32_BIAS: DMOE_TC_ROWS(BMN, EPI_F32_BIAS);    \
+    case EPI_GATE_TOPK:                                    \
+      if constexpr (!BMN && BN <= 128) { DMOE_TC_ROWS(BMN, EPI_GATE_TOPK); } \
+      return set_error(DMOE_ERR_UNSUPPORTED, "gate_topk: N tile %d", BN);   \
     case EPI_BIAS_RELU: DMOE_TC_ROWS(BMN, EPI_BIAS_RELU);  \
     case EPI_BIAS: DMOE_TC_ROWS(BMN, EPI_BIAS);            \
     case EPI_RELU_MASK: DMOE_TC_ROWS(BMN, EPI_RELU_MASK);  \
@@ -1375,6 +1169,13 @@ static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
   p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
   p.max_ctas = g.max_ctas;
   p.hmask = g.hmask; p.hmask_ld = g.hmask_ld;
+  if (g.epi == EPI_GATE_TOPK) {
+    int64_t E = 1, words = 0, n = g.topk.M;
+    for (int i = 0; i < g.topk.d; ++i) { E *= g.topk.M; words += (n + 31) / 32; n *= g.topk.M; }
+    p.topk = g.topk;
+    p.pa_words = (int)words;
+    p.topk_bytes = (int)align_up((size_t)TC_BM * (g.N + 1) * 4 + (size_t)words * 4, 16);
+  }
   const int64_t tiles = g.max_tiles * ((g.N + BN - 1) / BN);
   switch (BN) {
     case 256: return rows_bn<256>(g, ta, tb, p, tiles, s);
@@ -1390,69 +1191,7 @@ static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
 }
 
 
-template <int NT, bool W_MN, int EPI>
-static dmoe_status launch_rows(const CUtensorMap& w, const CUtensorMap& x, const TcParams& p, int64_t max_tiles,
-                               cudaStream_t s) {
-  auto kern = k_tc_rows<NT, W_MN, EPI>;
-  const int smem = SwCfg<NT, EPI == EPI_F32_BIAS>::SMEM;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
-  int64_t grid = max_tiles < num_sms() ? max_tiles : num_sms();
-  if (grid < 1) grid = 1;
-  TcParams pp = p;
-  pp.dbg = debug_flags();
-  pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  launch_pdl(kern, (unsigned)grid, SwCfg<NT>::THREADS, smem, s, w, x, pp);
-  __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
-  return check_launch("tc_gemm_rows");
-}
-
-template <int NT>
-static dmoe_status rows_nt(const GemmRows& g, const CUtensorMap& w, const CUtensorMap& x, const TcParams& p,
-                           int64_t tiles, cudaStream_t s) {
-#define DMOE_TC_ROWS(WMN, E_) return launch_rows<NT, WMN, E_>(w, x, p, tiles, s)
-#define DMOE_TC_EPI(WMN)                                   \
-  switch (g.epi) {                                         \
-    case EPI_F32_BIAS: DMOE_TC_ROWS(WMN, EPI_F32_BIAS);    \
-    case EPI_BIAS_RELU: DMOE_TC_ROWS(WMN, EPI_BIAS_RELU);  \
-    case EPI_BIAS: DMOE_TC_ROWS(WMN, EPI_BIAS);            \
-    case EPI_RELU_MASK: DMOE_TC_ROWS(WMN, EPI_RELU_MASK);  \
-    default: DMOE_TC_ROWS(WMN, EPI_PLAIN);                 \
-  }
-  if (g.b_mn) { DMOE_TC_EPI(true) }
-  DMOE_TC_EPI(false)
-#undef DMOE_TC_EPI
-#undef DMOE_TC_ROWS
-}
-
-dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) {
-  if (g.max_tiles <= 0) return DMOE_OK;
-  if (!rows_swap()) return tc_gemm_rows_mk(g, s);
-  const int NT = tc_rows_tile(g);
-  // W (MMA A): K-major [E][N][K] boxes {64 K, 128 features}, or MN-major [E][K][N] boxes
-  // {64 features, 64 K} x 2.  X (MMA B): tokens [rows_cap][K], boxes {64 K, NT rows};
-  // rows past rows_cap are zero-filled by TMA, rows past a segment are never stored.
-  CUtensorMap tw, tx;
-  if (g.b_mn) {
-    uint64_t d[3] = {(uint64_t)g.N, (uint64_t)g.K, (uint64_t)g.E};
-    DMOE_TRY(make_map(&tw, g.B, 3, d, 64));
-  } else {
-    uint64_t d[3] = {(uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.E};
-    DMOE_TRY(make_map(&tw, g.B, 3, d, SW_FEAT));
-  }
-  uint64_t xd[2] = {(uint64_t)g.K, (uint64_t)(g.rows_cap > 0 ? g.rows_cap : 1)};
-  DMOE_TRY(make_map(&tx, g.A, 2, xd, (uint32_t)NT));
-  TcParams p{};
-  p.offsets = g.offsets; p.plan = g.plan; p.bias = g.bias; p.aux = (const __nv_bfloat16*)g.aux;
-  p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
-  const int64_t tiles = g.max_tiles * ((g.N + SW_FEAT - 1) / SW_FEAT);
-  if (NT == 64) return rows_nt<64>(g, tw, tx, p, tiles, s);
-  if (NT == 128) return rows_nt<128>(g, tw, tx, p, tiles, s);
-  return rows_nt<256>(g, tw, tx, p, tiles, s);
-}
+dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s) { return tc_gemm_rows_mk(g, s); }
 
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   // weight-gradient tiles have ~1 K block each and are bound by shared-memory traffic (TMA

@@ -53,7 +53,6 @@ class EPDMoELayer:
         self.dW2, self.db2 = e(El, D, H), e(El, D, dt=f32)
         T = T_max
         R = T * k                                     # rows this rank sends at most
-        self.G_ = e(T, dM, dt=f32)
         self.sel, self.sel_score = e(T, k, dt=i32), e(T, k, dt=f32)
         self.w, self.valid, self.n_dropped = e(T, k, dt=f32), e(T, dt=torch.uint8), e(1, dt=i32)
         self.counts, self.offsets = e(E, dt=i32), e(E + 1, dt=i32)
@@ -89,8 +88,7 @@ class EPDMoELayer:
     def forward(self, x, alive_bits, responded_bits):
         T = x.shape[0]
         self._x = x
-        L.dmoe_gate_scores(x, self.Wg, self.bg, self.g, self.G_[:T], self.ws)
-        L.dmoe_beam_topk(self.G_[:T], self.g, alive_bits, self.sel[:T], self.sel_score[:T], self.ws)
+        L.dmoe_gate_topk(x, self.Wg, self.bg, self.g, alive_bits, None, self.sel[:T], self.sel_score[:T], self.ws)
         L.dmoe_dispatch(x, self.g, self.sel[:T], self.sel_score[:T], responded_bits, self.w[:T], self.valid[:T],
                         self.n_dropped, self.counts, self.offsets, self.row_of_slot[:T], self.token_of_row,
                         self.xd, self.ws)

@@ -101,6 +101,9 @@ class HostPipeline:
         self.n += 1
 
     def synchronize(self):
+        """Wait for every submitted step; raises if the layer's exchange reported an error."""
         self.d2h.synchronize()
         self.compute.synchronize()
         self.h2d.synchronize()
+        if hasattr(self.lay, "check"):
+            self.lay.check()

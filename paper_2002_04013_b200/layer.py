@@ -15,8 +15,9 @@ from . import _lib as L
 
 class DMoELayer:
     def __init__(self, d, M, k, D, H, dtype=torch.bfloat16, beam=0, T_max=4096, device="cuda",
-                 E_local=None, R_cap=None):
+                 E_local=None, R_cap=None, pool=0, keep_G=False):
         self.d, self.M, self.k, self.D, self.H = d, M, k, D, H
+        self.keep_G = keep_G  # also write the gate scores G (tests); the fused path otherwise never stores them
         self.beam = beam or k
         self.E = M ** d
         self.E_local = E_local or self.E
@@ -27,7 +28,12 @@ class DMoELayer:
         dev = torch.device(device)
         f32 = torch.float32
         dM = d * M
-        E, El = self.E, self.E_local
+        E = self.E
+        # tied-weight pool (reading X20): `pool` parameter slots, expert e -> slot e // tie
+        self.P = pool or self.E_local
+        assert self.E_local % self.P == 0
+        self.tie = self.E_local // self.P
+        El = self.P
         e = lambda *s, dt=dtype: torch.empty(*s, dtype=dt, device=dev)
         # parameters (filled by the caller / generator)
         self.Wg, self.bg = e(D, dM), e(dM, dt=f32)
@@ -39,7 +45,7 @@ class DMoELayer:
         self.dW2, self.db2 = e(El, D, H), e(El, D, dt=f32)
         # activations / routing records (forward) and backward buffers
         T, R = T_max, self.R_cap
-        self.G = e(T, dM, dt=f32)
+        self.G = e(T if keep_G else 1, dM, dt=f32)
         self.sel = e(T, k, dt=torch.int32)
         self.sel_score = e(T, k, dt=f32)
         self.w = e(T, k, dt=f32)
@@ -47,6 +53,8 @@ class DMoELayer:
         self.n_dropped = e(1, dt=torch.int32)
         self.counts = e(E, dt=torch.int32)
         self.offsets = e(E + 1, dt=torch.int32)
+        # FFN segments: the slot segments offsets[::tie] when tied, else offsets itself
+        self.seg = e(El + 1, dt=torch.int32) if self.tie > 1 else self.offsets
         self.row_of_slot = e(T, k, dt=torch.int32)
         self.token_of_row = e(max(T * k, 1), dt=torch.int32)
         self.xd = e(max(R, 1), D)
@@ -67,12 +75,14 @@ class DMoELayer:
         T = x.shape[0]
         assert T <= self.T_max and x.dtype == self.dtype and x.shape[1] == self.D
         self._x = x
-        L.dmoe_gate_scores(x, self.Wg, self.bg, self.g, self.G[:T], self.ws)
-        L.dmoe_beam_topk(self.G[:T], self.g, alive_bits, self.sel[:T], self.sel_score[:T], self.ws)
+        L.dmoe_gate_topk(x, self.Wg, self.bg, self.g, alive_bits, self.G[:T] if self.keep_G else None,
+                         self.sel[:T], self.sel_score[:T], self.ws)
         L.dmoe_dispatch(x, self.g, self.sel[:T], self.sel_score[:T], responded_bits, self.w[:T], self.valid[:T],
                         self.n_dropped, self.counts, self.offsets, self.row_of_slot[:T], self.token_of_row,
                         self.xd, self.ws)
-        L.dmoe_expert_ffn_fwd(self.xd, self.offsets, self.W1, self.b1, self.W2, self.b2, self.h, self.out,
+        if self.tie > 1:
+            L.dmoe_segment_offsets(self.offsets, self.tie, self.seg)
+        L.dmoe_expert_ffn_fwd(self.xd, self.seg, self.W1, self.b1, self.W2, self.b2, self.h, self.out,
                               self.ws, hmask=self.hmask)
         L.dmoe_combine(self.out, self.row_of_slot[:T], self.w[:T], self.valid[:T], self.y[:T])
         return self.y[:T]
@@ -82,7 +92,7 @@ class DMoELayer:
         x = self._x
         T = x.shape[0]
         L.dmoe_combine_bwd(dy, self.out, self.row_of_slot[:T], self.w[:T], self.dout, self.dscore[:T])
-        L.dmoe_expert_ffn_bwd(self.xd, self.h, self.dout, self.offsets, self.W1, self.W2, self.dxd,
+        L.dmoe_expert_ffn_bwd(self.xd, self.h, self.dout, self.seg, self.W1, self.W2, self.dxd,
                               self.dW1, self.db1, self.dW2, self.db2, self.ws, hmask=self.hmask)
         L.dmoe_gate_bwd(x, self.Wg, self.sel[:T], self.dscore[:T], self.dxd, self.row_of_slot[:T], self.g,
                         self.dx[:T], self.dWg, self.dbg, self.ws)

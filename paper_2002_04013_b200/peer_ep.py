@@ -68,7 +68,6 @@ class PeerEPDMoELayer:
         self.dW1, self.db1 = e(El, H, D), e(El, H, dt=f32)
         self.dW2, self.db2 = e(El, D, H), e(El, D, dt=f32)
         # local (not peer-written) buffers
-        self.G_ = e(T, dM, dt=f32)
         self.sel, self.sel_score = e(T, k, dt=i32), e(T, k, dt=f32)
         self.w, self.valid, self.n_dropped = e(T, k, dt=f32), e(T, dt=torch.uint8), e(1, dt=i32)
         self.counts, self.offsets = e(E, dt=i32), e(E + 1, dt=i32)
@@ -132,8 +131,7 @@ class PeerEPDMoELayer:
         self._x = x
         ep = self.ep
         L.dmoe_ep_begin(ep)
-        L.dmoe_gate_scores(x, self.Wg, self.bg, self.g, self.G_[:T], self.ws)
-        L.dmoe_beam_topk(self.G_[:T], self.g, alive_bits, self.sel[:T], self.sel_score[:T], self.ws)
+        L.dmoe_gate_topk(x, self.Wg, self.bg, self.g, alive_bits, None, self.sel[:T], self.sel_score[:T], self.ws)
         L.dmoe_dispatch(x, self.g, self.sel[:T], self.sel_score[:T], responded_bits, self.w[:T], self.valid[:T],
                         self.n_dropped, self.counts, self.offsets, self.row_of_slot[:T], self.token_of_row,
                         None, self.ws)
@@ -170,7 +168,12 @@ class PeerEPDMoELayer:
         return host_step(self, hx, hdy, hy, hdx, alive_bits, responded_bits)
 
     def check(self):
-        """Raise if a wait timed out (err & 1) or a receive buffer would have overflowed (err & 2)."""
+        """Raise if a wait timed out (err & 1) or a receive buffer would have overflowed (err & 2)
+        since the last check.  The error word is sticky inside the kernels (once set, every later
+        push / return of this rank skips its row writes, so a broken step cannot scribble over
+        peers' buffers); reading it here clears it, so the next step runs normally.  Callers must
+        check at their sync points: HostPipeline.synchronize() does."""
         v = int(self.err.item())
         if v:
+            self.err.zero_()
             raise RuntimeError(f"peer exchange error word {v} (1 = wait timeout, 2 = receive overflow)")

@@ -28,6 +28,15 @@ class FakeLib:
         G[:] = torch.from_numpy(O.gate_scores(x.numpy(), Wg.numpy(), bg.numpy()))
 
     @staticmethod
+    def dmoe_gate_topk(x, Wg, bg, g, alive_bits, G, sel, sel_score, ws):
+        Gv = O.gate_scores(x.numpy(), Wg.numpy(), bg.numpy())
+        if G is not None:
+            G[:] = torch.from_numpy(Gv)
+        s, sc, _ = O.select_experts(Gv, g.d, g.M, g.k, g.beam, _bits(alive_bits, g.M ** g.d))
+        sel[:] = torch.from_numpy(s)
+        sel_score[:] = torch.from_numpy(sc)
+
+    @staticmethod
     def dmoe_beam_topk(G, g, alive_bits, sel, sel_score, ws):
         s, sc, _ = O.select_experts(G.numpy(), g.d, g.M, g.k, g.beam, _bits(alive_bits, g.M ** g.d))
         sel[:] = torch.from_numpy(s)

@@ -29,8 +29,9 @@ def gpu_layer(cfg, inp, T=None):
     from paper_2002_04013_b200 import DMoELayer
     T = inp["X"].shape[0] if T is None else T
     dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
-    lay = DMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=max(T, 1))
-    E, D, H, dM = cfg.E, cfg.D, cfg.H, cfg.dM
+    lay = DMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=max(T, 1), pool=cfg.pool,
+                    keep_G=True)
+    E, D, H, dM = cfg.P, cfg.D, cfg.H, cfg.dM   # parameter slots
     lay.Wg.copy_(to_torch(inp["dev_Wg"], cfg.dtype, (D, dM)))
     lay.bg.copy_(torch.from_numpy(inp["dev_bg"]).cuda())
     lay.W1.copy_(to_torch(inp["dev_W1"], cfg.dtype, (E, H, D)))
@@ -64,7 +65,7 @@ def oracle_step(cfg, inp, sel_override=None):
     from oracle import oracle as O
     return O.layer_step(inp["X"], inp["Wg"], inp["bg"], inp["W1"], inp["b1"], inp["W2"], inp["b2"],
                         inp["dY"], inp["alive"], inp["responded"], cfg.d, cfg.M, cfg.k, cfg.B,
-                        sel_override=sel_override)
+                        sel_override=sel_override, tie=cfg.tie)
 
 
 def check_routing(cfg, gsel, ref, exact, alive):

@@ -154,3 +154,30 @@ def test_host_pipeline_matches_device_steps():
         pipe.synchronize()
         for (y_ref, dx_ref), (_, _, hy, hdx) in zip(want, host):
             assert np.array_equal(np64(hy), y_ref) and np.array_equal(np64(hdx), dx_ref)
+
+
+@pytest.mark.parametrize("T", [77, 600])
+def test_k8_30pct_failures_mnist_grid(T):
+    """k = 8 (the stress configuration's k) with 30% non-responding experts, full oracle: runs
+    the k = 8 instantiations of beam top-k, combine, combine backward and the gate backward."""
+    cfg = CONFIGS["mnist"].with_(k=8, fail_frac=0.3)
+    inp = make_inputs(cfg, seed=30, T=T)
+    _compare_layer(cfg, inp, gpu_layer(cfg, inp))
+
+
+def test_stress_shape_tied_pool():
+    """BASELINE config 5's shapes (64x64 grid, d_model 2048, FFN hidden 8192, k = 8, 30% dropped
+    experts) at a reduced token count, with the declared tied-weight pool (reading X20: 16
+    parameter slots, expert e -> slot e // 256): routing over all 4096 experts, the FFN GEMMs at
+    K = 2048 / 8192 over slot segments that span many experts, dW summed over tied experts."""
+    cfg = CONFIGS["stress"].with_(pool=16)
+    inp = make_inputs(cfg, seed=31, T=128)
+    _compare_layer(cfg, inp, gpu_layer(cfg, inp))
+
+
+def test_tied_pool_exact_grid_masked():
+    """Tied pool on the 16x16 grid with dead experts and B > k, exact-grid inputs (all routing
+    compared bit for bit)."""
+    cfg = CONFIGS["mnist"].with_(pool=32, exact_grid=True, dead_frac=0.2, fail_frac=0.2, beam=6, k=5)
+    inp = make_inputs(cfg, seed=32, T=500)
+    _compare_layer(cfg, inp, gpu_layer(cfg, inp), exact=True)

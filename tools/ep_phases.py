@@ -37,7 +37,7 @@ def mark(name):
 
 
 # wrap the binding's calls used by the layer so that each is bracketed by events
-names = ["dmoe_ep_begin", "dmoe_gate_scores", "dmoe_beam_topk", "dmoe_dispatch", "dmoe_ep_exchange_counts",
+names = ["dmoe_ep_begin", "dmoe_gate_topk", "dmoe_dispatch", "dmoe_ep_exchange_counts",
          "dmoe_ep_push_rows", "dmoe_expert_ffn_fwd", "dmoe_ep_return_rows", "dmoe_combine", "dmoe_combine_bwd",
          "dmoe_expert_ffn_bwd", "dmoe_gate_bwd"]
 orig = {n: getattr(L, n) for n in names}

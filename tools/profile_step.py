@@ -15,8 +15,12 @@ from gen import CONFIGS  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="mnist")
 ap.add_argument("--steps", type=int, default=3)
+ap.add_argument("--set", nargs="*", default=[],
+                help="config overrides key=int, e.g. M=16 T=4096 (a transformer-shaped slice: 64 rows/expert)")
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
+if a.set:
+    cfg = cfg.with_(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.set})
 lay, x, dy, alive, resp = bench.build_layer(cfg, 0, torch.device("cuda", 0), cfg.T)
 for _ in range(a.steps):
     bench.run_calls(lay, x, dy, alive, resp)

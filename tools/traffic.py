@@ -11,8 +11,9 @@ import sys
 
 # kernel-name prefixes launched by each ABI call, in step order
 CALLS = [
-    ("gate_scores", ["k_transpose", "k_tc_gemm<32", "k_tc_gemm<48", "k_tc_gemm<128, 0, 0, 0>", "k_simt_rows"]),
-    ("beam_topk", ["k_prefix_alive", "k_beam_topk"]),
+    ("gate_topk", ["k_transpose", "k_tc_gemm<32, 0, 0, 5>", "k_tc_gemm<48, 0, 0, 5>", "k_tc_gemm<128, 0, 0, 5>",
+                   "k_tc_gemm<32, 0, 0, 0>", "k_tc_gemm<48, 0, 0, 0>", "k_tc_gemm<128, 0, 0, 0>", "k_simt_rows",
+                   "k_prefix_alive", "k_beam_topk"]),
     ("dispatch", ["k_weights_hist", "k_scan_chunks", "k_scan_experts", "k_rank", "k_gather"]),
     ("expert_ffn_fwd", ["k_tile_plan", "k_tc_gemm<256, 0, 0, 1>", "k_tc_gemm<256, 0, 0, 2>", "k_tc_gemm<128, 0, 0, 1>",
                         "k_tc_gemm<128, 0, 0, 2>"]),
