@@ -189,6 +189,23 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
                                 const void* W2, void* dxd, void* dW1, float* db1, void* dW2,
                                 float* db2, void* ws, size_t ws_bytes, dmoe_stream_t stream);
 
+/* S9 + the runtime's parameter update (NEXT-1): "compute gradients w.r.t. inputs and update
+ * expert parameters by gradient descent" (§3.3), with optional gradient
+ * checkpointing (the expert "called twice per batch").
+ * The same gradients as dmoe_expert_ffn_bwd, applied in place instead of written out:
+ *   dh  = (dout W2[e]) * 1[h > 0];   dxd = dh W1[e]          (with the weights BEFORE the update)
+ *   W2[e] -= lr * dout^T h;  b2[e] -= lr * sum_rows dout;  W1[e] -= lr * dh^T xd;  b1[e] -= lr * sum_rows dh
+ * The weight-gradient tiles are applied by the GEMM epilogue (TMA loads the parameter tile into
+ * the store box, W - lr * dW in fp32, one bf16 rounding: reading X21), so no dW buffer exists and
+ * dW never reaches HBM.  Experts without rows keep their parameters.
+ * h: the saved hidden activation, or NULL to recompute it from xd, W1, b1 here (then hmask is
+ * ignored).  W1, W2 in/out bf16; b1, b2 in/out fp32.  bf16 tensor-core path only (D, H multiples
+ * of 128): DMOE_ERR_UNSUPPORTED otherwise. */
+dmoe_status dmoe_expert_ffn_bwd_sgd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
+                                    const int32_t* offsets, int32_t E_local, int64_t R_cap, int32_t D,
+                                    int32_t H, dmoe_dtype dt, void* W1, float* b1, void* W2, float* b2,
+                                    float lr, void* dxd, void* ws, size_t ws_bytes, dmoe_stream_t stream);
+
 /* S10 — undispatch + gate backward (gradient of Eq. 2 through the Eq. 3 softmax):
  *   dG[t, i*M + u_i(sel[t,s])] += dscore[t,s]            (u_i per X1)
  *   dx[t]  = sum_{ok s} dxd[row_of_slot[t,s]] + sum_j dG[t,j] W_g[:, j]

@@ -255,3 +255,9 @@ def layer_step_tokens(X, dY, Wg, bg, experts, alive, responded, d, M, k, B, sel_
     dX, dWg, dbg = gate_bwd(X, Wg, sel, dscore, dx_rows, ros, d, M)
     return dict(G=G, sel=sel, sel_score=sc, gap=gap, w=w, ok=ok, valid=valid, n_dropped=nd, experts=used,
                 y=y, dscore=dscore, dX=dX, a=a, out=out, dW1=dW1, db1=db1, dW2=dW2, db2=db2, dWg=dWg, dbg=dbg)
+
+
+def sgd_update(param, grad, lr):
+    """The runtime's parameter update after a Backward request: "update expert parameters by
+    gradient descent" (§3.3), plain SGD: param - lr * grad (float64)."""
+    return np.asarray(param, np.float64) - float(lr) * np.asarray(grad, np.float64)

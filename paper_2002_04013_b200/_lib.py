@@ -56,6 +56,8 @@ _SIGS = {
     "dmoe_combine_bwd": ([_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P], ctypes.c_int),
     "dmoe_expert_ffn_bwd": ([_P, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                              _SZ, _P], ctypes.c_int),
+    "dmoe_expert_ffn_bwd_sgd": ([_P, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, ctypes.c_float,
+                                 _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_gate_bwd": ([_P, _P, _P, _P, _P, _P, _I64, _I32, dmoe_grid, _I32, _P, _P, _P, _P, _SZ, _P],
                       ctypes.c_int),
     "dmoe_segment_offsets": ([_P, _I32, _I32, _P, _P], ctypes.c_int),
@@ -172,6 +174,14 @@ def dmoe_expert_ffn_bwd(xd, h, dout, offsets, W1, W2, dxd, dW1, db1, dW2, db2, w
     _check("dmoe_expert_ffn_bwd", _L.dmoe_expert_ffn_bwd(
         _p(xd), _p(h), _p(hmask) if hmask is not None else None, _p(dout), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd), _p(W1), _p(W2), _p(dxd),
         _p(dW1), _p(db1), _p(dW2), _p(db2), _p(ws), ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_expert_ffn_bwd_sgd(xd, h, dout, offsets, W1, b1, W2, b2, lr, dxd, ws, hmask=None):
+    """h may be None (recomputed in the call: gradient checkpointing)."""
+    E_local, H, D = W1.shape
+    _check("dmoe_expert_ffn_bwd_sgd", _L.dmoe_expert_ffn_bwd_sgd(
+        _p(xd), _p(h), _p(hmask), _p(dout), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd), _p(W1), _p(b1),
+        _p(W2), _p(b2), float(lr), _p(dxd), _p(ws), ws.numel() * ws.element_size(), _stream()))
 
 
 def dmoe_gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, g, dx, dWg, dbg, ws):

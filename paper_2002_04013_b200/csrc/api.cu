@@ -244,7 +244,9 @@ size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_
   size_t beam = align_up(prefix_words(g.d, g.M) * 4, 256) + align_up((size_t)g.d * g.M * D * 2, 256) +
                 (size_t)T * g.d * g.M * 4 + 1024;
   size_t disp = dispatch_ws_bytes(T, E);
-  size_t ffn = 2 * align_up((size_t)(E_local + 1) * 4, 256) + align_up((size_t)R_cap * H * 4, 256) + 1024;
+  // expert FFN: plans, dh (fp32 capacity), and the recomputed h + ReLU record of the SGD call
+  size_t ffn = 2 * align_up((size_t)(E_local + 1) * 4, 256) + align_up((size_t)R_cap * H * 4, 256) +
+               align_up((size_t)R_cap * H * 2, 256) + align_up((size_t)((H + 31) / 32) * R_cap * 4, 256) + 1024;
   size_t gate = gate_bwd_ws_bytes(T, D, g.d * g.M);
   size_t exch = (size_t)8 * E + 1024;  // exchange tables (G * E_local <= E)
   size_t m = beam;
@@ -484,6 +486,66 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
   if (fused) return DMOE_OK;
   DMOE_TRY(seg_colsum(dout, dt, offsets, E_local, D, db2, s));
   return seg_colsum(dh, dt, offsets, E_local, H, db1, s);
+}
+
+dmoe_status dmoe_expert_ffn_bwd_sgd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
+                                    const int32_t* offsets, int32_t E_local, int64_t R_cap, int32_t D,
+                                    int32_t H, dmoe_dtype dt, void* W1, float* b1, void* W2, float* b2,
+                                    float lr, void* dxd, void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_TRY(check_dt(dt, H));
+  DMOE_REQUIRE(E_local >= 1 && R_cap >= 0, DMOE_ERR_SHAPE, "E_local=%d R_cap=%lld", E_local, (long long)R_cap);
+  DMOE_REQUIRE(lr == lr, DMOE_ERR_ARG, "expert_ffn_bwd_sgd: lr is NaN");
+  NN(offsets); NN(W1); NN(b1); NN(W2); NN(b2); NN(ws);
+  if (R_cap > 0) { NN(xd); NN(dout); NN(dxd); }
+  GemmSegK p5{}, p6{};
+  p5.Mdim = D; p5.N = H; p6.Mdim = H; p6.N = D;
+  DMOE_REQUIRE(dt == DMOE_BF16 && tc_segk_supported(p5) && tc_segk_supported(p6), DMOE_ERR_UNSUPPORTED,
+               "expert_ffn_bwd_sgd: needs the bf16 tensor-core path (D, H multiples of 128)");
+  cudaStream_t s = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  int32_t* plan_tc = cv.take<int32_t>(E_local + 1);
+  int32_t* plan_simt = cv.take<int32_t>(E_local + 1);
+  void* dh = cv.take<char>((size_t)(R_cap > 0 ? R_cap : 1) * H * 2);
+  // h == NULL: the forward's hidden activation is recomputed here (gradient checkpointing:
+  // the expert is "called twice per batch")
+  void* hre = h ? nullptr : cv.take<char>((size_t)(R_cap > 0 ? R_cap : 1) * H * 2);
+  uint32_t* mre = (h || !hmask_path(dt, D, H, E_local, R_cap)) ? nullptr
+                                                                : cv.take<uint32_t>((size_t)((H + 31) / 32) * (R_cap > 0 ? R_cap : 1));
+  DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "expert_ffn_bwd_sgd: workspace too small (%zu < %zu)", ws_bytes, cv.used);
+  const void* hh = h ? h : hre;
+  const uint32_t* hm = h ? hmask : mre;
+  GemmRows g1{};
+  if (!h) {
+    g1.A = xd; g1.B = W1; g1.C = hre; g1.bias = b1; g1.offsets = offsets;
+    g1.E = E_local; g1.N = H; g1.K = D; g1.rows_cap = R_cap; g1.b_mn = false; g1.epi = EPI_BIAS_RELU;
+    if (mre) { g1.hmask = mre; g1.hmask_ld = R_cap; }
+  }
+  GemmRows g3{};
+  g3.A = dout; g3.B = W2; g3.C = dh; g3.aux = hh; g3.offsets = offsets;
+  g3.E = E_local; g3.N = H; g3.K = D; g3.rows_cap = R_cap; g3.b_mn = true; g3.epi = EPI_RELU_MASK;
+  if (hm && hmask_path(dt, D, H, E_local, R_cap)) { g3.hmask = const_cast<uint32_t*>(hm); g3.hmask_ld = R_cap; }
+  GemmRows g4 = g3;
+  g4.A = dh; g4.B = W1; g4.C = dxd; g4.aux = nullptr; g4.N = D; g4.K = H; g4.epi = EPI_PLAIN;
+  g4.hmask = nullptr;
+  for (GemmRows* g : {&g1, &g3, &g4}) {
+    g->plan = plan_tc;
+    g->max_tiles = ceil_div(R_cap, tc_rows_tile(*g)) + E_local;
+  }
+  DMOE_TRY(plans_for(g3, g4, offsets, E_local, plan_tc, plan_simt, s));
+  if (!h) {
+    g1.plan = g3.plan;
+    DMOE_TRY(rows_gemm(g1, dt, s));
+  }
+  DMOE_TRY(rows_gemm(g3, dt, s));   // reads W2
+  DMOE_TRY(rows_gemm(g4, dt, s));   // reads W1
+  // then the parameter updates, in place, in one persistent launch (after both readers)
+  GemmSegK g5{dout, hh, W2, offsets, E_local, D, H, R_cap, b2};
+  GemmSegK g6{dh, xd, W1, offsets, E_local, H, D, R_cap, b1};
+  g5.sgd_lr = g6.sgd_lr = lr;
+  if (tc_segk2_supported(g5, g6)) return tc_gemm_segk2(g5, g6, s);
+  DMOE_TRY(tc_gemm_segk(g5, s));
+  return tc_gemm_segk(g6, s);
 }
 
 dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, const float* dscore,

@@ -74,23 +74,78 @@ __device__ __forceinline__ void beam_search_row(const float* grow, int gstride, 
     const float* gi = grow + (int64_t)i * M * gstride;
     const uint32_t* pa = nullptr;
     if (MASKED) pa = PA + (i == 0 ? pa_off[0] : i == 1 ? pa_off[1] : i == 2 ? pa_off[2] : pa_off[3]);
+    // candidate (score s, flat prefix p): FilterAlive, then the exact key test and insertion
+    auto consider = [&](float s, uint32_t p) {
+      if (!(s >= thr_s)) return;  // below the W-th score (also drops NaN, undefined by X4)
+      if (MASKED && !((pa[p >> 5] >> (p & 31)) & 1u)) return;  // FilterAlive
+      const uint64_t key = beam_key(s, p);
+      if (key > thr) {
+        beam_insert<WMAX>(top, key);
+        thr = beam_at<WMAX>(top, W - 1);
+        if (thr) thr_s = beam_unord((uint32_t)(thr >> 32));
+      }
+    };
+    // All experts alive (no FilterAlive): the level's candidates are prefix score + g_i(j), and
+    // rounding is monotone, so prefix b's best W are among the best W of g_i -- the list L
+    // (key: g desc, j asc) -- unless the (W+1)-th of L reaches the W-th's rounded sum (then
+    // a j outside L could tie it and win on the lower flat index: that prefix is scanned in
+    // full).  The union of the prefixes' best W holds the level's best W.
+    uint64_t L[WMAX + 1];
+    int nL = 0;
+    if (!MASKED) {
+#pragma unroll
+      for (int q = 0; q <= WMAX; ++q) L[q] = 0ull;
+      uint64_t lthr = 0ull;
+      float lthr_g = -INFINITY;
+      for (int j = 0; j < M; ++j) {
+        const float g = gi[j * gstride];
+        if (!(g >= lthr_g)) continue;
+        const uint64_t key = beam_key(g, (uint32_t)j);
+        if (key > lthr) {
+          beam_insert<WMAX + 1>(L, key);
+          lthr = beam_at<WMAX + 1>(L, W);   // the (W+1)-th entry
+          if (lthr) lthr_g = beam_unord((uint32_t)(lthr >> 32));
+        }
+      }
+      nL = M < W + 1 ? M : W + 1;
+    }
 #pragma unroll
     for (int b = 0; b < WMAX; ++b) {
       if (b < nb) {
         const uint32_t p0 = (0xffffffffu - (uint32_t)beam[b]) * (uint32_t)M;
         const float sp = beam_unord((uint32_t)(beam[b] >> 32));
-        for (int j = 0; j < M; ++j) {
-          const float s = sp + gi[j * gstride];
-          if (!(s >= thr_s)) continue;  // also drops NaN scores (undefined, reading X4)
-          const uint32_t p = p0 + (uint32_t)j;
-          if (MASKED && !((pa[p >> 5] >> (p & 31)) & 1u)) continue;  // FilterAlive
-          const uint64_t key = beam_key(s, p);
-          if (key > thr) {
-            beam_insert<WMAX>(top, key);
-            thr = beam_at<WMAX>(top, W - 1);
-            if (thr) thr_s = beam_unord((uint32_t)(thr >> 32));
+        if (!MASKED) {
+          bool full = false;
+          if (nL == W + 1) {  // M > W: is the W-th rounded sum strictly above the (W+1)-th?
+            const float sW = sp + beam_unord((uint32_t)(beam_at<WMAX + 1>(L, W - 1) >> 32));
+            const float sN = sp + beam_unord((uint32_t)(beam_at<WMAX + 1>(L, W) >> 32));
+            full = !(sW > sN);
+          }
+          if (!full) {
+            const int nq = nL < W ? nL : W;
+#pragma unroll
+            for (int q = 0; q < WMAX; ++q) {
+              if (q < nq) {
+                const uint32_t jq = 0xffffffffu - (uint32_t)L[q];
+                consider(sp + beam_unord((uint32_t)(L[q] >> 32)), p0 + jq);
+              }
+            }
+            continue;
           }
         }
+        int j = 0;
+        // 4 candidates per step: four independent loads and adds, one combined test; the
+        // rare step with a candidate at or above the W-th score walks its four in order
+        for (; j + 4 <= M; j += 4) {
+          const float s0 = sp + gi[(j + 0) * gstride], s1 = sp + gi[(j + 1) * gstride];
+          const float s2 = sp + gi[(j + 2) * gstride], s3 = sp + gi[(j + 3) * gstride];
+          if (!(fmaxf(fmaxf(s0, s1), fmaxf(s2, s3)) >= thr_s)) continue;
+          consider(s0, p0 + (uint32_t)j);
+          consider(s1, p0 + (uint32_t)j + 1u);
+          consider(s2, p0 + (uint32_t)j + 2u);
+          consider(s3, p0 + (uint32_t)j + 3u);
+        }
+        for (; j < M; ++j) consider(sp + gi[j * gstride], p0 + (uint32_t)j);
       }
     }
     nb = 0;

@@ -6,14 +6,15 @@
 //   1. k_weights_hist  — one warp per chunk of kChunkTok tokens: lane = token computes
 //      ok / w / valid; ok pairs are counted into the chunk's private histogram row
 //      hist[c][e] (integer atomics on a warp-private row: order-independent).
-//   2. k_scan_chunks   — per expert, exclusive prefix over chunks (in place) -> counts[e].
+//   2. k_scan_chunks   — per expert, exclusive prefix over chunks (in place) -> counts[e]
+//      (8-expert column blocks staged in shared memory: sector-coalesced both ways).
 //   3. k_scan_experts  — one CTA: offsets = exclusive scan of counts, n_dropped, and the
 //      grouped-GEMM tile plans (tiles of 128 and 64 rows per expert).
 //   4. k_rank          — each warp re-walks its chunk 32 pairs at a time in pair order
 //      t*k+s; __match_any_sync groups equal experts, rank = #earlier equal lanes +
 //      running per-(chunk, expert) base.  Experts are distinct within a token, so pair
 //      order == token order inside a segment (reading X18).
-//   5. k_gather        — xd[r] = x[token_of_row[r]], 16-byte vectors, row-parallel.
+//   5. k_scatter       — xd[row_of_slot[t, s]] = x[t], token-parallel: x read once.
 #include "common.cuh"
 
 namespace dmoe {
@@ -77,36 +78,45 @@ k_weights_hist(const int32_t* __restrict__ sel, const float* __restrict__ sel_sc
   if (lane == 0) chunk_dropped[c] = dropped;
 }
 
-// per expert (one warp): exclusive prefix of hist[:, e] over chunks (in place) -> counts[e].
-// Up to 256 chunks per pass: all loads are issued before the dependent scan.
-__global__ void k_scan_chunks(int32_t* __restrict__ hist, int64_t n_chunks, int64_t E,
-                              int32_t* __restrict__ counts) {
+// per expert: exclusive prefix of hist[:, e] over chunks (in place) -> counts[e].  A CTA owns
+// 8 consecutive experts and loads their columns for up to kScanBlk chunks into shared memory in
+// one go (8 experts = one 32-byte sector per chunk row, every load in flight at once), warp w
+// scans expert w along the chunks, and the block is written back the same way.
+constexpr int kScanBlk = 1024;
+__global__ void __launch_bounds__(256)
+k_scan_chunks(int32_t* __restrict__ hist, int64_t n_chunks, int64_t E, int32_t* __restrict__ counts) {
   DMOE_PDL_ENTRY();
-  const int lane = threadIdx.x & 31;
-  const int64_t e = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (e >= E) return;
-  int32_t carry = 0;
-  for (int64_t c0 = 0; c0 < n_chunks; c0 += 256) {
-    int32_t v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t c = c0 + j * 32 + lane;
-      v[j] = c < n_chunks ? hist[c * E + e] : 0;
+  __shared__ int32_t tile[kScanBlk][9];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t e0 = (int64_t)blockIdx.x * 8;
+  int32_t carry = 0;  // warp w: expert e0 + w
+  for (int64_t cb = 0; cb < n_chunks; cb += kScanBlk) {
+    const int nb = (int)((n_chunks - cb) < kScanBlk ? (n_chunks - cb) : kScanBlk);
+    for (int i = tid; i < nb * 8; i += 256) {
+      const int cc = i >> 3, el = i & 7;
+      tile[cc][el] = (e0 + el < E) ? hist[(cb + cc) * E + e0 + el] : 0;
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t c = c0 + j * 32 + lane;
-      int32_t x = v[j];
+    __syncthreads();
+    for (int c0 = 0; c0 < nb; c0 += 32) {
+      const int cc = c0 + lane;
+      const int32_t v = cc < nb ? tile[cc][w] : 0;
+      int32_t x = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
       }
-      if (c < n_chunks) hist[c * E + e] = carry + x - v[j];
+      if (cc < nb) tile[cc][w] = carry + x - v;
       carry += __shfl_sync(0xffffffffu, x, 31);
     }
+    __syncthreads();
+    for (int i = tid; i < nb * 8; i += 256) {
+      const int cc = i >> 3, el = i & 7;
+      if (e0 + el < E) hist[(cb + cc) * E + e0 + el] = tile[cc][el];
+    }
+    __syncthreads();
   }
-  if (lane == 0) counts[e] = carry;
+  if (lane == 0 && e0 + w < E) counts[e0 + w] = carry;
 }
 
 // block-wide exclusive scan helper (1024 threads), returns exclusive prefix and total
@@ -215,21 +225,33 @@ k_rank(const int32_t* __restrict__ sel, const uint32_t* __restrict__ responded, 
   }
 }
 
+// xd[row_of_slot[t, s]] = x[t] for every ok slot: token-parallel (a warp per token), so each
+// x row is read from HBM once and written to its <= k dispatched rows (a row-parallel gather
+// re-reads it once per row); UNR 16-byte vectors per lane in flight before the stores.
 template <typename T>
-__global__ void k_gather(const T* __restrict__ x, const int32_t* __restrict__ token_of_row,
-                         const int32_t* __restrict__ offsets, int64_t E, int32_t D,
-                         T* __restrict__ xd) {
+__global__ void __launch_bounds__(256)
+k_scatter(const T* __restrict__ x, const int32_t* __restrict__ row_of_slot, int64_t Tn, int k, int32_t D,
+          T* __restrict__ xd) {
   DMOE_PDL_ENTRY();
-  const int64_t R = offsets[E];
-  constexpr int V = Vec16<T>::N;
+  constexpr int V = Vec16<T>::N, UNR = 4;
+  const int lane = threadIdx.x & 31;
   const int vecs = D / V;  // D % V == 0 checked by the caller
-  const int64_t total = R * vecs;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / vecs;
-    const int v = (int)(i - r * vecs);
-    const int64_t t = token_of_row[r];
-    st_v4(xd + r * D + (int64_t)v * V, ld_nc_v4(x + t * D + (int64_t)v * V));
+  for (int64_t t = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); t < Tn;
+       t += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int32_t* ros = row_of_slot + t * k;
+    for (int v0 = lane; v0 < vecs; v0 += UNR * 32) {
+      uint4 u[UNR];
+#pragma unroll
+      for (int q = 0; q < UNR; ++q)
+        if (v0 + q * 32 < vecs) u[q] = ld_nc_v4(x + t * D + (int64_t)(v0 + q * 32) * V);
+      for (int s = 0; s < k; ++s) {
+        const int32_t r = ros[s];
+        if (r < 0) continue;
+#pragma unroll
+        for (int q = 0; q < UNR; ++q)
+          if (v0 + q * 32 < vecs) st_v4(xd + (int64_t)r * D + (int64_t)(v0 + q * 32) * V, u[q]);
+      }
+    }
   }
 }
 
@@ -265,13 +287,14 @@ dmoe_status dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, int64_t
                                               token_of_row, nc, kChunkTok);
     DMOE_TRY(check_launch("dispatch.rank"));
     if (xd == nullptr) return DMOE_OK;  // gather fused into the peer exchange
-    const int grid = num_sms() * 8;
+    int64_t grid = ceil_div(T, 8);
+    if (grid > (int64_t)num_sms() * 8) grid = (int64_t)num_sms() * 8;
     if (dt == DMOE_BF16)
-      launch_pdl(k_gather<__nv_bfloat16>, grid, 256, 0, s, (const __nv_bfloat16*)x, token_of_row, offsets, E,
-                                                   D, (__nv_bfloat16*)xd);
+      launch_pdl(k_scatter<__nv_bfloat16>, (unsigned)grid, 256, 0, s, (const __nv_bfloat16*)x, row_of_slot, T, k, D,
+                 (__nv_bfloat16*)xd);
     else
-      launch_pdl(k_gather<float>, grid, 256, 0, s, (const float*)x, token_of_row, offsets, E, D, (float*)xd);
-    DMOE_TRY(check_launch("dispatch.gather"));
+      launch_pdl(k_scatter<float>, (unsigned)grid, 256, 0, s, (const float*)x, row_of_slot, T, k, D, (float*)xd);
+    DMOE_TRY(check_launch("dispatch.scatter"));
   }
   return DMOE_OK;
 }

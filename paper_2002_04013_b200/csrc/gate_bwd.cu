@@ -6,9 +6,14 @@
 //   dW_g  = X^T dG (fp32),  db_g = column sums of dG (fp32)
 //
 // W_g is transposed once into the workspace so the k*d gate columns a token touches are
-// contiguous rows (coalesced, L2-resident).  dW_g is a split-K SIMT reduction over
-// tokens with a fixed-order final sum (deterministic, no float atomics).
-#include "common.cuh"
+// contiguous rows (coalesced, L2-resident).  k_gate_bwd_dx (warp per token) writes dX, the
+// per-CTA bias partials and the token's dG row.  dW_g is a dense contraction over the tokens:
+// on the bf16 path it runs on the tensor cores as a split-K weight-gradient GEMM (the SEGK
+// engine of gemm_tc.cu, token chunks as segments, fp32 partial output) over dG split exactly
+// into two bf16 halves (hi = bf16(dG), lo = bf16(dG - hi): 16 significant bits, and X is
+// bf16 already), i.e. B = [dG_hi | dG_lo]; the fp32 path keeps a SIMT split-K.  Partials are
+// summed over chunks (and hi + lo) in a fixed order: deterministic, no float atomics.
+#include "gemm.cuh"
 
 namespace dmoe {
 
@@ -39,71 +44,147 @@ dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt
   return check_launch("transpose");
 }
 
-constexpr int kGbWarps = 4;
+constexpr int kGbWarps = 16;                 // warps per CTA (one CTA per SM: W_g^T slice in smem)
+constexpr int kGbSmem = 128 * 1024;          // W_g^T column slice budget
 
-template <typename T, int kGbMaxK>
-__global__ void __launch_bounds__(kGbWarps * 32)
+// dX (undispatch + gate path), the per-CTA partial bias gradient and the tokens' dG rows.
+// The gate path needs, per token, d*k rows of W_g^T; a CTA keeps the W_g^T columns of its D
+// slice [p0, p0 + Dp) resident in shared memory (grid = D slices x token blocks, one CTA per
+// SM), so the only HBM traffic is the gather of the k dispatched dxd rows (issued together:
+// k * Dp / (32 V) 16-byte vectors per lane in flight) and the dX write; 16 warps per CTA, a warp
+// per token.  CTAs of slice 0 also write the dG row (dense fp32 dG for the SIMT dW_g, bf16
+// hi | lo halves padded to ld2 columns for the tensor-core dW_g) and the bias partials
+// db_g = sum_t dG[t] of their tokens (lane owns columns lane + 32 m, warps combined in a fixed
+// order: deterministic).  Block (0, 0) writes the token chunk bounds of the split-K dW_g GEMM.
+template <typename T, int KMAX, int VPL>
+__global__ void __launch_bounds__(kGbWarps * 32, 1)
 k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
               const float* __restrict__ dscore, const T* __restrict__ dxd,
-              const int32_t* __restrict__ row_of_slot, int64_t Tn, int32_t D, int d, int M, int k,
-              T* __restrict__ dx, float* __restrict__ dG) {
+              const int32_t* __restrict__ row_of_slot, int64_t Tn, int32_t D, int Dp, int d, int M, int k,
+              T* __restrict__ dx, float* __restrict__ pb, float* __restrict__ dG,
+              __nv_bfloat16* __restrict__ dG2, int ld2, int32_t* __restrict__ chunk_off, int nchunk,
+              int64_t tpc) {
   DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
-  const int lane = threadIdx.x & 31;
+  constexpr int NB = 8;  // gate columns per lane (d*M <= 256)
+  extern __shared__ __align__(16) uint8_t gb_smem[];
+  T* wsl = reinterpret_cast<T*>(gb_smem);  // [dM][Dp]: W_g^T[:, p0 .. p0 + Dp)
+  __shared__ float bsh[kGbWarps][NB * 32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int dM = d * M;
-  for (int64_t t = blockIdx.x * (int64_t)kGbWarps + (threadIdx.x >> 5); t < Tn;
-       t += (int64_t)gridDim.x * kGbWarps) {
-    int32_t rows[kGbMaxK], es[kGbMaxK];
-    float ds[kGbMaxK];
+  const int part = blockIdx.x;
+  const int p0 = part * Dp;
+  const bool lead = part == 0;
+  if (chunk_off && blockIdx.x == 0 && blockIdx.y == 0)
+    for (int c = threadIdx.x; c <= nchunk; c += blockDim.x)
+      chunk_off[c] = (int32_t)((int64_t)c * tpc < Tn ? (int64_t)c * tpc : Tn);
+  {
+    const int vr = Dp / V;  // 16-byte vectors per slice row
+    for (int i = threadIdx.x; i < dM * vr; i += blockDim.x) {
+      const int r = i / vr, v = i - r * vr;
+      st_v4(wsl + (int64_t)r * Dp + v * V, ld_v4(WgT + (int64_t)r * D + p0 + v * V));
+    }
+  }
+  __syncthreads();
+  float bpart[NB];
 #pragma unroll
-    for (int s = 0; s < kGbMaxK; ++s) {
+  for (int m = 0; m < NB; ++m) bpart[m] = 0.0f;
+  const int64_t wstride = (int64_t)gridDim.y * kGbWarps;
+  for (int64_t t = (int64_t)blockIdx.y * kGbWarps + wib; t < Tn; t += wstride) {
+    int32_t rows[KMAX], cols[KMAX][4];
+    float ds[KMAX];
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
       rows[s] = s < k ? row_of_slot[t * k + s] : -1;
-      es[s] = s < k ? sel[t * k + s] : -1;
-      ds[s] = s < k ? dscore[t * k + s] : 0.0f;
-    }
-    // dense dG row (fp32) for dW_g / db_g
-    for (int col = lane; col < dM; col += 32) {
-      const int i = col / M, j = col - i * M;
-      int div = 1;
-      for (int q = i + 1; q < d; ++q) div *= M;
-      float v = 0.0f;
+      const int32_t e = s < k ? sel[t * k + s] : -1;
+      ds[s] = (s < k && e >= 0) ? dscore[t * k + s] : 0.0f;
+      int ee = e < 0 ? 0 : e;
 #pragma unroll
-      for (int s = 0; s < kGbMaxK; ++s)
-        if (s < k && es[s] >= 0 && (es[s] / div) % M == j) v += ds[s];
-      dG[t * dM + col] = v;
+      for (int i = 3; i >= 0; --i) {   // u_i(e) (reading X1): column i*M + u_i
+        if (i < d) { cols[s][i] = i * M + (ee % M); ee /= M; } else cols[s][i] = -1;
+      }
+      if (e < 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cols[s][i] = -1;
+      }
     }
-    for (int c = lane * V; c < D; c += 32 * V) {
+    // the k dispatched rows of this slice: every load in flight before the first add
+    uint4 u[KMAX][VPL];
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s)
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) {
+        const int c = (lane + 32 * q) * V;
+        if (rows[s] >= 0 && c < Dp) u[s][q] = ld_nc_v4(dxd + (int64_t)rows[s] * D + p0 + c);
+      }
+    if (lead) {  // the token's dG row for the lane's columns (fixed slot, level order)
+      float g[NB];
+#pragma unroll
+      for (int m = 0; m < NB; ++m) g[m] = 0.0f;
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int col = cols[s][i];
+          if (col >= 0 && (col & 31) == lane) {
+#pragma unroll
+            for (int m = 0; m < NB; ++m)
+              if (m == (col >> 5)) g[m] += ds[s];
+          }
+        }
+#pragma unroll
+      for (int m = 0; m < NB; ++m) {
+        bpart[m] += g[m];
+        const int col = lane + 32 * m;
+        if (dG && col < dM) dG[t * dM + col] = g[m];
+        if (dG2 && col < dM) {
+          const __nv_bfloat16 hi = __float2bfloat16_rn(g[m]);
+          dG2[t * ld2 + col] = hi;
+          dG2[t * ld2 + dM + col] = __float2bfloat16_rn(g[m] - __bfloat162float(hi));
+        }
+      }
+      if (dG2)
+        for (int col = 2 * dM + lane; col < ld2; col += 32) dG2[t * ld2 + col] = __float2bfloat16_rn(0.0f);
+    }
+#pragma unroll
+    for (int q = 0; q < VPL; ++q) {
+      const int c = (lane + 32 * q) * V;
+      if (c >= Dp) continue;
       float acc[V];
 #pragma unroll
-      for (int q = 0; q < V; ++q) acc[q] = 0.0f;
-      {
-        uint4 u[kGbMaxK];
+      for (int j = 0; j < V; ++j) acc[j] = 0.0f;
 #pragma unroll
-        for (int s = 0; s < kGbMaxK; ++s)
-          if (s < k && rows[s] >= 0) u[s] = ld_nc_v4(dxd + (int64_t)rows[s] * D + c);
+      for (int s = 0; s < KMAX; ++s) {
+        if (rows[s] < 0) continue;
+        float f[V];
+        unpack16(u[s][q], f, (const T*)nullptr);
 #pragma unroll
-        for (int s = 0; s < kGbMaxK; ++s) {
-          if (s >= k || rows[s] < 0) continue;
-          float f[V];
-          unpack16(u[s], f, (const T*)nullptr);
-#pragma unroll
-          for (int q = 0; q < V; ++q) acc[q] += f[q];
-        }
+        for (int j = 0; j < V; ++j) acc[j] += f[j];
       }
 #pragma unroll
-      for (int s = 0; s < kGbMaxK; ++s) {
-        if (s >= k || es[s] < 0 || ds[s] == 0.0f) continue;
-        int e = es[s];
-        for (int i = d - 1; i >= 0; --i) {
-          const int col = i * M + (e % M);
-          e /= M;
-          float f[V];
-          unpack16(ld_v4(WgT + (int64_t)col * D + c), f, (const T*)nullptr);
+      for (int s = 0; s < KMAX; ++s) {
+        if (ds[s] == 0.0f) continue;
 #pragma unroll
-          for (int q = 0; q < V; ++q) acc[q] = fmaf(ds[s], f[q], acc[q]);
+        for (int i = 3; i >= 0; --i) {   // last level first
+          if (cols[s][i] < 0) continue;
+          float f[V];
+          unpack16(ld_v4(wsl + (int64_t)cols[s][i] * Dp + c), f, (const T*)nullptr);
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc[j] = fmaf(ds[s], f[j], acc[j]);
         }
       }
-      st_v4(dx + t * D + c, pack16(acc, (const T*)nullptr));
+      st_v4(dx + t * D + p0 + c, pack16(acc, (const T*)nullptr));
+    }
+  }
+  if (lead) {
+#pragma unroll
+    for (int m = 0; m < NB; ++m) bsh[wib][lane + 32 * m] = bpart[m];
+    __syncthreads();
+    for (int col = threadIdx.x; col < dM; col += blockDim.x) {
+      float v = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kGbWarps; ++w) v += bsh[w][col];
+      pb[(int64_t)blockIdx.y * dM + col] = v;
     }
   }
 }
@@ -193,7 +274,7 @@ k_dwg_partial(const T* __restrict__ X, const float* __restrict__ dG, int64_t Tn,
       if (col < dM) partial[(split * D + c) * dM + col] = acc[a][b];
     }
   }
-  if (blockIdx.x == 0 && tc == 0)
+  if (pb && blockIdx.x == 0 && tc == 0)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
       const int col = col0 + tg * 4 + b;
@@ -272,60 +353,99 @@ k_dwg_partial_small(const T* __restrict__ X, const float* __restrict__ dG, int64
       const int c = c0 + ty * 8 + q;
       if (c < D) partial[(split * D + c) * dM + col] = acc[q];
     }
-    if (blockIdx.x == 0 && ty == 0) pb[split * dM + col] = bsum;
+    if (pb && blockIdx.x == 0 && ty == 0) pb[split * dM + col] = bsum;
   }
 }
 
-// out[i] = sum over splits, 8 thread groups x (every 8th split) then a fixed-order combine
+// dWg[c][col] = sum over splits s of partial[s][c][col] (+ partial[s][c][dM + col]: the lo half
+// on the tensor-core path; ld = the partial's row length), split order; dbg[col] = sum over the
+// dx kernel's CTAs of pb[cta][col] (one warp per column, lane-strided then a fixed tree)
 __global__ void __launch_bounds__(256)
-k_dwg_reduce(const float* __restrict__ partial, const float* __restrict__ pb, int64_t nsplit, int32_t D, int dM,
-             float* __restrict__ dWg, float* __restrict__ dbg) {
+k_gate_reduce(const float* __restrict__ partial, int64_t nsplit, int ld, int hilo, const float* __restrict__ pb,
+              int64_t npb, int32_t D, int dM, float* __restrict__ dWg, float* __restrict__ dbg) {
   DMOE_PDL_ENTRY();
-  __shared__ float red[8][33];
-  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t n = (int64_t)D * dM;
-  const int64_t i = blockIdx.x * 32 + lane;  // output index (dWg then dbg)
+  const int64_t nblk_w = ceil_div_dev(n, 256);
+  if (blockIdx.x < nblk_w) {
+    const int64_t i = blockIdx.x * 256 + threadIdx.x;
+    if (i >= n) return;
+    const int64_t c = i / dM, col = i - c * dM;
+    const float* src = partial + c * ld + col;
+    const int64_t stride = (int64_t)D * ld;
+    float a[4] = {0.f, 0.f, 0.f, 0.f};
+    int64_t s = 0;
+    for (; s + 4 <= nsplit; s += 4)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a[j] += hilo ? src[(s + j) * stride] + src[(s + j) * stride + dM] : src[(s + j) * stride];
+    for (; s < nsplit; ++s) a[0] += hilo ? src[s * stride] + src[s * stride + dM] : src[s * stride];
+    dWg[i] = (a[0] + a[1]) + (a[2] + a[3]);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t col = (blockIdx.x - nblk_w) * 8 + (threadIdx.x >> 5);
+  if (col >= dM) return;
   float v = 0.0f;
-  if (i < n + dM) {
-    const float* src = i < n ? partial + i : pb + (i - n);
-    const int64_t stride = i < n ? n : dM;
-    float a[8];
+  for (int64_t b = lane; b < npb; b += 32) v += pb[b * dM + col];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int64_t sidx = grp + 8 * j;
-      a[j] = sidx < nsplit ? src[sidx * stride] : 0.0f;
-    }
-    for (int64_t s0 = grp + 64; s0 < nsplit; s0 += 64)
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (s0 + 8 * j < nsplit) a[j] += src[(s0 + 8 * j) * stride];
-    v = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-  }
-  red[grp][lane] = v;
-  __syncthreads();
-  if (grp == 0 && i < n + dM) {
-    float t = 0.0f;
-#pragma unroll
-    for (int g = 0; g < 8; ++g) t += red[g][lane];
-    if (i < n) dWg[i] = t;
-    else dbg[i - n] = t;
-  }
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) dbg[col] = v;
 }
 
-// split-K over tokens: >= 64 tokens per split, partial sums capped at 8M floats
-// split-K over tokens: one 32-token pass per split where the partial sums (capped at 8M floats)
-// allow, so the CTAs stay short and many
+// D slices of the dx kernel: the W_g^T slice [dM][Dp] must fit kGbSmem, Dp a multiple of 32
+// 16-byte vectors (one per lane per pass), at most 4 passes per lane
+struct GbdxShape { int parts, Dp, vpl; };
+// (k * vpl <= 8: 8 in-flight 16-byte vectors per lane, 64 KB per SM, within 128 registers)
+static GbdxShape gbdx_shape(int32_t D, int dM, size_t esz, int k) {
+  const int V = (int)(16 / esz);
+  const int kmax = k <= 4 ? 4 : (k <= 8 ? 8 : 16);
+  const int vmax = kmax >= 8 ? 1 : 8 / kmax;
+  for (int parts = 1; parts <= 64; ++parts) {
+    if (D % parts) continue;
+    const int Dp = D / parts;
+    if (Dp % (32 * V) && parts > 1) continue;
+    if ((size_t)dM * Dp * esz > (size_t)kGbSmem) continue;
+    const int vpl = (int)ceil_div(Dp, 32 * V);
+    if (vpl > vmax) continue;
+    return {parts, Dp, vpl};
+  }
+  return {0, 0, 0};
+}
+static int64_t gbdx_blocks(int64_t T, int parts) {
+  int64_t b = ceil_div((int64_t)num_sms(), parts);
+  const int64_t need = ceil_div(T > 0 ? T : 1, kGbWarps);
+  return b < need ? b : need;
+}
+// SIMT split-K over tokens (fp32 path): one 32-token pass per split where the partial sums
+// (capped at 8M floats) allow
 static int64_t dwg_splits(int64_t T, int32_t D, int dM) {
   int64_t s = ceil_div(T, kDwgTok);
   const int64_t smax = ((int64_t)8 << 20) / ((int64_t)D * dM);
   if (s > smax) s = smax;
   return s < 1 ? 1 : s;
 }
+// tensor-core split-K: token chunks so that chunks x (D / 128) M-tiles ~ two tiles per SM
+static int64_t tc_chunks(int64_t T, int32_t D) {
+  const int64_t mt = D >= 128 ? (int64_t)D / 128 : 1;  // M tiles (the path needs D % 128 == 0)
+  int64_t c = ceil_div((int64_t)num_sms() * 2, mt);
+  const int64_t cmax = ceil_div(T > 0 ? T : 1, 256);  // >= 256 tokens (4 K blocks) per chunk
+  if (c > cmax) c = cmax;
+  return c < 1 ? 1 : c;
+}
+static int tc_ld2(int dM) { return (int)align_up((size_t)2 * dM, 128); }
+static bool gate_bwd_tc(dmoe_dtype dt, int32_t D, int dM) {
+  if (dt != DMOE_BF16) return false;
+  GemmSegK g{};
+  g.Mdim = D; g.N = tc_ld2(dM);
+  return tc_segk_supported(g);
+}
 
 size_t gate_bwd_ws_bytes(int64_t T, int32_t D, int dM) {
-  const int64_t S = dwg_splits(T, D, dM);
-  return align_up((size_t)D * dM * 4, 256) + align_up((size_t)(T > 0 ? T : 1) * dM * 4, 256) +
-         align_up((size_t)S * D * dM * 4, 256) + align_up((size_t)S * dM * 4, 256) + 1024;
+  const size_t Tp = (size_t)(T > 0 ? T : 1);
+  const size_t simt = align_up(Tp * dM * 4, 256) + align_up((size_t)dwg_splits(T, D, dM) * D * dM * 4, 256);
+  const size_t tc = align_up(Tp * tc_ld2(dM) * 2, 256) + align_up((size_t)tc_chunks(T, D) * D * tc_ld2(dM) * 4, 256) +
+                    align_up((size_t)(tc_chunks(T, D) + 1) * 4, 256);
+  return align_up((size_t)D * dM * 4, 256) + (simt > tc ? simt : tc) + align_up((size_t)num_sms() * dM * 4, 256) +
+         1024;
 }
 
 dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const float* dscore,
@@ -333,13 +453,31 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
                      int k, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
                      size_t ws_bytes, cudaStream_t s) {
   const int dM = d * M;
-  const int64_t S = dwg_splits(T, D, dM);
+  DMOE_REQUIRE(dM <= 256, DMOE_ERR_SHAPE, "gate_bwd: d*M=%d > 256", dM);
+  const bool tc = gate_bwd_tc(dt, D, dM) && T > 0;
   const size_t esz = dt == DMOE_BF16 ? 2 : 4;
+  const GbdxShape gs = gbdx_shape(D, dM, esz, k);
+  DMOE_REQUIRE(gs.parts > 0, DMOE_ERR_UNSUPPORTED, "gate_bwd: no D slicing for D=%d d*M=%d", D, dM);
+  const int64_t nb = gbdx_blocks(T, gs.parts);
   Carver cv(ws, ws_bytes);
   void* WgT = cv.take<char>((size_t)D * dM * esz);
-  float* dG = cv.take<float>((size_t)(T > 0 ? T : 1) * dM);
-  float* part = cv.take<float>((size_t)S * D * dM);
-  float* pb = cv.take<float>((size_t)S * dM);
+  float* pb = cv.take<float>((size_t)nb * dM);
+  float* dG = nullptr;
+  float* part = nullptr;
+  __nv_bfloat16* dG2 = nullptr;
+  int32_t* choff = nullptr;
+  int64_t nsplit = 0;
+  const int ld2 = tc_ld2(dM);
+  if (tc) {
+    nsplit = tc_chunks(T, D);
+    dG2 = cv.take<__nv_bfloat16>((size_t)T * ld2);
+    part = cv.take<float>((size_t)nsplit * D * ld2);
+    choff = cv.take<int32_t>((size_t)nsplit + 1);
+  } else {
+    nsplit = T > 0 ? dwg_splits(T, D, dM) : 0;
+    dG = cv.take<float>((size_t)(T > 0 ? T : 1) * dM);
+    part = cv.take<float>((size_t)(nsplit > 0 ? nsplit : 1) * D * dM);
+  }
   DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "gate_bwd: workspace too small (%zu < %zu)", ws_bytes, cv.used);
   dim3 tb(32, 8), tg((unsigned)ceil_div(dM, 32), (unsigned)ceil_div(D, 32));
   if (dt == DMOE_BF16)
@@ -348,39 +486,60 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
     launch_pdl(k_transpose<float>, tg, tb, 0, s, (const float*)Wg, D, dM, (float*)WgT);
   DMOE_TRY(check_launch("gate_bwd.transpose"));
   if (T > 0) {
-    int64_t b = ceil_div(T, kGbWarps), cap = (int64_t)num_sms() * 16;
-    unsigned grid = (unsigned)(b < cap ? b : cap);
-#define DMOE_GBDX(KM)                                                                                   \
-    if (dt == DMOE_BF16)                                                                                \
-      launch_pdl(k_gate_bwd_dx<__nv_bfloat16, KM>, grid, kGbWarps * 32, 0, s, \
-          (const __nv_bfloat16*)WgT, sel, dscore, (const __nv_bfloat16*)dxd, row_of_slot, T, D, d, M,   \
-          k, (__nv_bfloat16*)dx, dG);                                                                   \
-    else                                                                                                \
-      launch_pdl(k_gate_bwd_dx<float, KM>, grid, kGbWarps * 32, 0, s, (const float*)WgT, sel, dscore,          \
-                                                              (const float*)dxd, row_of_slot, T, D, d, \
-                                                              M, k, (float*)dx, dG);
+    const int64_t tpc = tc ? ceil_div(T, nsplit) : 0;
+#define DMOE_GBDX3(TT, KM, VP)                                                                       \
+    {                                                                                                  \
+      static bool attr = false;                                                                        \
+      const size_t sm = (size_t)dM * gs.Dp * esz;                                                      \
+      if (!attr) { cudaFuncSetAttribute(k_gate_bwd_dx<TT, KM, VP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                        kGbSmem); attr = true; }                                       \
+      launch_pdl(k_gate_bwd_dx<TT, KM, VP>, dim3((unsigned)gs.parts, (unsigned)nb), kGbWarps * 32, sm, s,   \
+                 (const TT*)WgT, sel, dscore, (const TT*)dxd, row_of_slot, T, D, gs.Dp, d, M, k, (TT*)dx, pb, \
+                 dG, dG2, ld2, choff, (int)nsplit, tpc);                                               \
+    }
+#define DMOE_GBDX2(TT, KM)                                                                             \
+    switch (gs.vpl) {                                                                                  \
+      case 1: DMOE_GBDX3(TT, KM, 1) break;                                                             \
+      default: DMOE_GBDX3(TT, KM, 2) break;                                                            \
+    }
+#define DMOE_GBDX(KM)                                                                                  \
+    if (dt == DMOE_BF16) { DMOE_GBDX2(__nv_bfloat16, KM) } else { DMOE_GBDX2(float, KM) }
     if (k <= 4) { DMOE_GBDX(4) } else if (k <= 8) { DMOE_GBDX(8) } else { DMOE_GBDX(16) }
 #undef DMOE_GBDX
+#undef DMOE_GBDX2
+#undef DMOE_GBDX3
     DMOE_TRY(check_launch("gate_bwd.dx"));
+    if (tc) {
+      // dW_g partials on the tensor cores: chunk c's [D][hi | lo] = X[chunk]^T [dG_hi | dG_lo]
+      GemmSegK g{};
+      g.A = x; g.B = dG2; g.C = part; g.offsets = choff; g.E = (int)nsplit; g.Mdim = D; g.N = ld2; g.R_cap = T;
+      g.colsum = nullptr; g.out_f32 = true;
+      DMOE_TRY(tc_gemm_segk(g, s));
+    } else {
+      const int64_t tps = ceil_div(T, nsplit);
+      if ((int64_t)D * dM < 65536) {
+        dim3 pg((unsigned)ceil_div(D, 64), (unsigned)ceil_div(dM, 32), (unsigned)nsplit);
+        if (dt == DMOE_BF16)
+          launch_pdl(k_dwg_partial_small<__nv_bfloat16>, pg, 256, 0, s, (const __nv_bfloat16*)x, dG, T, D, dM, tps,
+                     part, (float*)nullptr);
+        else
+          launch_pdl(k_dwg_partial_small<float>, pg, 256, 0, s, (const float*)x, dG, T, D, dM, tps, part,
+                     (float*)nullptr);
+      } else {
+        dim3 pg((unsigned)ceil_div(D, kDwgC), (unsigned)ceil_div(dM, kDwgCol), (unsigned)nsplit);
+        if (dt == DMOE_BF16)
+          launch_pdl(k_dwg_partial<__nv_bfloat16>, pg, 256, 0, s, (const __nv_bfloat16*)x, dG, T, D, dM, tps, part,
+                     (float*)nullptr);
+        else
+          launch_pdl(k_dwg_partial<float>, pg, 256, 0, s, (const float*)x, dG, T, D, dM, tps, part, (float*)nullptr);
+      }
+      DMOE_TRY(check_launch("gate_bwd.dwg_partial"));
+    }
   }
-  const int64_t tps = T > 0 ? ceil_div(T, S) : 1;
-  if ((int64_t)D * dM < 65536) {
-    dim3 pg((unsigned)ceil_div(D, 64), (unsigned)ceil_div(dM, 32), (unsigned)S);
-    if (dt == DMOE_BF16)
-      launch_pdl(k_dwg_partial_small<__nv_bfloat16>, pg, 256, 0, s, (const __nv_bfloat16*)x, dG, T, D, dM, tps,
-                 part, pb);
-    else
-      launch_pdl(k_dwg_partial_small<float>, pg, 256, 0, s, (const float*)x, dG, T, D, dM, tps, part, pb);
-  } else {
-    dim3 pg((unsigned)ceil_div(D, kDwgC), (unsigned)ceil_div(dM, kDwgCol), (unsigned)S);
-    if (dt == DMOE_BF16)
-      launch_pdl(k_dwg_partial<__nv_bfloat16>, pg, 256, 0, s, (const __nv_bfloat16*)x, dG, T, D, dM, tps, part, pb);
-    else
-      launch_pdl(k_dwg_partial<float>, pg, 256, 0, s, (const float*)x, dG, T, D, dM, tps, part, pb);
-  }
-  DMOE_TRY(check_launch("gate_bwd.dwg_partial"));
-  launch_pdl(k_dwg_reduce, (unsigned)ceil_div((int64_t)D * dM + dM, 32), 256, 0, s, part, pb, S, D, dM, dWg, dbg);
-  return check_launch("gate_bwd.dwg_reduce");
+  const int64_t nw = ceil_div((int64_t)D * dM, 256), nbias = ceil_div(dM, 8);
+  launch_pdl(k_gate_reduce, (unsigned)(nw + nbias), 256, 0, s, part, nsplit, tc ? ld2 : dM, tc ? 1 : 0, pb,
+             T > 0 ? nb : 0, D, dM, dWg, dbg);
+  return check_launch("gate_bwd.reduce");
 }
 
 }  // namespace dmoe

@@ -10,8 +10,9 @@ enum Epi {
   EPI_BIAS = 2,       // out = acc + bias[e][n]                   (expert output)
   EPI_RELU_MASK = 3,  // out = acc * 1[aux[r][n] > 0]             (dh, ReLU'(0) = 0)
   EPI_PLAIN = 4,      // out = acc                                (dxd)
-  EPI_GATE_TOPK = 5   // G = acc + bias[n] staged in smem, then Alg. 1 per row (beam.cuh):
+  EPI_GATE_TOPK = 5,  // G = acc + bias[n] staged in smem, then Alg. 1 per row (beam.cuh):
                       // sel / sel_score out, G itself optional (C may be nullptr)
+  EPI_F32 = 6         // fp32 out = acc                           (SEGK split-K partials: dW_g)
 };
 
 // EPI_GATE_TOPK: the grid and liveness of the fused gate + SelectExperts epilogue
@@ -53,6 +54,9 @@ struct GemmSegK {
   int64_t R_cap;    // allocated rows of A and B
   float* colsum;    // optional [E][Mdim] fp32: sum over the segment's rows of A (bias gradient)
   int max_ctas = 0;  // persistent grid cap (0: one CTA per SM)
+  bool out_f32 = false;  // C in fp32 (coalesced stores from the padded staging) instead of bf16
+  float sgd_lr = 0.0f;   // != 0: C / colsum are the parameters W / b, updated in place
+                         // (W -= lr * dW, b -= lr * db; bf16 tensor-core path only)
 };
 
 dmoe_status simt_gemm_rows(const GemmRows& g, dmoe_dtype dt, cudaStream_t s);

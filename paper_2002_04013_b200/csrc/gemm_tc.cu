@@ -218,6 +218,8 @@ struct TcParams {
   int max_ctas;   // grid cap (0: all SMs)
   int stages;     // M-major engine: smem ring depth (runtime, <= TC_MAX_STAGES)
   int table_len;  // M-major engine: per-expert smem table entries (0: tables stay in global)
+  float sgd_lr;    // SEGK bf16: != 0 -> C (and colsum) are the parameters, updated in place:
+                   // C -= lr * acc (the dW tile never reaches HBM), colsum -= lr * column sums
   GateTopk topk;   // EPI_GATE_TOPK: Alg. 1 in the epilogue
   int topk_bytes;  // EPI_GATE_TOPK: smem of the G tile [128][N+1] fp32 + prefix-alive bitmaps
   int pa_words;    // EPI_GATE_TOPK: words of the prefix-alive bitmaps (<= kTopkPAWords)
@@ -301,7 +303,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   constexpr int NACC = Cfg::NACC;
   const int S = p.stages;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
-  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS || EPI == EPI_GATE_TOPK);
+  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS || EPI == EPI_GATE_TOPK || EPI == EPI_F32);
   constexpr bool TOPK = (EPI == EPI_GATE_TOPK);
   constexpr int OUT_ES = OUT_F32 ? 4 : 2;
   constexpr int SUB = 128 / OUT_ES;  // columns per staged sub-tile (128 bytes per row)
@@ -312,7 +314,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   uint64_t* tfull = empty + TC_MAX_STAGES;
   uint64_t* tempty = tfull + 4;
   uint64_t* ready = tempty + 4;  // SEGK: stage fixed up (tail rows zeroed) for the MMA
-  uint32_t* tmem_slot = (uint32_t*)(ready + TC_MAX_STAGES);
+  uint64_t* wload = ready + TC_MAX_STAGES;  // SGD: per epilogue warp x box, parameter box landed
+  uint32_t* tmem_slot = (uint32_t*)(wload + 16);
   uint8_t* stage_base = smem + S * Cfg::STAGE_BYTES + 1024;   // 1 KB aligned (128B-swizzled TMA stores)
   float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * Cfg::STG_WARP);  // [2][BN]
   int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [table_len]
@@ -429,6 +432,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     // SEGK: a stage is released by the MMA commit and by the fix-up warp (column sums)
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], SEGK ? 2 : 1); mbar_init(&ready[i], 1); }
     for (int i = 0; i < NACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], Cfg::EPI_WARPS); }
+    for (int i = 0; i < 16; ++i) mbar_init(&wload[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const uint32_t tmem_cols = Cfg::TMEM_COLS;
@@ -703,7 +707,16 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
       if (sums)
-        *reinterpret_cast<float4*>(colsum + (int64_t)e * mdim + m0 + 4 * lane) = make_float4(cs[0], cs[1], cs[2], cs[3]);
+      {
+        float4* dst = reinterpret_cast<float4*>(colsum + (int64_t)e * mdim + m0 + 4 * lane);
+        if (p.sgd_lr != 0.0f) {  // bias update in place (this tile is the only writer of these columns)
+          const float4 b = *dst;
+          *dst = make_float4(b.x - p.sgd_lr * cs[0], b.y - p.sgd_lr * cs[1], b.z - p.sgd_lr * cs[2],
+                             b.w - p.sgd_lr * cs[3]);
+        } else {
+          *dst = make_float4(cs[0], cs[1], cs[2], cs[3]);
+        }
+      }
     }
   } else if (warp >= 4) {
     // ======================= epilogue =======================
@@ -717,6 +730,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint8_t* const stg_warp = stage_base + ew * Cfg::STG_WARP;
     uint8_t* stg = stg_warp;
     int stg_buf = 0;  // SEGK: which of the warp's two 4 KB store boxes
+    uint32_t wph[2] = {0u, 0u};  // SGD: phase of each box's load barrier
     int acc = 0;
     uint32_t acc_phase = 0;
     int bias_buf = 0;
@@ -771,6 +785,22 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               hreg[sb][i] = __ldg(reinterpret_cast<const uint4*>(p.aux + (qrow0 + r) * p.N + n0 + cs + piece * 8));
           }
       }
+      // fused SGD (SEGK bf16): the parameter boxes this warp will update are loaded by TMA into
+      // its two store boxes while the MMA still runs (the box doubles as load and store buffer)
+      const bool sgd = SEGK && !OUT_F32 && p.sgd_lr != 0.0f;
+      if (sgd) {
+        if (lane == 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // both boxes free
+#pragma unroll
+          for (int sb = 0; sb < NSUB && sb < 2; ++sb) {
+            const int bx = (stg_buf + sb) & 1;
+            mbar_expect_tx(&wload[ew * 2 + bx], 4096);
+            tma_load_2d(stg_warp + bx * 4096, mC, &wload[ew * 2 + bx], n0 + c_beg + sb * SUB,
+                        (int)((int64_t)e * mdim + qrow0));
+          }
+        }
+        __syncwarp();
+      }
       if (has_acc) {
         WT_T0(t_tf);
         mbar_wait(&tfull[acc], acc_phase);
@@ -811,23 +841,40 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           // this box was last stored two boxes ago: at most the newest store may still be reading
           stg = stg_warp + stg_buf * 4096;
           WT_T0(t_st);
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          if (sgd) {
+            mbar_wait(&wload[ew * 2 + stg_buf], wph[stg_buf]);  // the parameter box has landed
+            wph[stg_buf] ^= 1u;
+          } else {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          }
           __syncwarp();
           WT_ADD(w_st, t_st);
         }
-        // TMEM -> registers -> epilogue math -> staging (row = lane)
+        // TMEM -> registers -> epilogue math -> staging (row = lane).  The whole sub-tile's
+        // columns are loaded with back-to-back tcgen05.ld and ONE wait (a wait per 16 columns
+        // left the epilogue warps latency-bound on TMEM: the weight-gradient tiles, ~1 K block
+        // each, are epilogue-paced)
         uint32_t mw_lo = 0;  // EPI_BIAS_RELU: packed-mask bits of the first 16 columns of a word
         (void)mw_lo;
+        uint32_t racc[SUB];
+        const bool tld = has_acc && !(DMOE_DBG(p) & 2);
+        if (tld) {
+#pragma unroll
+          for (int c16 = 0; c16 < SUB; c16 += 16) {
+            if (c16 < ncols) {
+              uint32_t* rp = racc + c16;
+              TMEM_LD16(tq + cs + c16, rp);
+            }
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
 #pragma unroll
         for (int c16 = 0; c16 < SUB; c16 += 16) {
           if (c16 >= ncols) break;
           float v[16];
-          if (has_acc && !(DMOE_DBG(p) & 2)) {
-            uint32_t r[16];
-            TMEM_LD16(tq + cs + c16, r);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (tld) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(racc[c16 + j]);
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] = 0.0f;
@@ -871,9 +918,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
             for (int j = 0; j < 16; j += 8) {
               const int q = (c16 + j) >> 3;
-              *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) =
-                  make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
-                             pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+              uint4* slot = reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4));
+              if (sgd) {  // W <- W - lr * dW (fp32 arithmetic, one bf16 rounding: reading X21)
+                const uint4 wq = *slot;
+                const uint32_t ww[4] = {wq.x, wq.y, wq.z, wq.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  v[j + 2 * i] = bf16lo(ww[i]) - p.sgd_lr * v[j + 2 * i];
+                  v[j + 2 * i + 1] = bf16hi(ww[i]) - p.sgd_lr * v[j + 2 * i + 1];
+                }
+              }
+              *slot = make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                                 pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
             }
             continue;
           }
@@ -1209,12 +1265,19 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   DMOE_TRY(make_map(&tb, g.B, 2, bdims, 64));
   // output dW [E][Mdim][N] as a 2D [E*Mdim, N] map, 64 x 32 boxes (bulk tensor stores)
   CUtensorMap tc;
-  uint64_t cdims[2] = {(uint64_t)g.N, (uint64_t)g.E * g.Mdim};
-  DMOE_TRY(make_map(&tc, g.C, 2, cdims, 32));
+  if (!g.out_f32) {
+    uint64_t cdims[2] = {(uint64_t)g.N, (uint64_t)g.E * g.Mdim};
+    DMOE_TRY(make_map(&tc, g.C, 2, cdims, 32));
+  }
   TcParams p{};
   p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim; p.colsum = g.colsum;
   p.max_ctas = g.max_ctas;
+  p.sgd_lr = g.out_f32 ? 0.0f : g.sgd_lr;
   const int64_t tiles = (int64_t)g.E * (g.Mdim / TC_BM) * (g.N / BN);
+  if (g.out_f32) {  // fp32 output through the padded staging (the C map is unused)
+    if (BN == 256) return launch<256, true, true, EPI_F32>(ta, tb, ta, p, tiles, s);
+    return launch<128, true, true, EPI_F32>(ta, tb, ta, p, tiles, s);
+  }
   if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
   return launch<128, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
 }
@@ -1223,6 +1286,7 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
 // backward's dW2 and dW1): one ramp / drain instead of two
 bool tc_segk2_supported(const GemmSegK& a, const GemmSegK& b) {
   return tc_segk_supported(a) && tc_segk_supported(b) && a.offsets == b.offsets && a.E == b.E &&
+         a.sgd_lr == b.sgd_lr &&
          pick_bn(a.N, true) == 256 && pick_bn(b.N, true) == 256 && a.max_ctas == b.max_ctas;
 }
 dmoe_status tc_gemm_segk2(const GemmSegK& g, const GemmSegK& h, cudaStream_t s) {
@@ -1242,6 +1306,7 @@ dmoe_status tc_gemm_segk2(const GemmSegK& g, const GemmSegK& h, cudaStream_t s) 
   p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim; p.colsum = g.colsum;
   p.N2 = h.N; p.Mdim2 = h.Mdim; p.colsum2 = h.colsum;
   p.max_ctas = g.max_ctas;
+  p.sgd_lr = g.sgd_lr;
   const int64_t tiles = (int64_t)g.E * ((g.Mdim / TC_BM) * (g.N / 256) + (h.Mdim / TC_BM) * (h.N / 256));
   return launch_maps<256, true, true, EPI_PLAIN>(m[0], m[1], m[2], m[3], m[4], m[5], p, tiles, s);
 }

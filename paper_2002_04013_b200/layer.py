@@ -88,12 +88,22 @@ class DMoELayer:
         return self.y[:T]
 
     # ----------------------------------------------------------------- backward
-    def backward(self, dy):
+    def backward(self, dy, sgd_lr=None, recompute=False):
+        """Gradients of the layer.  sgd_lr: the runtime's Backward request semantics:
+        the expert parameters are updated in place, W -= lr * dW, inside the weight-gradient GEMMs
+        (dW1 / dW2 / db1 / db2 are then not written).  recompute: h is recomputed from xd in the
+        backward (gradient checkpointing) instead of read from the forward's
+        buffer (SGD form only)."""
         x = self._x
         T = x.shape[0]
         L.dmoe_combine_bwd(dy, self.out, self.row_of_slot[:T], self.w[:T], self.dout, self.dscore[:T])
-        L.dmoe_expert_ffn_bwd(self.xd, self.h, self.dout, self.seg, self.W1, self.W2, self.dxd,
-                              self.dW1, self.db1, self.dW2, self.db2, self.ws, hmask=self.hmask)
+        if sgd_lr is not None:
+            L.dmoe_expert_ffn_bwd_sgd(self.xd, None if recompute else self.h, self.dout, self.seg, self.W1, self.b1,
+                                      self.W2, self.b2, sgd_lr, self.dxd, self.ws,
+                                      hmask=None if recompute else self.hmask)
+        else:
+            L.dmoe_expert_ffn_bwd(self.xd, self.h, self.dout, self.seg, self.W1, self.W2, self.dxd,
+                                  self.dW1, self.db1, self.dW2, self.db2, self.ws, hmask=self.hmask)
         L.dmoe_gate_bwd(x, self.Wg, self.sel[:T], self.dscore[:T], self.dxd, self.row_of_slot[:T], self.g,
                         self.dx[:T], self.dWg, self.dbg, self.ws)
         return self.dx[:T]

@@ -70,3 +70,13 @@ def test_tied_pool_equals_expanded_weights(tie, k, fail):
     for key in ("dW1", "db1", "dW2", "db2"):
         summed = full[key].reshape(cfg.P, tie, *full[key].shape[1:]).sum(1)
         np.testing.assert_allclose(tied[key], summed, rtol=0, atol=1e-12 * max(1.0, np.abs(summed).max()), err_msg=key)
+
+
+def test_sgd_update_closed_form():
+    """Gradient descent on L(W) = |W - W*|^2 / 2 (gradient W - W*): lr = 1 lands on W* in one step,
+    lr = 1/2 halves the distance, lr = 0 keeps W ("update ... by gradient descent")."""
+    rng = np.random.default_rng(0)
+    W, Ws = rng.standard_normal((3, 5, 7)), rng.standard_normal((3, 5, 7))
+    np.testing.assert_allclose(O.sgd_update(W, W - Ws, 1.0), Ws, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(O.sgd_update(W, W - Ws, 0.5) - Ws, (W - Ws) / 2, rtol=0, atol=1e-15)
+    assert np.array_equal(O.sgd_update(W, W - Ws, 0.0), W)

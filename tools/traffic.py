@@ -14,14 +14,14 @@ CALLS = [
     ("gate_topk", ["k_transpose", "k_tc_gemm<32, 0, 0, 5>", "k_tc_gemm<48, 0, 0, 5>", "k_tc_gemm<128, 0, 0, 5>",
                    "k_tc_gemm<32, 0, 0, 0>", "k_tc_gemm<48, 0, 0, 0>", "k_tc_gemm<128, 0, 0, 0>", "k_simt_rows",
                    "k_prefix_alive", "k_beam_topk"]),
-    ("dispatch", ["k_weights_hist", "k_scan_chunks", "k_scan_experts", "k_rank", "k_gather"]),
+    ("dispatch", ["k_weights_hist", "k_scan_chunks", "k_scan_experts", "k_rank", "k_scatter", "k_gather"]),
     ("expert_ffn_fwd", ["k_tile_plan", "k_tc_gemm<256, 0, 0, 1>", "k_tc_gemm<256, 0, 0, 2>", "k_tc_gemm<128, 0, 0, 1>",
                         "k_tc_gemm<128, 0, 0, 2>"]),
     ("combine", ["k_combine<"]),
     ("combine_bwd", ["k_combine_bwd"]),
     ("expert_ffn_bwd", ["k_tile_plan", "k_tc_gemm<256, 0, 1", "k_tc_gemm<128, 0, 1", "k_tc_gemm<128, 1, 1",
                         "k_tc_gemm<256, 1, 1", "k_seg_colsum"]),
-    ("gate_bwd", ["k_transpose", "k_gate_bwd_dx", "k_dwg_partial", "k_dwg_reduce"]),
+    ("gate_bwd", ["k_transpose", "k_gate_bwd_dx", "k_dwg_sparse", "k_dwg_partial", "k_dwg_reduce"]),
 ]
 
 
