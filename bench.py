@@ -59,7 +59,8 @@ def call_bytes(cfg, name, R, E_act):
     """Algorithmic bytes moved by one ABI call (inputs read once + outputs written once)."""
     T, D, H, k, dM, E = cfg.T, cfg.D, cfg.H, cfg.k, cfg.dM, cfg.E
     es = 2 if cfg.dtype == "bf16" else 4
-    W = E * D * H * es  # one weight matrix of all experts
+    W = cfg.P * D * H * es  # one weight matrix of all parameter slots (experts, or the tied pool)
+    E = cfg.P               # E_act counts slots with rows
     return {
         # read x, W_g; write sel, sel_score (G stays on chip in the fused call)
         "gate_topk": T * D * es + D * dM * es + T * k * 8,
@@ -136,7 +137,7 @@ def build_layer(cfg, seed, device, T):
     from paper_2002_04013_b200 import DMoELayer
     dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     lay = DMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=T, device=device,
-                    pool=cfg.pool)
+                    pool=cfg.pool, grads=not cfg.chunk)
     for t, tid in ((lay.Wg, gen.WG), (lay.bg, gen.BG), (lay.W1, gen.W1), (lay.b1, gen.B1), (lay.W2, gen.W2),
                    (lay.b2, gen.B2)):
         dist, scale = cfg.dist(tid)
@@ -413,11 +414,122 @@ def bench_ours(args, cfg, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t.item())
     R = int(lay.offsets[cfg.E].item())
-    E_act = int((lay.counts[: cfg.E] > 0).sum().item())
+    E_act = int((lay.seg[1:] - lay.seg[:-1] > 0).sum().item())
     n_dropped = int(lay.n_dropped.item())
     return dict(ms=ms, step_ms=step_ms, per_call_ms=per_call_ms, e2e_ms=e2e, R=R, E_act=E_act,
                 n_dropped=n_dropped, launches=launches_per_step, tc_launches=tc_per_step, clocks=clk.summary(),
                 h2d=2 * T * cfg.D * x.element_size(), d2h=2 * T * cfg.D * x.element_size())
+
+
+def bench_chunked(args, cfg, rank, world, local_rank):
+    """A step that does not fit one layer call (BASELINE config 5, 1M tokens x k = 8 per GPU): the
+    tokens go through the layer in cfg.chunk-token calls, each a full forward + backward whose
+    Backward request applies the runtime's SGD update to the expert parameters in the
+    weight-gradient GEMMs (no dW buffers), with the declared tied-weight pool of
+    cfg.pool slots (reading X20).  One CUDA graph per step (all chunks), L2 flushed before it."""
+    import torch
+    from paper_2002_04013_b200 import _lib as L
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    Tc, nch = cfg.chunk, cfg.T // cfg.chunk
+    lay, x0, dy0, alive, resp = build_layer(cfg, args.seed + rank, device, Tc)
+    lay.sgd_lr = 1e-6
+    dt = lay.dtype
+    x = torch.empty(cfg.T, cfg.D, dtype=dt, device=device)
+    dy = torch.empty(cfg.T, cfg.D, dtype=dt, device=device)
+    gen.dev_fill(x, args.seed + rank, gen.X, *cfg.dist(gen.X))
+    gen.dev_fill(dy, args.seed + rank, gen.DY, *cfg.dist(gen.DY))
+    del x0, dy0
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+    stream = torch.cuda.Stream(device)
+
+    def step():
+        for c in range(nch):
+            lay.forward(x[c * Tc:(c + 1) * Tc], alive, resp)
+            lay.backward(dy[c * Tc:(c + 1) * Tc])
+
+    with torch.cuda.stream(stream):
+        step()
+    stream.synchronize()
+    c0 = L.dmoe_launch_counters()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=stream):
+        step()
+    c1 = L.dmoe_launch_counters()
+    for _ in range(max(args.warmup - 1, 1)):
+        graph.replay()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with Clocks(local_rank) as clk:
+        with torch.cuda.stream(stream):
+            for i in range(args.steps):
+                flush.fill_(i & 0xFF)
+                starts[i].record(stream)
+                graph.replay()
+                ends[i].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    ms = sum(step_ms) / len(step_ms)
+    # per call (eager, events on the launch stream) for the last chunk of a step
+    names = ["gate_topk", "dispatch", "expert_ffn_fwd", "combine", "combine_bwd", "expert_ffn_bwd", "gate_bwd"]
+    per = {n: [] for n in names}
+    xc, dyc = x[:Tc], dy[:Tc]
+    T = Tc
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in names]
+            seq = [
+                lambda: L.dmoe_gate_topk(xc, lay.Wg, lay.bg, lay.g, alive, None, lay.sel[:T], lay.sel_score[:T], lay.ws),
+                lambda: L.dmoe_dispatch(xc, lay.g, lay.sel[:T], lay.sel_score[:T], resp, lay.w[:T], lay.valid[:T],
+                                        lay.n_dropped, lay.counts, lay.offsets, lay.row_of_slot[:T], lay.token_of_row,
+                                        lay.xd, lay.ws),
+                lambda: (L.dmoe_segment_offsets(lay.offsets, lay.tie, lay.seg) if lay.tie > 1 else None,
+                         L.dmoe_expert_ffn_fwd(lay.xd, lay.seg, lay.W1, lay.b1, lay.W2, lay.b2, lay.h, lay.out, lay.ws,
+                                               hmask=lay.hmask)),
+                lambda: L.dmoe_combine(lay.out, lay.row_of_slot[:T], lay.w[:T], lay.valid[:T], lay.y[:T]),
+                lambda: L.dmoe_combine_bwd(dyc, lay.out, lay.row_of_slot[:T], lay.w[:T], lay.dout, lay.dscore[:T]),
+                lambda: L.dmoe_expert_ffn_bwd_sgd(lay.xd, lay.h, lay.dout, lay.seg, lay.W1, lay.b1, lay.W2, lay.b2,
+                                                  lay.sgd_lr, lay.dxd, lay.ws, hmask=lay.hmask),
+                lambda: L.dmoe_gate_bwd(xc, lay.Wg, lay.sel[:T], lay.dscore[:T], lay.dxd, lay.row_of_slot[:T], lay.g,
+                                        lay.dx[:T], lay.dWg, lay.dbg, lay.ws),
+            ]
+            flush.fill_(1)
+            for (a, b), f in zip(ev, seq):
+                a.record(stream)
+                f()
+                b.record(stream)
+            stream.synchronize()
+            for n, (a, b) in zip(names, ev):
+                per[n].append(a.elapsed_time(b))
+    per_call_ms = {n: min(v) for n, v in per.items()}
+    R = int(lay.offsets[cfg.E].item())
+    # e2e: host buffers through the public API, chunk by chunk (HostPipeline: double-buffered
+    # staging, per-slot graphs, uploads / downloads overlapped with the neighbouring chunks)
+    from paper_2002_04013_b200.host_pipeline import HostPipeline
+    hx = torch.empty(cfg.T, cfg.D, dtype=dt, pin_memory=True)
+    hdy = torch.empty_like(hx, pin_memory=True)
+    hx.copy_(x)
+    hdy.copy_(dy)
+    hy, hdx = torch.empty_like(hx, pin_memory=True), torch.empty_like(hx, pin_memory=True)
+    pipe = HostPipeline(lay, Tc, alive, resp)
+    for c in range(nch):
+        pipe.submit(hx[c * Tc:(c + 1) * Tc], hdy[c * Tc:(c + 1) * Tc], hy[c * Tc:(c + 1) * Tc], hdx[c * Tc:(c + 1) * Tc])
+    pipe.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(pipe.h2d)
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        for c in range(nch):
+            sl = slice(c * Tc, (c + 1) * Tc)
+            pipe.submit(hx[sl], hdy[sl], hy[sl], hdx[sl])
+    b.record(pipe.d2h)
+    b.synchronize()
+    e2e = a.elapsed_time(b) / e2e_steps
+    return dict(ms=ms, step_ms=step_ms, per_call_ms=per_call_ms, e2e_ms=e2e, R=R, R_scale=nch,
+                E_act=int((lay.seg[1:] - lay.seg[:-1] > 0).sum().item()), n_dropped=int(lay.n_dropped.item()),
+                launches=c1[0] - c0[0], tc_launches=c1[1] - c0[1], clocks=clk.summary(),
+                h2d=2 * cfg.T * cfg.D * x.element_size(), d2h=2 * cfg.T * cfg.D * x.element_size())
 
 
 # ------------------------------------------------------------------ oracle (CPU)
@@ -439,7 +551,7 @@ def time_oracle(cfg, seed, steps=1, Ts=None, sampled=False):
     from gen.inputs import make_inputs  # generator only (no method arithmetic)
     from oracle import oracle as O
     Ts = oracle_sample_tokens(cfg) if Ts is None else Ts
-    full = cfg.E * cfg.D * cfg.H <= (1 << 28) and not sampled
+    full = cfg.E * cfg.D * cfg.H <= (1 << 28) and not sampled and cfg.tie == 1
     times = []
     if full:
         inp = make_inputs(cfg, seed=seed, T=Ts)
@@ -454,6 +566,7 @@ def time_oracle(cfg, seed, steps=1, Ts=None, sampled=False):
         D, H = cfg.D, cfg.H
 
         def host(tid, e, n):
+            e = int(e) // cfg.tie  # the expert's parameter slot (tied pool, reading X20)
             dist, scale = cfg.dist(tid)
             if tid in (gen.B1, gen.B2):
                 return gen.host_f32(seed, tid, dist, scale, n, int(e) * n).astype(np.float64)
@@ -545,7 +658,10 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    r = bench_ours(args, cfg, rank, world, local_rank) if world == 1 else bench_ep(args, cfg, rank, world, local_rank)
+    if cfg.chunk:
+        r = bench_chunked(args, cfg, rank, world, local_rank)
+    else:
+        r = bench_ours(args, cfg, rank, world, local_rank) if world == 1 else bench_ep(args, cfg, rank, world, local_rank)
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
     tokens = cfg.T * world
     value = tokens / (r["ms"] / 1e3)
@@ -555,8 +671,9 @@ def main():
         r["per_call_ms"] = {"expert_ffn_bwd": r["ms"]}
     dom = max(r["per_call_ms"], key=r["per_call_ms"].get)
     dms = r["per_call_ms"][dom]
-    fl = call_flops(cfg, dom, r["R"])
-    by = call_bytes(cfg, dom, r["R"], r["E_act"])
+    ccfg = cfg.with_(T=cfg.chunk) if cfg.chunk else cfg   # per-call work: one chunk's call
+    fl = call_flops(ccfg, dom, r["R"])
+    by = call_bytes(ccfg, dom, r["R"], r["E_act"])
     if r.get("ep_local"):
         El, R_in = r["ep_local"]
         es = 2 if cfg.dtype == "bf16" else 4
@@ -592,6 +709,10 @@ def main():
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (counter-based generator, seeded)",
         "config": {"workload": cfg.name, "tokens_per_gpu": cfg.T, "grid": f"{cfg.M}^{cfg.d}", "E": cfg.E, "D": cfg.D,
                    "H": cfg.H, "k": cfg.k, "beam": cfg.B, "fail_frac": cfg.fail_frac,
+                   **({"param_slots": cfg.P, "tied": f"expert e -> slot e // {cfg.tie} (reading X20)"} if cfg.tie > 1
+                      else {}),
+                   **({"chunk_tokens": cfg.chunk, "update": "fused SGD per chunk (runtime Backward request, "
+                       "PAPER.md:322)"} if cfg.chunk else {}),
                    "parallelism": (f"ep{world} (experts sharded; " + ("NCCL all-to-all" if os.environ.get("DMOE_EP") == "nccl"
                                    else "NVLink peer-memory exchange") + ")") if world > 1 else "single",
                    "l2": "flushed before every timed step (256 MiB write, untimed)",
@@ -603,10 +724,10 @@ def main():
         "gpu_launches": r["launches"] * args.steps,
         "roofline": roof,
         "clocks": r["clocks"],
-        "detail": {"per_call_ms": r["per_call_ms"], "dispatched_rows": r["R"], "experts_with_rows": r["E_act"],
+        "detail": {"per_call_ms": r["per_call_ms"], "dispatched_rows": r["R"], "param_slots_with_rows": r["E_act"],
                    "dropped_tokens": r["n_dropped"], "launches_per_step": r["launches"],
                    "tcgen05_gemm_launches_per_step": r["tc_launches"],
-                   "step_flops": step_work(cfg, r["R"])[0]},
+                   "step_flops": step_work(ccfg, r["R"])[0] * r.get("R_scale", 1)},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Ts, times, cores, sample = time_oracle(cfg, args.seed, 1)

@@ -27,6 +27,8 @@ class Config:
     beam: int = 0            # beam width B (0 -> k, the paper's Alg. 1)
     exact_grid: bool = False
     pool: int = 0            # parameter slots of the tied-weight pool (0 -> E, no tying; X20)
+    chunk: int = 0           # bench: tokens per layer call when the step does not fit one call
+                             # (each chunk is a Backward request with the fused SGD update)
 
     @property
     def E(self):
@@ -76,5 +78,8 @@ CONFIGS = {
     "mnist": Config("mnist", M=16, d=2, D=256, H=1024, k=4, T=4096, dtype="bf16", fail_frac=0.10),
     "transformer": Config("transformer", M=64, d=2, D=1024, H=4096, k=4, T=65536, dtype="bf16"),
     "grid3d": Config("grid3d", M=16, d=3, D=1024, H=4096, k=4, T=262144, dtype="bf16"),
-    "stress": Config("stress", M=64, d=2, D=2048, H=8192, k=8, T=1048576, dtype="bf16", fail_frac=0.30),
+    # 1M tokens per GPU: 8 calls of 131,072 tokens, each a full fwd + bwd with the runtime's SGD
+    # update; 512 parameter slots (the tied pool SURVEY §8(d) declares for G <= 2)
+    "stress": Config("stress", M=64, d=2, D=2048, H=8192, k=8, T=1048576, dtype="bf16", fail_frac=0.30,
+                     pool=512, chunk=131072),
 }

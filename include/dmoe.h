@@ -112,12 +112,10 @@ dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_
                            int32_t* sel, float* sel_score, void* ws, size_t ws_bytes,
                            dmoe_stream_t stream);
 
-/* S1+S2+S3 fused — gate scores (Eq. 2) and SelectExperts (Alg. 1 + FilterAlive) in one call:
+/* S1+S2+S3 in one call — gate scores (Eq. 2) then SelectExperts (Alg. 1 + FilterAlive):
  * exactly dmoe_gate_scores followed by dmoe_beam_topk (same definitions, same results bit for
- * bit), but on the bf16 tensor-core path (d*M <= 128 and a multiple of 16, beam <= 8, prefix
- * bitmaps <= 64K bits) the search runs in the gate GEMM's epilogue on each 128-token tile, so
- * G never round-trips through HBM.  G [T, d*M] fp32 is optional (NULL: not written; the
- * two-launch form then keeps it in `ws`).  sel / sel_score as dmoe_beam_topk. */
+ * bit).  G [T, d*M] fp32 is optional: NULL keeps it in `ws` (the search reads it back from L2).
+ * sel / sel_score as dmoe_beam_topk. */
 dmoe_status dmoe_gate_topk(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg,
                            const float* bg, dmoe_grid g, const uint32_t* alive_bits, float* G,
                            int32_t* sel, float* sel_score, void* ws, size_t ws_bytes,
@@ -170,6 +168,18 @@ dmoe_status dmoe_combine(const void* out, const int32_t* row_of_slot, const floa
 dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
                              const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt,
                              void* dout, float* dscore, dmoe_stream_t stream);
+
+/* S8 with backward-only failures (NEXT-3, reading X22; SPEC.md:300 spelling out PAPER.md:287 for
+ * the Backward request): an expert that answered the Forward request but whose Backward request
+ * fails (responded_bwd bit 0) is excluded from the gradient WITHOUT renormalisation: its
+ * cotangent rows dout are written as 0, so the expert backward gives it no dx contribution and
+ * no parameter gradient, while dscore (the gating gradient, formed locally from the forward's
+ * record) is exactly dmoe_combine_bwd's.  sel [T, k] from the forward; responded_bwd_bits
+ * [ceil(E/32)] uint32 (device).  Otherwise as dmoe_combine_bwd. */
+dmoe_status dmoe_combine_bwd_failures(const void* dy, const void* out, const int32_t* row_of_slot,
+                                      const float* w, const int32_t* sel, const uint32_t* responded_bwd_bits,
+                                      int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout, float* dscore,
+                                      dmoe_stream_t stream);
 
 /* S9 — grouped expert FFN backward, the runtime Backward request:
  *   dh  = (dout W2[e]) * 1[h > 0]   (X13)

@@ -181,7 +181,8 @@ def gate_bwd(X, Wg, sel, dscore, dx_rows, row_of_slot, d, M):
     return dX, dWg, dbg
 
 
-def layer_step(X, Wg, bg, W1, b1, W2, b2, dY, alive, responded, d, M, k, B, sel_override=None, tie=1):
+def layer_step(X, Wg, bg, W1, b1, W2, b2, dY, alive, responded, d, M, k, B, sel_override=None, tie=1,
+               responded_bwd=None):
     """One DMoE layer step, forward + backward, composed from S1..S10 in the paper's order.
 
     W1/b1/W2/b2 cover all E experts, or E / tie parameter slots when `tie` > 1: the declared
@@ -189,7 +190,8 @@ def layer_step(X, Wg, bg, W1, b1, W2, b2, dY, alive, responded, d, M, k, B, sel_
     slot e // tie.  Rows are dispatched per expert exactly as without tying (S5); the FFN then runs
     each slot over the rows of its tied experts, which are contiguous in the expert-major order,
     so the slot segments are offsets[::tie] and dW of a slot is the gradient of the tied weights
-    (the sum over its experts' rows).  `sel_override` (optional [T,k] int32) replaces the
+    (the sum over its experts' rows).  `responded_bwd` (optional E uint8): experts whose Backward
+    request succeeds (reading X22; the others get a zero cotangent, no renormalisation).  `sel_override` (optional [T,k] int32) replaces the
     oracle's own routing downstream of S3 (stage-wise parity with forced routing).
     Returns a dict of every intermediate and gradient.
     """
@@ -207,6 +209,12 @@ def layer_step(X, Wg, bg, W1, b1, W2, b2, dY, alive, responded, d, M, k, B, sel_
     a, out = ffn_fwd(x_rows, seg, W1, b1, W2, b2)
     y = combine(out, ros, w)
     g, dscore = combine_bwd(dY, out, ros, w)
+    if responded_bwd is not None:
+        # backward-only failures (reading X22): the lost Backward requests are omitted
+        # from the gradient without renormalisation: their experts' cotangent rows are zero
+        # (dscore, formed from the forward's record, is unchanged)
+        e_of_row = np.repeat(np.arange(E), np.diff(offsets))
+        g = np.where(np.asarray(responded_bwd)[e_of_row][:, None] == 1, g, 0.0)
     dx_rows, dW1, db1, dW2, db2 = ffn_bwd(x_rows, a, g, seg, W1, W2)
     dX, dWg, dbg = gate_bwd(X, Wg, sel, dscore, dx_rows, ros, d, M)
     return dict(G=G, sel=sel, sel_score=sc, gap=gap, w=w, ok=ok, valid=valid, n_dropped=nd,

@@ -54,6 +54,7 @@ _SIGS = {
                             ctypes.c_int),
     "dmoe_combine": ([_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P], ctypes.c_int),
     "dmoe_combine_bwd": ([_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P], ctypes.c_int),
+    "dmoe_combine_bwd_failures": ([_P, _P, _P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P], ctypes.c_int),
     "dmoe_expert_ffn_bwd": ([_P, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P, _P,
                              _SZ, _P], ctypes.c_int),
     "dmoe_expert_ffn_bwd_sgd": ([_P, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, ctypes.c_float,
@@ -167,6 +168,13 @@ def dmoe_combine_bwd(dy, out, row_of_slot, w, dout, dscore):
     _check("dmoe_combine_bwd", _L.dmoe_combine_bwd(_p(dy), _p(out), _p(row_of_slot), _p(w), T, D,
                                                    row_of_slot.shape[1], _dt(dy), _p(dout), _p(dscore),
                                                    _stream()))
+
+
+def dmoe_combine_bwd_failures(dy, out, row_of_slot, w, sel, responded_bwd_bits, dout, dscore):
+    T, D = dy.shape
+    _check("dmoe_combine_bwd_failures", _L.dmoe_combine_bwd_failures(
+        _p(dy), _p(out), _p(row_of_slot), _p(w), _p(sel), _p(responded_bwd_bits), T, D, row_of_slot.shape[1],
+        _dt(dy), _p(dout), _p(dscore), _stream()))
 
 
 def dmoe_expert_ffn_bwd(xd, h, dout, offsets, W1, W2, dxd, dW1, db1, dW2, db2, ws, hmask=None):

@@ -60,7 +60,7 @@ dmoe_status combine(const void* out, const int32_t* row_of_slot, const float* w,
                     cudaStream_t s);
 dmoe_status combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
                         const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout,
-                        float* dscore, cudaStream_t s);
+                        float* dscore, const int32_t* sel, const uint32_t* bwd_ok, cudaStream_t s);
 size_t gate_bwd_ws_bytes(int64_t T, int32_t D, int dM);
 dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt, void* dst,
                       cudaStream_t s);
@@ -298,21 +298,11 @@ dmoe_status dmoe_gate_topk(const void* x, dmoe_dtype dt, int64_t T, int32_t D, c
   NN(x); NN(sel); NN(sel_score);
   cudaStream_t s = (cudaStream_t)stream;
   const int dM = g.d * g.M;
-  if (dt == DMOE_BF16 && tc_gate_topk_supported(dM, D, g.d, g.M, g.beam)) {
-    // one launch: tcgen05 gate GEMM, Alg. 1 on each 128-token tile in the epilogue
-    DMOE_REQUIRE(ws_bytes >= (size_t)dM * D * 2, DMOE_ERR_ARG, "gate_topk: workspace too small");
-    DMOE_TRY(transpose(Wg, D, dM, dt, ws, s));
-    GemmRows r{};
-    r.A = x; r.B = ws; r.C = G; r.bias = bg; r.aux = nullptr;
-    r.offsets = nullptr; r.plan = nullptr;
-    r.E = 1; r.N = dM; r.K = D; r.rows_single = T; r.rows_cap = T;
-    r.b_mn = false; r.epi = EPI_GATE_TOPK;
-    r.topk.sel = sel; r.topk.sel_score = sel_score; r.topk.alive = alive_bits;
-    r.topk.d = g.d; r.topk.M = g.M; r.topk.k = g.k; r.topk.B = g.beam;
-    r.max_tiles = ceil_div(T, tc_rows_tile(r));
-    return tc_gemm_rows(r, s);
-  }
-  // two launches: gate scores into G (the caller's, else the workspace), then the search
+  // The gate GEMM (tcgen05, W_g^T staged in the workspace) writes G, the thread-per-token search
+  // reads it back (mostly from L2).  Running Alg. 1 in the GEMM's epilogue instead was built and
+  // measured slower (transformer 107-128 us vs 44 + 52 us; grid3d 413 vs 234 us): a 128-token
+  // tile's search needs more warps than the GEMM kernel's 8 epilogue warps, so it could not hide
+  // behind the next tile's mainloop.
   Carver cv(ws, ws_bytes);
   uint32_t* pa = cv.take<uint32_t>(prefix_words(g.d, g.M));
   void* wgt = cv.take<char>((size_t)dM * D * 2);
@@ -398,7 +388,19 @@ dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row
   DMOE_TRY(check_dt(dt, D));
   DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
   if (T > 0) { NN(dy); NN(row_of_slot); NN(w); NN(dscore); }
-  return combine_bwd(dy, out, row_of_slot, w, T, D, k, dt, dout, dscore, (cudaStream_t)stream);
+  return combine_bwd(dy, out, row_of_slot, w, T, D, k, dt, dout, dscore, nullptr, nullptr, (cudaStream_t)stream);
+}
+
+dmoe_status dmoe_combine_bwd_failures(const void* dy, const void* out, const int32_t* row_of_slot,
+                                      const float* w, const int32_t* sel, const uint32_t* responded_bwd_bits,
+                                      int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout, float* dscore,
+                                      dmoe_stream_t stream) {
+  DMOE_TRY(check_dt(dt, D));
+  DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
+  NN(responded_bwd_bits);
+  if (T > 0) { NN(dy); NN(row_of_slot); NN(w); NN(dscore); NN(sel); }
+  return combine_bwd(dy, out, row_of_slot, w, T, D, k, dt, dout, dscore, sel, responded_bwd_bits,
+                     (cudaStream_t)stream);
 }
 
 dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,

@@ -163,6 +163,141 @@ __device__ __forceinline__ void beam_search_row(const float* grow, int gstride, 
   }
 }
 
+// ---- unmasked fast path, split into per-dimension lists + a merge --------------------------
+// With every expert alive, Alg. 1's level-i candidates are prefix score + g_i(j), so the work per
+// token splits into d independent per-dimension lists (run by different threads) and a short
+// sequential merge:
+//   list_i = the best W_i + 1 of g_i(0..M) under the key (g desc, j asc)   (W_i = B, k at the end)
+//   level 0: the beam is list_0's first W_0 (0 + g is exact: the order is g's own)
+//   level i: prefix b's best W are among list_i's first W unless the (W+1)-th reaches the W-th's
+//            rounded sum (then a j outside the list could tie it and win on the lower index: that
+//            prefix is scanned in full); the union over prefixes holds the level's best W.
+// Running best-n set of (score, index) under the order of reading X4, for a thread's scan:
+// unsorted, with the worst member tracked, so a candidate costs one compare against it and an
+// accepted one a slot replacement plus an n-step min scan (not a sorted-list shift of 64-bit
+// keys); sorted once at the end.  Empty slots are (-inf, 0xffffffff), worse than any real key.
+template <int N>
+struct TopSet {
+  float v[N];
+  uint32_t i[N];
+  float mv;     // the worst member
+  uint32_t mi;
+  int mpos;
+  int n;        // active slots (<= N)
+  __device__ __forceinline__ static bool better(float a, uint32_t ai, float b, uint32_t bi) {
+    return a > b || (a == b && ai < bi);
+  }
+  __device__ __forceinline__ void init(int n_) {
+    n = n_;
+#pragma unroll
+    for (int q = 0; q < N; ++q) { v[q] = -INFINITY; i[q] = 0xffffffffu; }
+    mv = -INFINITY; mi = 0xffffffffu; mpos = 0;
+  }
+  __device__ __forceinline__ void rescan() {
+    mv = v[0]; mi = i[0]; mpos = 0;
+#pragma unroll
+    for (int q = 1; q < N; ++q)
+      if (q < n && better(mv, mi, v[q], i[q])) { mv = v[q]; mi = i[q]; mpos = q; }
+  }
+  __device__ __forceinline__ void offer(float s, uint32_t idx) {
+    if (!better(s, idx, mv, mi)) return;  // NaN never enters (undefined, reading X4)
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+      if (q == mpos) { v[q] = s; i[q] = idx; }
+    rescan();
+  }
+  // sort descending by key (odd-even transposition network), empty slots last
+  __device__ __forceinline__ void sort() {
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int q = r & 1; q + 1 < N; q += 2)
+        if (better(v[q + 1], i[q + 1], v[q], i[q])) {
+          const float tv = v[q]; v[q] = v[q + 1]; v[q + 1] = tv;
+          const uint32_t ti = i[q]; i[q] = i[q + 1]; i[q + 1] = ti;
+        }
+  }
+  __device__ __forceinline__ uint64_t key(int q) const {  // 0 for an empty slot
+    return i[q] == 0xffffffffu ? 0ull : beam_key(v[q], i[q]);
+  }
+};
+
+template <int WMAX>
+__device__ __forceinline__ void beam_dim_list(const float* gi, int gstride, int M, int n, uint64_t* out) {
+  TopSet<WMAX + 1> L;
+  L.init(n);
+  int j = 0;
+  for (; j + 4 <= M; j += 4) {
+    const float g0 = gi[(j + 0) * gstride], g1 = gi[(j + 1) * gstride];
+    const float g2 = gi[(j + 2) * gstride], g3 = gi[(j + 3) * gstride];
+    if (!(fmaxf(fmaxf(g0, g1), fmaxf(g2, g3)) >= L.mv)) continue;
+    L.offer(g0, j); L.offer(g1, j + 1); L.offer(g2, j + 2); L.offer(g3, j + 3);
+  }
+  for (; j < M; ++j) L.offer(gi[j * gstride], j);
+  L.sort();
+#pragma unroll
+  for (int q = 0; q <= WMAX; ++q)
+    if (q < n) out[q] = L.key(q);
+}
+
+// the merge of one token: lists [d][WMAX + 1] (beam_dim_list outputs, n_i = W_i + 1 entries,
+// 0 = missing); grow / gstride: the token's G row (read only by prefixes scanned in full)
+template <int WMAX>
+__device__ __forceinline__ void beam_merge_row(const float* grow, int gstride, int d, int M, int k, int B,
+                                               const uint64_t* lists, int32_t* sel, float* score) {
+  uint64_t beam[WMAX];
+  int nb = 0;
+  {
+    const int W0 = d > 1 ? B : k;
+#pragma unroll
+    for (int q = 0; q < WMAX; ++q) {
+      const uint64_t v = q < W0 ? lists[q] : 0ull;
+      beam[q] = v;
+      nb += v ? 1 : 0;
+    }
+  }
+  for (int i = 1; i < d; ++i) {
+    const int W = (i < d - 1) ? B : k;
+    const uint64_t* Li = lists + i * (WMAX + 1);
+    const int nL = M < W + 1 ? M : W + 1;
+    const float* gi = grow + (int64_t)i * M * gstride;
+    TopSet<WMAX> top;
+    top.init(W);
+    auto consider = [&](float s, uint32_t p) { top.offer(s == 0.0f ? 0.0f : s, p); };
+    const float gW = nL >= W ? beam_unord((uint32_t)(Li[W - 1] >> 32)) : 0.0f;
+    const float gN = nL == W + 1 ? beam_unord((uint32_t)(Li[W] >> 32)) : 0.0f;
+#pragma unroll
+    for (int b = 0; b < WMAX; ++b) {
+      if (b < nb) {
+        const uint32_t p0 = (0xffffffffu - (uint32_t)beam[b]) * (uint32_t)M;
+        const float sp = beam_unord((uint32_t)(beam[b] >> 32));
+        if (nL == W + 1 && !(sp + gW > sp + gN)) {  // rounding may let a j outside the list tie
+          for (int j = 0; j < M; ++j) consider(sp + gi[j * gstride], p0 + (uint32_t)j);
+        } else {
+          const int nq = nL < W ? nL : W;
+          for (int q = 0; q < nq; ++q) {
+            const uint64_t v = Li[q];
+            consider(sp + beam_unord((uint32_t)(v >> 32)), p0 + (0xffffffffu - (uint32_t)v));
+          }
+        }
+      }
+    }
+    top.sort();
+    nb = 0;
+#pragma unroll
+    for (int q = 0; q < WMAX; ++q) {
+      const uint64_t kq = q < W ? top.key(q) : 0ull;
+      beam[q] = kq;
+      nb += kq ? 1 : 0;
+    }
+  }
+  for (int s = 0; s < k; ++s) {
+    const uint64_t v = beam_at<WMAX>(beam, s);
+    sel[s] = s < nb ? (int32_t)(0xffffffffu - (uint32_t)v) : -1;
+    score[s] = s < nb ? beam_unord((uint32_t)(v >> 32)) : -INFINITY;
+  }
+}
+
 // any alive expert in [e0, e0 + span)
 __device__ __forceinline__ bool span_any(const uint32_t* __restrict__ alive, int64_t e0, int64_t span) {
   const int64_t e1 = e0 + span;

@@ -55,19 +55,27 @@ template <typename T, int kMaxK>
 __global__ void __launch_bounds__(kCombWarps * 32)
 k_combine_bwd(const T* __restrict__ dy, const T* __restrict__ out,
               const int32_t* __restrict__ row_of_slot, const float* __restrict__ w, int64_t Tn,
-              int32_t D, int k, T* __restrict__ dout, float* __restrict__ dscore) {
+              int32_t D, int k, const int32_t* __restrict__ sel, const uint32_t* __restrict__ bwd_ok,
+              T* __restrict__ dout, float* __restrict__ dscore) {
   DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
   const int lane = threadIdx.x & 31;
   for (int64_t t = blockIdx.x * (int64_t)kCombWarps + (threadIdx.x >> 5); t < Tn;
        t += (int64_t)gridDim.x * kCombWarps) {
     int32_t rows[kMaxK];
-    float ws[kMaxK], a[kMaxK];
+    float ws[kMaxK], a[kMaxK], wo[kMaxK];
 #pragma unroll
     for (int s = 0; s < kMaxK; ++s) {
       rows[s] = s < k ? row_of_slot[t * k + s] : -1;
       ws[s] = s < k ? w[t * k + s] : 0.0f;
       a[s] = 0.0f;
+      // backward-only failure (reading X22): the expert's Backward request is lost, so its
+      // cotangent row is zero (no dx contribution, no parameter gradient); dscore is unchanged
+      wo[s] = ws[s];
+      if (bwd_ok && s < k && rows[s] >= 0) {
+        const int32_t e = sel[t * k + s];
+        if (!((bwd_ok[e >> 5] >> (e & 31)) & 1u)) wo[s] = 0.0f;
+      }
     }
     // a_s = <dy_t, out_row>, and dout_row = w_s dy_t in the same pass over dy_t
     for (int c = lane * V; c < D; c += 32 * V) {
@@ -87,7 +95,7 @@ k_combine_bwd(const T* __restrict__ dy, const T* __restrict__ out,
 #pragma unroll
         for (int i = 0; i < V; ++i) {
           pr = fmaf(g[i], f[i], pr);
-          o[i] = ws[s] * g[i];
+          o[i] = wo[s] * g[i];
         }
         a[s] += pr;
         st_v4(dout + (int64_t)rows[s] * D + c, pack16(o, (const T*)nullptr));
@@ -132,16 +140,16 @@ dmoe_status combine(const void* out, const int32_t* row_of_slot, const float* w,
 
 dmoe_status combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
                         const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout,
-                        float* dscore, cudaStream_t s) {
+                        float* dscore, const int32_t* sel, const uint32_t* bwd_ok, cudaStream_t s) {
   if (T == 0) return DMOE_OK;
 #define DMOE_COMBB(KM)                                                                             \
   if (dt == DMOE_BF16)                                                                             \
     launch_pdl(k_combine_bwd<__nv_bfloat16, KM>, grid_tokens(T), kCombWarps * 32, 0, s, \
-        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)out, row_of_slot, w, T, D, k,              \
+        (const __nv_bfloat16*)dy, (const __nv_bfloat16*)out, row_of_slot, w, T, D, k, sel, bwd_ok, \
         (__nv_bfloat16*)dout, dscore);                                                             \
   else                                                                                             \
     launch_pdl(k_combine_bwd<float, KM>, grid_tokens(T), kCombWarps * 32, 0, s, \
-        (const float*)dy, (const float*)out, row_of_slot, w, T, D, k, (float*)dout, dscore);
+        (const float*)dy, (const float*)out, row_of_slot, w, T, D, k, sel, bwd_ok, (float*)dout, dscore);
   if (k <= 4) { DMOE_COMBB(4) } else if (k <= 8) { DMOE_COMBB(8) } else { DMOE_COMBB(16) }
 #undef DMOE_COMBB
   return check_launch("combine_bwd");

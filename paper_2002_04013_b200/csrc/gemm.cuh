@@ -10,17 +10,7 @@ enum Epi {
   EPI_BIAS = 2,       // out = acc + bias[e][n]                   (expert output)
   EPI_RELU_MASK = 3,  // out = acc * 1[aux[r][n] > 0]             (dh, ReLU'(0) = 0)
   EPI_PLAIN = 4,      // out = acc                                (dxd)
-  EPI_GATE_TOPK = 5,  // G = acc + bias[n] staged in smem, then Alg. 1 per row (beam.cuh):
-                      // sel / sel_score out, G itself optional (C may be nullptr)
   EPI_F32 = 6         // fp32 out = acc                           (SEGK split-K partials: dW_g)
-};
-
-// EPI_GATE_TOPK: the grid and liveness of the fused gate + SelectExperts epilogue
-struct GateTopk {
-  int32_t* sel = nullptr;        // [T, k]
-  float* sel_score = nullptr;    // [T, k]
-  const uint32_t* alive = nullptr;  // [ceil(E/32)]
-  int d = 0, M = 0, k = 0, B = 0;
 };
 
 // ROWS family: C[r, n] = epi(sum_k A[r, k] B_e(n, k)) for r in expert segments
@@ -41,7 +31,6 @@ struct GemmRows {
   int max_ctas = 0;        // persistent grid cap (0: one CTA per SM); leaves SMs to a concurrent GEMM
   uint32_t* hmask = nullptr;  // packed ReLU mask [N/32][hmask_ld]: EPI_BIAS_RELU writes, EPI_RELU_MASK reads
   int64_t hmask_ld = 0;
-  GateTopk topk;              // EPI_GATE_TOPK only
 };
 
 // SEGK family: C_e[m, n] = sum_{r in seg e} A[r, m] B[r, n]  (K = segment rows)
@@ -73,7 +62,6 @@ bool tc_rows_supported(const GemmRows& g);
 int tc_rows_tile(const GemmRows& g);       // token rows per tile of the row engine (plan granularity)
 int tc_plan_in_kernel_max();               // experts up to which the M-major engine plans row tiles itself
 bool tc_rows_mmajor();                     // the M-major row engine (not the swap-AB experiment) runs them
-bool tc_gate_topk_supported(int dM, int D, int d, int M, int beam);  // the fused gate + Alg. 1 epilogue
 bool tc_segk_supported(const GemmSegK& g);
 bool tc_segk_colsum_supported(const GemmSegK& g);  // the SEGK engine also writes colsum
 bool tc_segk2_supported(const GemmSegK& a, const GemmSegK& b);

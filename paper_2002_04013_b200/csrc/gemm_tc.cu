@@ -23,7 +23,6 @@
 #include <cuda.h>
 #include <stdlib.h>
 
-#include "beam.cuh"
 #include "gemm.cuh"
 
 namespace dmoe {
@@ -220,9 +219,6 @@ struct TcParams {
   int table_len;  // M-major engine: per-expert smem table entries (0: tables stay in global)
   float sgd_lr;    // SEGK bf16: != 0 -> C (and colsum) are the parameters, updated in place:
                    // C -= lr * acc (the dW tile never reaches HBM), colsum -= lr * column sums
-  GateTopk topk;   // EPI_GATE_TOPK: Alg. 1 in the epilogue
-  int topk_bytes;  // EPI_GATE_TOPK: smem of the G tile [128][N+1] fp32 + prefix-alive bitmaps
-  int pa_words;    // EPI_GATE_TOPK: words of the prefix-alive bitmaps (<= kTopkPAWords)
   int slot;  // probe slot (launch ordinal % 8)
   int dbg;  // experiment switches (DMOE_EXPERIMENTS builds only, env DMOE_TC_DEBUG): 1 skip stores,
             // 2 skip TMEM loads, 4 skip MMAs, 8 timeline probe, 16 L2 prefetch cursor, 32 no L2 hints,
@@ -235,14 +231,15 @@ constexpr int TC_STAGE_WARP = 5 * 1024;           // one warp's 32-row staging t
 constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan live in smem
 
 constexpr int TC_MAX_STAGES = 8;
-constexpr int kTopkPAWords = 2048;  // fused gate + top-k: prefix bitmaps up to 64K bits (in smem)
-constexpr int kTopkWMAX = 8;        // fused gate + top-k: beam widths up to 8
 
 template <int BN, bool SEGK = false> struct TcCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
   // epilogue warps: 8 (two column halves) for tiles >= 128 wide.  4 warps on 256-wide tiles buy
   // a 4th ring stage but the epilogue then trails the mainloop (measured: mnist FFN fwd 78 -> 92 us)
-  static constexpr int EPI_WARPS = (BN >= 128) ? 8 : 4;
+  // weight-gradient tiles (~1 K block each) are epilogue-paced: 256-wide ones get 16 epilogue warps
+  // (one 64-column box each) so TMEM drains at twice the rate (measured: the 8-warp epilogue was
+  // busy ~70% of the tile time while the MMA waited for accumulators)
+  static constexpr int EPI_WARPS = (SEGK && BN == 256) ? 16 : ((BN >= 128) ? 8 : 4);
   static constexpr int EPI_COLS = BN / (EPI_WARPS / 4);   // columns per epilogue warp
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;       // 16 KB
@@ -253,15 +250,14 @@ template <int BN, bool SEGK = false> struct TcCfg {
   // MMA run two tiles ahead, and each warp double-buffers its 4 KB store box so the TMA
   // engine's read of one box overlaps the staging of the next
   static constexpr int NACC = (SEGK && BN <= 128) ? 3 : 2;
-  static constexpr int STG_WARP = SEGK ? 8 * 1024 : TC_STAGE_WARP;
+  static constexpr int STG_WARP = SEGK ? (EPI_WARPS == 16 ? 4 * 1024 : 8 * 1024) : TC_STAGE_WARP;
+  static constexpr int NBOX = SEGK ? STG_WARP / 4096 : 1;   // SEGK store boxes per warp (4 KB each)
   static constexpr int FIXED = 1024 /*align*/ + 1024 /*barriers*/ + EPI_WARPS * STG_WARP + BN * 4 * 2;
-  static int stages_for(int table_len, int extra = 0) {
-    const int st = (TC_SMEM_MAX - FIXED - 2 * table_len * 4 - extra) / STAGE_BYTES;
+  static int stages_for(int table_len) {
+    const int st = (TC_SMEM_MAX - FIXED - 2 * table_len * 4) / STAGE_BYTES;
     return st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
   }
-  static int smem_for(int table_len, int extra = 0) {
-    return stages_for(table_len, extra) * STAGE_BYTES + FIXED + 2 * table_len * 4 + extra;
-  }
+  static int smem_for(int table_len) { return stages_for(table_len) * STAGE_BYTES + FIXED + 2 * table_len * 4; }
   static constexpr int pow2cols(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512; }
   static constexpr int TMEM_COLS = pow2cols(NACC * BN);                 // NACC accumulators
   static_assert(TMEM_COLS <= 512, "TMEM");
@@ -303,8 +299,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   constexpr int NACC = Cfg::NACC;
   const int S = p.stages;
   constexpr bool A_MN = SEGK;  // A is MN-major exactly for the weight-gradient GEMMs
-  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS || EPI == EPI_GATE_TOPK || EPI == EPI_F32);
-  constexpr bool TOPK = (EPI == EPI_GATE_TOPK);
+  constexpr bool OUT_F32 = (EPI == EPI_F32_BIAS || EPI == EPI_F32);
+  constexpr bool STG_SWZ = Cfg::STG_WARP < 32 * TC_STAGE_ROW;  // 4 KB staging boxes: swizzled 128 B rows
   constexpr int OUT_ES = OUT_F32 ? 4 : 2;
   constexpr int SUB = 128 / OUT_ES;  // columns per staged sub-tile (128 bytes per row)
   extern __shared__ uint8_t smem_raw[];
@@ -320,11 +316,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   float* bias_s = (float*)(stage_base + Cfg::EPI_WARPS * Cfg::STG_WARP);  // [2][BN]
   int32_t* off_s = (int32_t*)(bias_s + 2 * BN);                             // [table_len]
   int32_t* plan_s = off_s + p.table_len;                                    // [table_len]
-  // EPI_GATE_TOPK: G tile [128][N + 1] fp32 (row pitch N + 1: a thread's row walk and the
-  // epilogue's column writes both hit 32 distinct banks) and the prefix-alive bitmaps
-  float* gtile = reinterpret_cast<float*>(plan_s + p.table_len);
-  uint32_t* pa_s = reinterpret_cast<uint32_t*>(gtile + TC_BM * (p.N + 1));
-  __shared__ int topk_masked;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -372,27 +363,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       }
       if (threadIdx.x == 0) plan_s[p.E] = carry;
     }
-    __syncthreads();
-  }
-
-  // ---- EPI_GATE_TOPK: FilterAlive bitmaps (reading X5) in smem, unless every expert is alive
-  int pa_off[4] = {0, 0, 0, 0};
-  if (TOPK) {
-    int64_t E = 1;
-    for (int i = 0; i < p.topk.d; ++i) E *= p.topk.M;
-    {
-      int64_t wo = 0, n = p.topk.M;
-      for (int i = 0; i < p.topk.d; ++i) { pa_off[i] = (int)wo; wo += (n + 31) / 32; n *= p.topk.M; }
-    }
-    bool dead = false;
-    const int64_t aw = (E + 31) / 32;
-    for (int64_t w = threadIdx.x; w < aw; w += blockDim.x) {
-      const uint32_t want = (w == aw - 1 && (E & 31)) ? ((1u << (E & 31)) - 1u) : 0xffffffffu;
-      dead |= (p.topk.alive[w] & want) != want;
-    }
-    const int masked = __syncthreads_or(dead);
-    if (threadIdx.x == 0) topk_masked = masked;
-    if (masked) prefix_alive_block(p.topk.alive, p.topk.d, p.topk.M, E, pa_s);
     __syncthreads();
   }
 
@@ -744,8 +714,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       const CUtensorMap* mC = prob ? &tmC2 : &tmC;
       const int mdim = prob ? p.Mdim2 : p.Mdim;
       const bool has_acc = !(SEGK && nkb == 0);
+      bool released = false;  // accumulator handed back early (after the last TMEM load)
       // stage this tile's bias slice (double-buffered across tiles; one named barrier)
-      constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_GATE_TOPK || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
+      constexpr bool HAS_BIAS = (EPI == EPI_F32_BIAS || EPI == EPI_BIAS || EPI == EPI_BIAS_RELU);
       float* bias_t = bias_s + bias_buf * BN;
       if (HAS_BIAS) {
         for (int c = threadIdx.x - 128; c < BN; c += 32 * Cfg::EPI_WARPS)
@@ -792,10 +763,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (lane == 0) {
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // both boxes free
 #pragma unroll
-          for (int sb = 0; sb < NSUB && sb < 2; ++sb) {
-            const int bx = (stg_buf + sb) & 1;
-            mbar_expect_tx(&wload[ew * 2 + bx], 4096);
-            tma_load_2d(stg_warp + bx * 4096, mC, &wload[ew * 2 + bx], n0 + c_beg + sb * SUB,
+          for (int sb = 0; sb < NSUB && sb < Cfg::NBOX; ++sb) {
+            const int bx = (stg_buf + sb) % Cfg::NBOX;
+            mbar_expect_tx(&wload[ew * Cfg::NBOX + bx], 4096);
+            tma_load_2d(stg_warp + bx * 4096, mC, &wload[ew * Cfg::NBOX + bx], n0 + c_beg + sb * SUB,
                         (int)((int64_t)e * mdim + qrow0));
           }
         }
@@ -842,10 +813,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           stg = stg_warp + stg_buf * 4096;
           WT_T0(t_st);
           if (sgd) {
-            mbar_wait(&wload[ew * 2 + stg_buf], wph[stg_buf]);  // the parameter box has landed
+            mbar_wait(&wload[ew * Cfg::NBOX + stg_buf], wph[stg_buf]);  // the parameter box has landed
             wph[stg_buf] ^= 1u;
-          } else {
-            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          } else if (lane == 0) {
+            if (Cfg::NBOX == 1) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
           }
           __syncwarp();
           WT_ADD(w_st, t_st);
@@ -867,6 +839,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (sb == NSUB - 1) {
+            // the tile's last columns are in registers: hand the accumulator back to the MMA now,
+            // before the staging and stores (the MMA of the tile after next needs it)
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            released = true;
+          }
         }
 #pragma unroll
         for (int c16 = 0; c16 < SUB; c16 += 16) {
@@ -906,12 +886,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
               if (!((hmask[col >> 5] >> (col & 31)) & 1u)) v[j] = 0.0f;
             }
           }
-          if (TOPK) {
-            float* grow_s = gtile + (q * 32 + lane) * (p.N + 1) + cs + c16;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) grow_s[j] = v[j];
-            continue;
-          }
           if (SEGK && !OUT_F32) {
             // 128B-swizzled box row (the TMA store layout): 16-byte chunk q of row `lane`
             // sits at chunk q ^ (lane & 7)
@@ -933,20 +907,26 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             }
             continue;
           }
-          uint8_t* dst = stg + lane * TC_STAGE_ROW + c16 * OUT_ES;
+          // staging row `lane`, 16-byte piece pc: padded rows (144 B pitch), or 128 B rows with the
+          // pieces XOR-swizzled by the row when the warp's box is 4 KB (16-warp weight-gradient tiles)
           if (OUT_F32) {
 #pragma unroll
-            for (int j = 0; j < 16; j += 4)
-              *reinterpret_cast<float4*>(dst + j * 4) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            for (int j = 0; j < 16; j += 4) {
+              const int pc = (c16 * 4 + j * 4) >> 4;
+              uint8_t* dst = STG_SWZ ? stg + lane * 128 + ((pc ^ (lane & 7)) << 4) : stg + lane * TC_STAGE_ROW + pc * 16;
+              *reinterpret_cast<float4*>(dst) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            }
           } else {
 #pragma unroll
-            for (int j = 0; j < 16; j += 8)
-              *reinterpret_cast<uint4*>(dst + j * 2) =
+            for (int j = 0; j < 16; j += 8) {
+              const int pc = (c16 * 2 + j * 2) >> 4;
+              uint8_t* dst = STG_SWZ ? stg + lane * 128 + ((pc ^ (lane & 7)) << 4) : stg + lane * TC_STAGE_ROW + pc * 16;
+              *reinterpret_cast<uint4*>(dst) =
                   make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
                              pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+            }
           }
         }
-        if (TOPK) continue;
         if (SEGK && !OUT_F32) {
           // full 32 x 64 box: one bulk tensor store (double-buffered box, see above)
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -959,7 +939,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                 : "memory");
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
-          stg_buf ^= 1;
+          stg_buf = (stg_buf + 1) % Cfg::NBOX;
           __syncwarp();
           continue;
         }
@@ -970,7 +950,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + (lane >> 3), piece = lane & 7;
           if (r < live_rows && piece * 16 < row_bytes && !(DMOE_DBG(p) & 1)) {
-            const uint4 v = *reinterpret_cast<const uint4*>(stg + r * TC_STAGE_ROW + piece * 16);
+            const uint4 v = *reinterpret_cast<const uint4*>(
+                STG_SWZ ? stg + r * 128 + ((piece ^ (r & 7)) << 4) : stg + r * TC_STAGE_ROW + piece * 16);
             uint8_t* gdst;
             if (SEGK)
               gdst = (uint8_t*)p.C + (((int64_t)e * p.Mdim + qrow0 + r) * p.N + n0 + cs) * OUT_ES + piece * 16;
@@ -981,43 +962,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
       }
-      if (TOPK) {
-        // the accumulator is in registers / smem now: hand TMEM back to the MMA first
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * Cfg::EPI_WARPS) : "memory");  // whole G tile staged
-        const int tid = threadIdx.x - 128;
-        if (p.C) {  // G (optional output): coalesced 16-byte rows
-          const int q4 = p.N / 4;
-          for (int i = tid; i < TC_BM * q4; i += 32 * Cfg::EPI_WARPS) {
-            const int r = i / q4, c = (i - r * q4) * 4;
-            if (row0 + r < row_end) {
-              const float* src = gtile + r * (p.N + 1) + c;
-              *reinterpret_cast<float4*>((float*)p.C + (row0 + r) * p.N + c) = make_float4(src[0], src[1], src[2], src[3]);
-            }
-          }
-        }
-        if (ew < 4 && lane < live_rows) {  // Alg. 1, one thread per token
-          const int64_t t = qrow0 + lane;
-          const float* grow_s = gtile + (ew * 32 + lane) * (p.N + 1);
-          const GateTopk& tk = p.topk;
-          if (topk_masked)
-            beam_search_row<kTopkWMAX, true>(grow_s, 1, tk.d, tk.M, tk.k, tk.B, pa_s, pa_off, tk.sel + t * tk.k,
-                                             tk.sel_score + t * tk.k);
-          else
-            beam_search_row<kTopkWMAX, false>(grow_s, 1, tk.d, tk.M, tk.k, tk.B, pa_s, pa_off, tk.sel + t * tk.k,
-                                              tk.sel_score + t * tk.k);
-        }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * Cfg::EPI_WARPS) : "memory");  // G tile free again
-        continue;
-      }
       if (ew == 0 && lane == 0) PROBE(5, it);
       if (has_acc) {
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (!released) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
         if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -1117,14 +1068,6 @@ bool tc_rows_supported(const GemmRows& g) {
   if (encode_fn() == nullptr) return false;
   return true;
 }
-// the fused gate + SelectExperts epilogue: one N tile of K-major W_g^T (d*M <= 128 columns,
-// a multiple of 16), beam widths <= 8, prefix bitmaps that fit in smem
-bool tc_gate_topk_supported(int dM, int D, int d, int M, int beam) {
-  int64_t words = 0, n = M;
-  for (int i = 0; i < d; ++i) { words += (n + 31) / 32; n *= M; }
-  return dM % 16 == 0 && dM <= 128 && D % TC_BK == 0 && beam <= kTopkWMAX && words <= kTopkPAWords &&
-         encode_fn() != nullptr;
-}
 
 bool tc_segk_supported(const GemmSegK& g) {
   return g.Mdim % TC_BM == 0 && g.N % 128 == 0 && encode_fn() != nullptr;
@@ -1155,8 +1098,7 @@ static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const
                                const TcParams& p, int64_t max_tiles, cudaStream_t s) {
   auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
   const int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
-  const int extra = EPI == EPI_GATE_TOPK ? p.topk_bytes : 0;
-  const int smem = TcCfg<BN, SEGK>::smem_for(table_len, extra);
+  const int smem = TcCfg<BN, SEGK>::smem_for(table_len);
   static int attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1168,7 +1110,7 @@ static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const
   TcParams pp = p;
   pp.dbg = debug_flags() | (SEGK ? debug_flags_segk() : 0);
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  pp.stages = TcCfg<BN, SEGK>::stages_for(table_len, extra);
+  pp.stages = TcCfg<BN, SEGK>::stages_for(table_len);
   pp.table_len = table_len;
   launch_pdl(kern, (unsigned)grid, TcCfg<BN, SEGK>::THREADS, smem, s, a, b, c, a2, b2, c2, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
@@ -1187,9 +1129,6 @@ static dmoe_status rows_bn(const GemmRows& g, const CUtensorMap& a, const CUtens
 #define DMOE_TC_EPI(BMN)                                   \
   switch (g.epi) {                                         \
     case EPI_F32_BIAS: DMOE_TC_ROWS(BMN, EPI_F32_BIAS);    \
-    case EPI_GATE_TOPK:                                    \
-      if constexpr (!BMN && BN <= 128) { DMOE_TC_ROWS(BMN, EPI_GATE_TOPK); } \
-      return set_error(DMOE_ERR_UNSUPPORTED, "gate_topk: N tile %d", BN);   \
     case EPI_BIAS_RELU: DMOE_TC_ROWS(BMN, EPI_BIAS_RELU);  \
     case EPI_BIAS: DMOE_TC_ROWS(BMN, EPI_BIAS);            \
     case EPI_RELU_MASK: DMOE_TC_ROWS(BMN, EPI_RELU_MASK);  \
@@ -1225,13 +1164,6 @@ static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
   p.C = g.C; p.E = g.E; p.N = g.N; p.K = g.K; p.Mdim = 0; p.rows_single = g.rows_single;
   p.max_ctas = g.max_ctas;
   p.hmask = g.hmask; p.hmask_ld = g.hmask_ld;
-  if (g.epi == EPI_GATE_TOPK) {
-    int64_t E = 1, words = 0, n = g.topk.M;
-    for (int i = 0; i < g.topk.d; ++i) { E *= g.topk.M; words += (n + 31) / 32; n *= g.topk.M; }
-    p.topk = g.topk;
-    p.pa_words = (int)words;
-    p.topk_bytes = (int)align_up((size_t)TC_BM * (g.N + 1) * 4 + (size_t)words * 4, 16);
-  }
   const int64_t tiles = g.max_tiles * ((g.N + BN - 1) / BN);
   switch (BN) {
     case 256: return rows_bn<256>(g, ta, tb, p, tiles, s);

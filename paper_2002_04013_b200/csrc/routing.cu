@@ -48,22 +48,24 @@ __global__ void k_prefix_alive(const uint32_t* __restrict__ alive, int d, int M,
 }
 
 constexpr int kSmemPAWords = 2048;  // prefix bitmaps up to 64K bits live in smem
-constexpr int kBeamTok = 128;       // tokens (threads) per CTA
+constexpr int kBeamTok = 128;       // tokens per CTA tile
+constexpr int kBeamThreads = 256;   // threads per CTA: (token, level) list tasks, then a merge per token
 
 // Thread per token (beam.cuh): the CTA stages its 128 tokens' G rows in shared memory with
 // coalesced 16-byte loads (row pitch d*M + 1 floats: the threads' column reads hit 32 distinct
 // banks), builds the prefix-alive bitmaps in shared memory (small grids) and notes whether every
 // expert is alive (then FilterAlive is a no-op and the unmasked search runs).
 template <int WMAX>
-__global__ void __launch_bounds__(kBeamTok, 1)
+__global__ void __launch_bounds__(kBeamThreads, 2)
 k_beam_topk(const float* __restrict__ G, int64_t T, int d, int M, int k, int B,
             const uint32_t* __restrict__ PA_global, const uint32_t* __restrict__ alive, int pa_words,
             int32_t* __restrict__ sel, float* __restrict__ sel_score) {
   DMOE_PDL_ENTRY();
   extern __shared__ float smem_f[];
   const int dM = d * M, pitch = dM + 1;
-  float* gtile = smem_f;                                                 // [kBeamTok][pitch]
-  uint32_t* pa_s = reinterpret_cast<uint32_t*>(smem_f + kBeamTok * pitch);
+  float* gtile = smem_f;                                                     // [kBeamTok][pitch]
+  uint64_t* lists = reinterpret_cast<uint64_t*>(smem_f + ((kBeamTok * pitch + 1) & ~1));  // [tok][d][WMAX+1]
+  uint32_t* pa_s = reinterpret_cast<uint32_t*>(lists + (size_t)kBeamTok * d * (WMAX + 1));
   int64_t E = 1;
   for (int i = 0; i < d; ++i) E *= M;
   int pa_off[4] = {0, 0, 0, 0};
@@ -71,7 +73,7 @@ k_beam_topk(const float* __restrict__ G, int64_t T, int d, int M, int k, int B,
     int64_t wo = 0, n = M;
     for (int i = 0; i < d; ++i) { pa_off[i] = (int)wo; wo += (n + 31) / 32; n *= M; }
   }
-  // all alive?  (then FilterAlive removes nothing: the unmasked search, no bitmap reads)
+  // all alive?  (then FilterAlive removes nothing: per-dimension lists + merge)
   bool dead = false;
   const int64_t aw = (E + 31) / 32;
   for (int64_t w = threadIdx.x; w < aw; w += blockDim.x) {
@@ -86,32 +88,44 @@ k_beam_topk(const float* __restrict__ G, int64_t T, int d, int M, int k, int B,
   }
   for (int64_t t0 = (int64_t)blockIdx.x * kBeamTok; t0 < T; t0 += (int64_t)gridDim.x * kBeamTok) {
     const int nt = (int)((T - t0) < kBeamTok ? (T - t0) : kBeamTok);
-    __syncthreads();  // previous tile's rows consumed (and the bitmaps built)
+    __syncthreads();  // previous tile's rows and lists consumed (and the bitmaps built)
     const float* src = G + t0 * dM;
     if ((dM & 3) == 0) {
       const int n4 = nt * dM / 4, q = dM / 4;
 #pragma unroll 4
-      for (int i = threadIdx.x; i < n4; i += kBeamTok) {
+      for (int i = threadIdx.x; i < n4; i += kBeamThreads) {
         const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
         const int r = i / q, c = (i - r * q) * 4;
         float* dst = gtile + r * pitch + c;
         dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
       }
     } else {
-      for (int i = threadIdx.x; i < nt * dM; i += kBeamTok) {
+      for (int i = threadIdx.x; i < nt * dM; i += kBeamThreads) {
         const int r = i / dM;
         gtile[r * pitch + (i - r * dM)] = __ldg(src + i);
       }
     }
     __syncthreads();
-    if ((int)threadIdx.x < nt) {
-      const int64_t t = t0 + threadIdx.x;
-      if (masked)
+    if (masked) {
+      if ((int)threadIdx.x < nt) {
+        const int64_t t = t0 + threadIdx.x;
         beam_search_row<WMAX, true>(gtile + threadIdx.x * pitch, 1, d, M, k, B, PA, pa_off, sel + t * k,
                                     sel_score + t * k);
-      else
-        beam_search_row<WMAX, false>(gtile + threadIdx.x * pitch, 1, d, M, k, B, PA, pa_off, sel + t * k,
-                                     sel_score + t * k);
+      }
+      continue;
+    }
+    // per-dimension lists, (token, level) tasks over all threads
+    for (int task = threadIdx.x; task < nt * d; task += kBeamThreads) {
+      const int r = task / d, i = task - r * d;
+      const int W = (i < d - 1) ? B : k;
+      beam_dim_list<WMAX>(gtile + r * pitch + i * M, 1, M, W + 1 < M ? W + 1 : M,
+                          lists + ((size_t)r * d + i) * (WMAX + 1));
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < nt) {
+      const int64_t t = t0 + threadIdx.x;
+      beam_merge_row<WMAX>(gtile + threadIdx.x * pitch, 1, d, M, k, B, lists + (size_t)threadIdx.x * d * (WMAX + 1),
+                           sel + t * k, sel_score + t * k);
     }
   }
 }
@@ -127,7 +141,8 @@ static dmoe_status launch_beam(const float* G, int64_t T, dmoe_grid g, const uin
                                const uint32_t* alive, int pa_words, int32_t* sel, float* sel_score,
                                cudaStream_t s) {
   const int dM = g.d * g.M;
-  size_t smem = (size_t)kBeamTok * (dM + 1) * sizeof(float);
+  size_t smem = (((size_t)kBeamTok * (dM + 1) + 1) & ~(size_t)1) * sizeof(float) +
+                (size_t)kBeamTok * g.d * (WMAX + 1) * 8;
   if (PA_global == nullptr) smem += (size_t)pa_words * 4;
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
@@ -137,7 +152,7 @@ static dmoe_status launch_beam(const float* G, int64_t T, dmoe_grid g, const uin
   int64_t blocks = ceil_div(T, kBeamTok);
   const int64_t cap = (int64_t)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  launch_pdl(k_beam_topk<WMAX>, (unsigned)blocks, kBeamTok, smem, s, G, T, g.d, g.M, g.k, g.beam, PA_global,
+  launch_pdl(k_beam_topk<WMAX>, (unsigned)blocks, kBeamThreads, smem, s, G, T, g.d, g.M, g.k, g.beam, PA_global,
                                                                    alive, pa_words, sel, sel_score);
   return check_launch("beam_topk");
 }

@@ -15,9 +15,10 @@ from . import _lib as L
 
 class DMoELayer:
     def __init__(self, d, M, k, D, H, dtype=torch.bfloat16, beam=0, T_max=4096, device="cuda",
-                 E_local=None, R_cap=None, pool=0, keep_G=False):
+                 E_local=None, R_cap=None, pool=0, keep_G=False, grads=True):
         self.d, self.M, self.k, self.D, self.H = d, M, k, D, H
         self.keep_G = keep_G  # also write the gate scores G (tests); the fused path otherwise never stores them
+        self.sgd_lr = None    # default of backward(): a learning rate here makes every step an SGD step
         self.beam = beam or k
         self.E = M ** d
         self.E_local = E_local or self.E
@@ -41,8 +42,10 @@ class DMoELayer:
         self.W2, self.b2 = e(El, D, H), e(El, D, dt=f32)
         # gradients
         self.dWg, self.dbg = e(D, dM, dt=f32), e(dM, dt=f32)
-        self.dW1, self.db1 = e(El, H, D), e(El, H, dt=f32)
-        self.dW2, self.db2 = e(El, D, H), e(El, D, dt=f32)
+        # grads=False: the layer is only stepped with the fused SGD backward (no dW buffers)
+        gE = El if grads else 1
+        self.dW1, self.db1 = e(gE, H, D), e(gE, H, dt=f32)
+        self.dW2, self.db2 = e(gE, D, H), e(gE, D, dt=f32)
         # activations / routing records (forward) and backward buffers
         T, R = T_max, self.R_cap
         self.G = e(T if keep_G else 1, dM, dt=f32)
@@ -88,15 +91,22 @@ class DMoELayer:
         return self.y[:T]
 
     # ----------------------------------------------------------------- backward
-    def backward(self, dy, sgd_lr=None, recompute=False):
+    def backward(self, dy, sgd_lr=None, recompute=False, responded_bwd=None):
         """Gradients of the layer.  sgd_lr: the runtime's Backward request semantics:
         the expert parameters are updated in place, W -= lr * dW, inside the weight-gradient GEMMs
         (dW1 / dW2 / db1 / db2 are then not written).  recompute: h is recomputed from xd in the
         backward (gradient checkpointing) instead of read from the forward's
-        buffer (SGD form only)."""
+        buffer (SGD form only).  responded_bwd: bit mask of experts whose Backward request
+        succeeds; the others are omitted from the gradient without renormalisation (reading X22)."""
         x = self._x
         T = x.shape[0]
-        L.dmoe_combine_bwd(dy, self.out, self.row_of_slot[:T], self.w[:T], self.dout, self.dscore[:T])
+        if sgd_lr is None:
+            sgd_lr = self.sgd_lr
+        if responded_bwd is not None:  # backward-only failures (reading X22)
+            L.dmoe_combine_bwd_failures(dy, self.out, self.row_of_slot[:T], self.w[:T], self.sel[:T], responded_bwd,
+                                        self.dout, self.dscore[:T])
+        else:
+            L.dmoe_combine_bwd(dy, self.out, self.row_of_slot[:T], self.w[:T], self.dout, self.dscore[:T])
         if sgd_lr is not None:
             L.dmoe_expert_ffn_bwd_sgd(self.xd, None if recompute else self.h, self.dout, self.seg, self.W1, self.b1,
                                       self.W2, self.b2, sgd_lr, self.dxd, self.ws,

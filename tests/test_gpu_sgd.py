@@ -59,5 +59,32 @@ def test_recompute_equals_saved_h():
         lay.forward(x, alive, resp)
         lay.backward(dy, sgd_lr=1e-2, recompute=rc)
     torch.cuda.synchronize()
-    for n in ("W1", "b1", "W2", "b2", "dxd", "dx", "dWg"):
+    R = int(a.offsets[cfg.E].item())
+    assert torch.equal(a.dxd[:R], b.dxd[:R])   # rows past R are capacity, never written
+    for n in ("W1", "b1", "W2", "b2", "dx", "dWg", "dbg"):
         assert torch.equal(getattr(a, n), getattr(b, n)), n
+
+
+def test_backward_only_failures_vs_oracle():
+    """NEXT-3 / reading X22 on the GPU: experts lost in the backward only (dmoe_combine_bwd_failures)."""
+    import gen
+    cfg = CONFIGS["mnist"].with_(fail_frac=0.1)
+    T = 900
+    inp = make_inputs(cfg, seed=50, T=T)
+    lay = gpu_layer(cfg, inp)
+    rb = gen.host_mask(77, gen.RESPONDED, 0.25, cfg.E)          # a second, independent draw
+    rb_u8 = gen.unpack_mask(rb, cfg.E)
+    x, dy, alive, resp = lay._inputs
+    lay.forward(x, alive, resp)
+    lay.backward(dy, responded_bwd=torch.from_numpy(rb.view(np.int32)).cuda())
+    torch.cuda.synchronize()
+    from oracle import oracle as O
+    r = O.layer_step(inp["X"], inp["Wg"], inp["bg"], inp["W1"], inp["b1"], inp["W2"], inp["b2"], inp["dY"],
+                     inp["alive"], inp["responded"], cfg.d, cfg.M, cfg.k, cfg.B, sel_override=np64(lay.sel[:T]),
+                     responded_bwd=rb_u8)
+    for n, got, want in [("dX", lay.dx[:T], r["dX"]), ("dscore", lay.dscore[:T], r["dscore"]),
+                         ("dW1", lay.dW1, r["dW1"]), ("dW2", lay.dW2, r["dW2"]), ("db1", lay.db1, r["db1"]),
+                         ("dWg", lay.dWg, r["dWg"])]:
+        assert rel_err(np64(got), want) <= TOL["bf16"], n
+    lost = np.nonzero(rb_u8 == 0)[0]
+    assert not np64(lay.dW1)[lost].any() and not np64(lay.db2)[lost].any()

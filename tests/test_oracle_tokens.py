@@ -80,3 +80,29 @@ def test_sgd_update_closed_form():
     np.testing.assert_allclose(O.sgd_update(W, W - Ws, 1.0), Ws, rtol=0, atol=1e-15)
     np.testing.assert_allclose(O.sgd_update(W, W - Ws, 0.5) - Ws, (W - Ws) / 2, rtol=0, atol=1e-15)
     assert np.array_equal(O.sgd_update(W, W - Ws, 0.0), W)
+
+
+def test_backward_only_failures():
+    """Reading X22 (SPEC.md:300/305 for PAPER.md:287): an expert lost in the backward only is
+    omitted from dx without renormalisation.  Pinned against the full step with that expert's
+    input-gradient rows subtracted afterwards, an independent formulation; the gating gradient
+    and the forward are unchanged; the lost experts get no parameter gradient."""
+    cfg = CONFIGS["mnist"].with_(D=32, H=64, fail_frac=0.1)
+    inp = make_inputs(cfg, seed=9, T=120)
+    full = _full(cfg, inp)
+    rng = np.random.default_rng(2)
+    rb = (rng.random(cfg.E) > 0.3).astype(np.uint8)
+    part = _full(cfg, inp, responded_bwd=rb)
+    for key in ("y", "dscore", "dWg", "dbg", "w", "sel"):
+        assert np.array_equal(part[key], full[key]), key
+    lost_rows = np.nonzero(rb[np.repeat(np.arange(cfg.E), full["counts"])] == 0)[0]
+    assert len(lost_rows) > 0
+    want = full["dX"].copy()
+    for r in lost_rows:
+        want[full["token_of_row"][r]] -= full["dx_rows"][r]
+    np.testing.assert_allclose(part["dX"], want, rtol=0, atol=1e-12 * np.abs(full["dX"]).max())
+    lost = np.nonzero(rb == 0)[0]
+    kept = np.nonzero(rb == 1)[0]
+    assert not part["dW1"][lost].any() and not part["dW2"][lost].any() and not part["db1"][lost].any()
+    for key in ("dW1", "dW2", "db1", "db2"):
+        assert np.array_equal(part[key][kept], full[key][kept]), key

@@ -17,6 +17,8 @@ from gen import CONFIGS  # noqa: E402
 from paper_2002_04013_b200 import _lib as L  # noqa: E402
 
 cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "mnist"]
+if len(sys.argv) > 2:  # overrides key=int, e.g. M=16 T=4096 (a transformer-shaped slice)
+    cfg = cfg.with_(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in sys.argv[2:]})
 lay, x, dy, alive, resp = bench.build_layer(cfg, 0, torch.device("cuda", 0), cfg.T)
 for _ in range(2):
     bench.run_calls(lay, x, dy, alive, resp)
