@@ -20,8 +20,8 @@ gen/libgen_host.so: gen/gen_host.c gen/counter_gen.h
 gen/libgen_device.so: gen/gen_device.cu gen/counter_gen.h
 	$(NVCC) $(NVFLAGS) -fmad=false -shared -o $@ gen/gen_device.cu
 
-oracle/liboracle.so: oracle/dmoe_oracle.c
-	gcc $(CFLAGS) -shared -o $@ oracle/dmoe_oracle.c -lm
+oracle/liboracle.so: oracle/dmoe_oracle.c oracle/dmoe_oracle_ffn3.c
+	gcc $(CFLAGS) -shared -o $@ oracle/dmoe_oracle.c oracle/dmoe_oracle_ffn3.c -lm
 
 COBJ      := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(CSRC))
 
