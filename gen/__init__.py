@@ -15,6 +15,8 @@ from .configs import CONFIGS, Config  # noqa: F401
 _HERE = os.path.dirname(os.path.abspath(__file__))
 
 X, WG, BG, W1, B1, W2, B2, DY, ALIVE, RESPONDED = range(1, 11)
+# the §4.1 expert block (NEXT-2): middle linear W2 [E,H,H] / b2 reuse W2 / B2's ids; these are new
+W3, B3, LN1G, LN1B, LN2G, LN2B = range(11, 17)
 NORMAL, UNIFORM, GRID8, ZERO = range(4)
 
 _host = None

@@ -216,6 +216,34 @@ dmoe_status dmoe_expert_ffn_bwd_sgd(const void* xd, const void* h, const uint32_
                                     int32_t H, dmoe_dtype dt, void* W1, float* b1, void* W2, float* b2,
                                     float lr, void* dxd, void* ws, size_t ws_bytes, dmoe_stream_t stream);
 
+/* S6 / S9 with the paper's own expert block (NEXT-2, §4.1: "feedforward blocks
+ * 1024 -> 4096 -> 4096 -> 1024 with layer normalization and ReLU activations in between";
+ * reading X23): per expert e over its rows
+ *   z1 = W1[e] x + b1[e];   a1 = relu(g1[e] * (z1 - mean z1) / sqrt(var z1 + eps) + be1[e])
+ *   z2 = W2[e] a1 + b2[e];  a2 = relu(g2[e] * (z2 - mean z2) / sqrt(var z2 + eps) + be2[e])
+ *   out = W3[e] a2 + b3[e]
+ * (LayerNorm over the H features, biased variance.)  W1 [E_local, H, D], W2 [E_local, H, H],
+ * W3 [E_local, D, H] bf16; b1, g1, be1, b2, g2, be2 [E_local, H] and b3 [E_local, D] fp32.
+ * Saved for the backward: z1, a1, z2, a2 [R_cap, H] bf16 and stats [2][R_cap][2] fp32 (mean,
+ * 1/std per row per LayerNorm).  The linears run on the grouped tcgen05 GEMMs, LayerNorm + ReLU
+ * as row kernels between them.  bf16 only; D, H multiples of 128, H <= 8192. */
+dmoe_status dmoe_expert_ffn3_fwd(const void* xd, const int32_t* offsets, int32_t E_local, int64_t R_cap,
+                                 int32_t D, int32_t H, dmoe_dtype dt, const void* W1, const float* b1,
+                                 const float* g1, const float* be1, const void* W2, const float* b2,
+                                 const float* g2, const float* be2, const void* W3, const float* b3, float eps,
+                                 void* z1, void* a1, void* z2, void* a2, float* stats, void* out, void* ws,
+                                 size_t ws_bytes, dmoe_stream_t stream);
+/* Its Backward request: dxd and every parameter gradient (dW1 [E_local, H, D], dW2 [E_local, H,
+ * H], dW3 [E_local, D, H] bf16; db1, dg1, dbe1, db2, dg2, dbe2 [E_local, H], db3 [E_local, D]
+ * fp32; zeros for experts without rows), from the saved z1, a1, z2, a2, stats. */
+dmoe_status dmoe_expert_ffn3_bwd(const void* xd, const void* z1, const void* a1, const void* z2, const void* a2,
+                                 const float* stats, const void* dout, const int32_t* offsets, int32_t E_local,
+                                 int64_t R_cap, int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
+                                 const float* g1, const float* be1, const void* W2, const float* g2,
+                                 const float* be2, const void* W3, void* dxd, void* dW1, float* db1, float* dg1,
+                                 float* dbe1, void* dW2, float* db2, float* dg2, float* dbe2, void* dW3,
+                                 float* db3, void* ws, size_t ws_bytes, dmoe_stream_t stream);
+
 /* S10 — undispatch + gate backward (gradient of Eq. 2 through the Eq. 3 softmax):
  *   dG[t, i*M + u_i(sel[t,s])] += dscore[t,s]            (u_i per X1)
  *   dx[t]  = sum_{ok s} dxd[row_of_slot[t,s]] + sum_j dG[t,j] W_g[:, j]

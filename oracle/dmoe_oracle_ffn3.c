@@ -35,7 +35,7 @@ void oracle_ffn3_fwd(const double* x, const int32_t* seg, int32_t S, int32_t D, 
                      const double* W1, const double* b1, const double* g1, const double* be1,
                      const double* W2, const double* b2, const double* g2, const double* be2,
                      const double* W3, const double* b3, double eps,
-                     double* z1, double* a1, double* z2, double* a2, double* out) {
+                     double* z1, double* a1, double* z2, double* a2, double* out, double* y1, double* y2) {
   #pragma omp parallel for schedule(dynamic, 1)
   for (int32_t s = 0; s < S; ++s) {
     double* xh = (double*)malloc(sizeof(double) * (size_t)H);
@@ -52,6 +52,7 @@ void oracle_ffn3_fwd(const double* x, const int32_t* seg, int32_t S, int32_t D, 
       }
       ln_row(z1 + r * H, g1 + (int64_t)s * H, be1 + (int64_t)s * H, H, eps, xh, y, &rstd);
       for (int32_t n = 0; n < H; ++n) a1[r * H + n] = y[n] > 0.0 ? y[n] : 0.0;
+      if (y1) memcpy(y1 + r * H, y, sizeof(double) * (size_t)H);
       for (int32_t m = 0; m < H; ++m) {
         double v = b2[(int64_t)s * H + m];
         for (int32_t n = 0; n < H; ++n) v += w2[(int64_t)m * H + n] * a1[r * H + n];
@@ -59,6 +60,7 @@ void oracle_ffn3_fwd(const double* x, const int32_t* seg, int32_t S, int32_t D, 
       }
       ln_row(z2 + r * H, g2 + (int64_t)s * H, be2 + (int64_t)s * H, H, eps, xh, y, &rstd);
       for (int32_t m = 0; m < H; ++m) a2[r * H + m] = y[m] > 0.0 ? y[m] : 0.0;
+      if (y2) memcpy(y2 + r * H, y, sizeof(double) * (size_t)H);
       for (int32_t c = 0; c < D; ++c) {
         double v = b3[(int64_t)s * D + c];
         for (int32_t m = 0; m < H; ++m) v += w3[(int64_t)c * H + m] * a2[r * H + m];
@@ -71,15 +73,18 @@ void oracle_ffn3_fwd(const double* x, const int32_t* seg, int32_t S, int32_t D, 
 }
 
 /* LayerNorm + ReLU backward for one row: dy = da * 1[y > 0]; dg += dy * xhat; dbe += dy;
- * dxhat = dy * g;  dz = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)) */
+ * dxhat = dy * g;  dz = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)).
+ * mask (optional, NULL = 1[y > 0]): the ReLU decisions to take instead (forced-decision parity,
+ * reading X23b: a decision within floating-point noise of y = 0 is taken from the kernel). */
 static void ln_relu_bwd_row(const double* z, const double* g, const double* be, const double* da,
                             int32_t H, double eps, double* xh, double* y, double* dz, double* dg,
-                            double* dbe) {
+                            double* dbe, const uint8_t* mask) {
   double rstd;
   ln_row(z, g, be, H, eps, xh, y, &rstd);
   double m1 = 0.0, m2 = 0.0;
   for (int32_t n = 0; n < H; ++n) {
-    const double dy = y[n] > 0.0 ? da[n] : 0.0;
+    const int on = mask ? mask[n] != 0 : y[n] > 0.0;
+    const double dy = on ? da[n] : 0.0;
     dg[n] += dy * xh[n];
     dbe[n] += dy;
     dz[n] = dy * g[n];  /* dxhat */
@@ -99,7 +104,8 @@ void oracle_ffn3_bwd(const double* x, const double* z1, const double* a1, const 
                      int32_t H, const double* W1, const double* g1, const double* be1,
                      const double* W2, const double* g2, const double* be2, const double* W3,
                      double eps, double* dx, double* dW1, double* db1, double* dg1, double* dbe1,
-                     double* dW2, double* db2, double* dg2, double* dbe2, double* dW3, double* db3) {
+                     double* dW2, double* db2, double* dg2, double* dbe2, double* dW3, double* db3,
+                     const uint8_t* m1, const uint8_t* m2) {
   #pragma omp parallel for schedule(dynamic, 1)
   for (int32_t s = 0; s < S; ++s) {
     const double* w1 = W1 + (int64_t)s * H * D;
@@ -135,7 +141,7 @@ void oracle_ffn3_bwd(const double* x, const double* z1, const double* a1, const 
         da[m] = v;
       }
       ln_relu_bwd_row(z2 + r * H, g2 + (int64_t)s * H, be2 + (int64_t)s * H, da, H, eps, xh, y, dz,
-                      dg2 + (int64_t)s * H, dbe2 + (int64_t)s * H);
+                      dg2 + (int64_t)s * H, dbe2 + (int64_t)s * H, m2 ? m2 + r * H : NULL);
       /* z2 = W2 a1 + b2 */
       for (int32_t m = 0; m < H; ++m) {
         db2[(int64_t)s * H + m] += dz[m];
@@ -147,7 +153,7 @@ void oracle_ffn3_bwd(const double* x, const double* z1, const double* a1, const 
         da[n] = v;
       }
       ln_relu_bwd_row(z1 + r * H, g1 + (int64_t)s * H, be1 + (int64_t)s * H, da, H, eps, xh, y, dz,
-                      dg1 + (int64_t)s * H, dbe1 + (int64_t)s * H);
+                      dg1 + (int64_t)s * H, dbe1 + (int64_t)s * H, m1 ? m1 + r * H : NULL);
       /* z1 = W1 x + b1 */
       for (int32_t n = 0; n < H; ++n) {
         db1[(int64_t)s * H + n] += dz[n];

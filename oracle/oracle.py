@@ -42,9 +42,10 @@ def lib():
         L.oracle_combine_bwd.argtypes = [_d, _d, _i32, _d, _I64, _I32, _I32, _d, _d]
         L.oracle_ffn_bwd.argtypes = [_d, _d, _d, _i32, _I32, _I32, _I32, _d, _d,
                                      _d, _d, _d, _d, _d]
-        L.oracle_ffn3_fwd.argtypes = [_d, _i32, _I32, _I32, _I32] + [_d] * 10 + [ctypes.c_double] + [_d] * 5
+        L.oracle_ffn3_fwd.argtypes = [_d, _i32, _I32, _I32, _I32] + [_d] * 10 + [ctypes.c_double] + [_d] * 5 + [
+            ctypes.c_void_p] * 2
         L.oracle_ffn3_bwd.argtypes = ([_d] * 6 + [_i32, _I32, _I32, _I32] + [_d] * 7 + [ctypes.c_double]
-                                      + [_d] * 11)
+                                      + [_d] * 11 + [ctypes.c_void_p] * 2)
         L.oracle_gate_bwd.argtypes = [_d, _d, _i32, _d, _d, _i32, _I64, _I32, _I32, _I32, _I32,
                                       _d, _d, _d]
         _lib = L
@@ -278,24 +279,29 @@ def sgd_update(param, grad, lr):
 LN_EPS = 1e-5   # reading X23 (PyTorch LayerNorm default)
 
 
-def ffn3_fwd(x_rows, seg, P, eps=LN_EPS):
+def ffn3_fwd(x_rows, seg, P, eps=LN_EPS, pre_relu=False):
     """The §4.1 block: Linear -> LayerNorm -> ReLU -> Linear -> LayerNorm -> ReLU ->
     Linear, per slot segment (dmoe_oracle_ffn3.c).  P: dict W1 [S,H,D], b1, g1, be1 [S,H], W2
-    [S,H,H], b2, g2, be2 [S,H], W3 [S,D,H], b3 [S,D].  Returns z1, a1, z2, a2 [R,H], out [R,D]."""
+    [S,H,H], b2, g2, be2 [S,H], W3 [S,D,H], b3 [S,D].  Returns z1, a1, z2, a2 [R,H], out [R,D]
+    (+ the pre-ReLU LayerNorm outputs y1, y2 when pre_relu)."""
     x_rows = _c(x_rows, np.float64)
     R, D = x_rows.shape
     S, H, _ = P["W1"].shape
     z1, a1, z2, a2 = (np.empty((max(R, 1), H)) for _ in range(4))
     out = np.empty((max(R, 1), D))
     args = [_c(P[n], np.float64) for n in ("W1", "b1", "g1", "be1", "W2", "b2", "g2", "be2", "W3", "b3")]
+    y1, y2 = np.empty((max(R, 1), H)), np.empty((max(R, 1), H))
     lib().oracle_ffn3_fwd(x_rows if R else np.zeros((1, D)), _c(seg, np.int32), S, D, H, *args, float(eps),
-                          z1, a1, z2, a2, out)
+                          z1, a1, z2, a2, out, y1.ctypes.data, y2.ctypes.data)
+    if pre_relu:
+        return z1[:R], a1[:R], z2[:R], a2[:R], out[:R], y1[:R], y2[:R]
     return z1[:R], a1[:R], z2[:R], a2[:R], out[:R]
 
 
-def ffn3_bwd(x_rows, z1, a1, z2, a2, g_rows, seg, P, eps=LN_EPS):
+def ffn3_bwd(x_rows, z1, a1, z2, a2, g_rows, seg, P, eps=LN_EPS, masks=None):
     """Backward of ffn3_fwd with row cotangents g_rows [R,D]: dx rows and every parameter gradient
-    (dict with keys dW1, db1, dg1, dbe1, dW2, db2, dg2, dbe2, dW3, db3)."""
+    (dict with keys dW1, db1, dg1, dbe1, dW2, db2, dg2, dbe2, dW3, db3).  masks: optional (m1, m2)
+    uint8 [R,H] ReLU decisions to take instead of 1[y > 0] (forced-decision parity, X23b)."""
     x_rows = _c(x_rows, np.float64)
     R, D = x_rows.shape
     S, H, _ = P["W1"].shape
@@ -307,13 +313,17 @@ def ffn3_bwd(x_rows, z1, a1, z2, a2, g_rows, seg, P, eps=LN_EPS):
     lib().oracle_ffn3_bwd(z(x_rows, D), z(z1, H), z(a1, H), z(z2, H), z(a2, H), z(g_rows, D), _c(seg, np.int32),
                           S, D, H, *[_c(P[n], np.float64) for n in ("W1", "g1", "be1", "W2", "g2", "be2", "W3")],
                           float(eps), dx, *[G[n] for n in ("dW1", "db1", "dg1", "dbe1", "dW2", "db2", "dg2", "dbe2",
-                                                             "dW3", "db3")])
+                                                             "dW3", "db3")],
+                          *((None, None) if masks is None or not R else
+                            (_c(masks[0], np.uint8).ctypes.data, _c(masks[1], np.uint8).ctypes.data)))
     return dx[:R], G
 
 
-def layer_step_ffn3(X, Wg, bg, P, dY, alive, responded, d, M, k, B, sel_override=None, eps=LN_EPS):
+def layer_step_ffn3(X, Wg, bg, P, dY, alive, responded, d, M, k, B, sel_override=None, eps=LN_EPS,
+                    relu_override=None):
     """layer_step with the paper's §4.1 expert block (ffn3_fwd / ffn3_bwd) in place of the
-    2-linear FFN; routing, weights, dispatch, combine and the gate gradient are the same steps."""
+    2-linear FFN; routing, weights, dispatch, combine and the gate gradient are the same steps.
+    relu_override(y1, y2) -> (m1, m2): the ReLU decisions the backward takes (X23b)."""
     E = M ** d
     G = gate_scores(X, Wg, bg)
     sel, sc, gap = select_experts(G, d, M, k, B, alive)
@@ -323,11 +333,13 @@ def layer_step_ffn3(X, Wg, bg, P, dY, alive, responded, d, M, k, B, sel_override
     w, ok, valid, nd = weights(sel, sc, responded)
     counts, offsets, ros, tor = dispatch(sel, ok, E)
     x_rows = np.asarray(X, np.float64)[tor]
-    z1, a1, z2, a2, out = ffn3_fwd(x_rows, offsets, P, eps)
+    z1, a1, z2, a2, out, y1, y2 = ffn3_fwd(x_rows, offsets, P, eps, pre_relu=True)
     y = combine(out, ros, w)
     g, dscore = combine_bwd(dY, out, ros, w)
-    dx_rows, grads = ffn3_bwd(x_rows, z1, a1, z2, a2, g, offsets, P, eps)
+    masks = relu_override(y1, y2) if relu_override is not None else None
+    dx_rows, grads = ffn3_bwd(x_rows, z1, a1, z2, a2, g, offsets, P, eps, masks=masks)
     dX, dWg, dbg = gate_bwd(X, Wg, sel, dscore, dx_rows, ros, d, M)
     return dict(G=G, sel=sel, sel_score=sc, gap=gap, w=w, ok=ok, valid=valid, n_dropped=nd, counts=counts,
-                offsets=offsets, row_of_slot=ros, token_of_row=tor, z1=z1, a1=a1, z2=z2, a2=a2, out=out, y=y,
+                offsets=offsets, row_of_slot=ros, token_of_row=tor, z1=z1, a1=a1, z2=z2, a2=a2, y1=y1, y2=y2,
+                out=out, y=y,
                 g_rows=g, dscore=dscore, dx_rows=dx_rows, dX=dX, dWg=dWg, dbg=dbg, **grads)

@@ -59,6 +59,9 @@ _SIGS = {
                              _SZ, _P], ctypes.c_int),
     "dmoe_expert_ffn_bwd_sgd": ([_P, _P, _P, _P, _P, _I32, _I64, _I32, _I32, _I32, _P, _P, _P, _P, ctypes.c_float,
                                  _P, _P, _SZ, _P], ctypes.c_int),
+    "dmoe_expert_ffn3_fwd": ([_P, _P, _I32, _I64, _I32, _I32, _I32] + [_P] * 10 + [ctypes.c_float] + [_P] * 6
+                             + [_P, _SZ, _P], ctypes.c_int),
+    "dmoe_expert_ffn3_bwd": ([_P] * 8 + [_I32, _I64, _I32, _I32, _I32] + [_P] * 19 + [_SZ, _P], ctypes.c_int),
     "dmoe_gate_bwd": ([_P, _P, _P, _P, _P, _P, _I64, _I32, dmoe_grid, _I32, _P, _P, _P, _P, _SZ, _P],
                       ctypes.c_int),
     "dmoe_segment_offsets": ([_P, _I32, _I32, _P, _P], ctypes.c_int),
@@ -190,6 +193,25 @@ def dmoe_expert_ffn_bwd_sgd(xd, h, dout, offsets, W1, b1, W2, b2, lr, dxd, ws, h
     _check("dmoe_expert_ffn_bwd_sgd", _L.dmoe_expert_ffn_bwd_sgd(
         _p(xd), _p(h), _p(hmask), _p(dout), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd), _p(W1), _p(b1),
         _p(W2), _p(b2), float(lr), _p(dxd), _p(ws), ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_expert_ffn3_fwd(xd, offsets, P, eps, z1, a1, z2, a2, stats, out, ws):
+    """P: dict of the block's parameters W1, b1, g1, be1, W2, b2, g2, be2, W3, b3 (layer.py)."""
+    E_local, H, D = P["W1"].shape
+    _check("dmoe_expert_ffn3_fwd", _L.dmoe_expert_ffn3_fwd(
+        _p(xd), _p(offsets), E_local, xd.shape[0], D, H, _dt(xd),
+        *[_p(P[n]) for n in ("W1", "b1", "g1", "be1", "W2", "b2", "g2", "be2", "W3", "b3")], float(eps),
+        _p(z1), _p(a1), _p(z2), _p(a2), _p(stats), _p(out), _p(ws), ws.numel() * ws.element_size(), _stream()))
+
+
+def dmoe_expert_ffn3_bwd(xd, z1, a1, z2, a2, stats, dout, offsets, P, dxd, Gr, ws):
+    """Gr: dict of gradient buffers dW1, db1, dg1, dbe1, dW2, db2, dg2, dbe2, dW3, db3."""
+    E_local, H, D = P["W1"].shape
+    _check("dmoe_expert_ffn3_bwd", _L.dmoe_expert_ffn3_bwd(
+        _p(xd), _p(z1), _p(a1), _p(z2), _p(a2), _p(stats), _p(dout), _p(offsets), E_local, xd.shape[0], D, H,
+        _dt(xd), *[_p(P[n]) for n in ("W1", "g1", "be1", "W2", "g2", "be2", "W3")], _p(dxd),
+        *[_p(Gr[n]) for n in ("dW1", "db1", "dg1", "dbe1", "dW2", "db2", "dg2", "dbe2", "dW3", "db3")],
+        _p(ws), ws.numel() * ws.element_size(), _stream()))
 
 
 def dmoe_gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, g, dx, dWg, dbg, ws):

@@ -70,6 +70,10 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
                      size_t ws_bytes, cudaStream_t s);
 
 dmoe_status segment_offsets(const int32_t* offsets, int64_t E, int group, int32_t* seg, cudaStream_t s);
+dmoe_status ln_relu_fwd(const void* z, const int32_t* offsets, int E, int64_t R_cap, int H, float eps,
+                        const float* g, const float* be, void* a, float* stats, cudaStream_t s);
+dmoe_status ln_relu_bwd(const void* da, const void* z, const float* stats, const int32_t* offsets, int E, int H,
+                        const float* g, const float* be, void* dz, float* dg, float* dbe, cudaStream_t s);
 dmoe_status exchange_layout(const int32_t* counts, int G, int El, int32_t* offsets,
                             int32_t* src_of_dst, int64_t R_cap, void* ws, size_t ws_bytes, cudaStream_t s);
 dmoe_status permute_rows(const void* src, const int32_t* idx, const int32_t* n_rows, int32_t D,
@@ -548,6 +552,87 @@ dmoe_status dmoe_expert_ffn_bwd_sgd(const void* xd, const void* h, const uint32_
   if (tc_segk2_supported(g5, g6)) return tc_gemm_segk2(g5, g6, s);
   DMOE_TRY(tc_gemm_segk(g5, s));
   return tc_gemm_segk(g6, s);
+}
+
+// ------------------------------------------------------------- NEXT-2: the §4.1 expert block
+static dmoe_status ffn3_check(dmoe_dtype dt, int32_t D, int32_t H, int32_t E_local, int64_t R_cap) {
+  DMOE_REQUIRE(dt == DMOE_BF16, DMOE_ERR_UNSUPPORTED, "expert_ffn3: bf16 only");
+  DMOE_REQUIRE(E_local >= 1 && R_cap >= 0 && D % 128 == 0 && H % 128 == 0 && H <= 8192, DMOE_ERR_SHAPE,
+               "expert_ffn3: E_local=%d D=%d H=%d (D, H multiples of 128, H <= 8192)", E_local, D, H);
+  GemmRows g{};
+  g.E = E_local; g.N = H; g.K = D; g.rows_cap = R_cap; g.offsets = reinterpret_cast<const int32_t*>(16);
+  g.epi = EPI_BIAS;
+  DMOE_REQUIRE(tc_rows_supported(g), DMOE_ERR_UNSUPPORTED, "expert_ffn3: tensor-core path unavailable");
+  return DMOE_OK;
+}
+
+static GemmRows rows_for(const void* A, const void* B, void* C, const float* bias, const int32_t* offsets, int E,
+                         int N, int K, int64_t R_cap, bool b_mn, int epi, int32_t* plan) {
+  GemmRows g{};
+  g.A = A; g.B = B; g.C = C; g.bias = bias; g.aux = nullptr; g.offsets = offsets;
+  g.E = E; g.N = N; g.K = K; g.rows_cap = R_cap; g.b_mn = b_mn; g.epi = epi;
+  g.plan = E <= tc_plan_in_kernel_max() ? nullptr : plan;
+  g.max_tiles = ceil_div(R_cap, tc_rows_tile(g)) + E;
+  return g;
+}
+
+dmoe_status dmoe_expert_ffn3_fwd(const void* xd, const int32_t* offsets, int32_t E_local, int64_t R_cap,
+                                 int32_t D, int32_t H, dmoe_dtype dt, const void* W1, const float* b1,
+                                 const float* g1, const float* be1, const void* W2, const float* b2,
+                                 const float* g2, const float* be2, const void* W3, const float* b3, float eps,
+                                 void* z1, void* a1, void* z2, void* a2, float* stats, void* out, void* ws,
+                                 size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_TRY(ffn3_check(dt, D, H, E_local, R_cap));
+  NN(offsets); NN(W1); NN(b1); NN(g1); NN(be1); NN(W2); NN(b2); NN(g2); NN(be2); NN(W3); NN(b3); NN(ws);
+  if (R_cap > 0) { NN(xd); NN(z1); NN(a1); NN(z2); NN(a2); NN(stats); NN(out); }
+  cudaStream_t s = (cudaStream_t)stream;
+  Carver cv(ws, ws_bytes);
+  int32_t* plan = cv.take<int32_t>(E_local + 1);
+  DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "expert_ffn3_fwd: workspace too small");
+  if (E_local > tc_plan_in_kernel_max()) DMOE_TRY(tile_plan(offsets, E_local, TC_ROWS_TILE_DEFAULT, plan, s));
+  // z1 = W1 x + b1 -> a1 = relu(LN1(z1)) -> z2 = W2 a1 + b2 -> a2 = relu(LN2(z2)) -> out = W3 a2 + b3
+  DMOE_TRY(tc_gemm_rows(rows_for(xd, W1, z1, b1, offsets, E_local, H, D, R_cap, false, EPI_BIAS, plan), s));
+  DMOE_TRY(ln_relu_fwd(z1, offsets, E_local, R_cap, H, eps, g1, be1, a1, stats, s));
+  DMOE_TRY(tc_gemm_rows(rows_for(a1, W2, z2, b2, offsets, E_local, H, H, R_cap, false, EPI_BIAS, plan), s));
+  DMOE_TRY(ln_relu_fwd(z2, offsets, E_local, R_cap, H, eps, g2, be2, a2, stats + 2 * (R_cap > 0 ? R_cap : 1), s));
+  return tc_gemm_rows(rows_for(a2, W3, out, b3, offsets, E_local, D, H, R_cap, false, EPI_BIAS, plan), s);
+}
+
+dmoe_status dmoe_expert_ffn3_bwd(const void* xd, const void* z1, const void* a1, const void* z2, const void* a2,
+                                 const float* stats, const void* dout, const int32_t* offsets, int32_t E_local,
+                                 int64_t R_cap, int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
+                                 const float* g1, const float* be1, const void* W2, const float* g2,
+                                 const float* be2, const void* W3, void* dxd, void* dW1, float* db1, float* dg1,
+                                 float* dbe1, void* dW2, float* db2, float* dg2, float* dbe2, void* dW3,
+                                 float* db3, void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_TRY(ffn3_check(dt, D, H, E_local, R_cap));
+  NN(offsets); NN(W1); NN(g1); NN(be1); NN(W2); NN(g2); NN(be2); NN(W3); NN(dW1); NN(db1); NN(dg1); NN(dbe1);
+  NN(dW2); NN(db2); NN(dg2); NN(dbe2); NN(dW3); NN(db3); NN(ws);
+  if (R_cap > 0) { NN(xd); NN(z1); NN(a1); NN(z2); NN(a2); NN(stats); NN(dout); NN(dxd); }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t Rc = R_cap > 0 ? R_cap : 1;
+  Carver cv(ws, ws_bytes);
+  int32_t* plan = cv.take<int32_t>(E_local + 1);
+  void* da = cv.take<char>((size_t)Rc * H * 2);
+  void* dz = cv.take<char>((size_t)Rc * H * 2);
+  DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "expert_ffn3_bwd: workspace too small (%zu < %zu)", ws_bytes, cv.used);
+  if (E_local > tc_plan_in_kernel_max()) DMOE_TRY(tile_plan(offsets, E_local, TC_ROWS_TILE_DEFAULT, plan, s));
+  // out = W3 a2 + b3:  da2 = dout W3;  dW3 = dout^T a2, db3 = sum dout
+  DMOE_TRY(tc_gemm_rows(rows_for(dout, W3, da, nullptr, offsets, E_local, H, D, R_cap, true, EPI_PLAIN, plan), s));
+  GemmSegK g3{dout, a2, dW3, offsets, E_local, D, H, R_cap, db3};
+  DMOE_TRY(tc_gemm_segk(g3, s));
+  // a2 = relu(LN2(z2)):  dz2, dg2, dbe2
+  DMOE_TRY(ln_relu_bwd(da, z2, stats + 2 * Rc, offsets, E_local, H, g2, be2, dz, dg2, dbe2, s));
+  // z2 = W2 a1 + b2:  da1 = dz2 W2;  dW2 = dz2^T a1, db2 = sum dz2
+  GemmSegK g2s{dz, a1, dW2, offsets, E_local, H, H, R_cap, db2};
+  DMOE_TRY(tc_gemm_segk(g2s, s));
+  DMOE_TRY(tc_gemm_rows(rows_for(dz, W2, da, nullptr, offsets, E_local, H, H, R_cap, true, EPI_PLAIN, plan), s));
+  // a1 = relu(LN1(z1)):  dz1, dg1, dbe1
+  DMOE_TRY(ln_relu_bwd(da, z1, stats, offsets, E_local, H, g1, be1, dz, dg1, dbe1, s));
+  // z1 = W1 x + b1:  dxd = dz1 W1;  dW1 = dz1^T xd, db1 = sum dz1
+  GemmSegK g1s{dz, xd, dW1, offsets, E_local, H, D, R_cap, db1};
+  DMOE_TRY(tc_gemm_segk(g1s, s));
+  return tc_gemm_rows(rows_for(dz, W1, dxd, nullptr, offsets, E_local, D, H, R_cap, true, EPI_PLAIN, plan), s);
 }
 
 dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, const float* dscore,

@@ -60,6 +60,7 @@ dmoe_status tc_gemm_rows(const GemmRows& g, cudaStream_t s);
 dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s);
 bool tc_rows_supported(const GemmRows& g);
 int tc_rows_tile(const GemmRows& g);       // token rows per tile of the row engine (plan granularity)
+constexpr int TC_ROWS_TILE_DEFAULT = 128;  // == tc_rows_tile() of the M-major row engine
 int tc_plan_in_kernel_max();               // experts up to which the M-major engine plans row tiles itself
 bool tc_rows_mmajor();                     // the M-major row engine (not the swap-AB experiment) runs them
 bool tc_segk_supported(const GemmSegK& g);

@@ -15,7 +15,7 @@ from . import _lib as L
 
 class DMoELayer:
     def __init__(self, d, M, k, D, H, dtype=torch.bfloat16, beam=0, T_max=4096, device="cuda",
-                 E_local=None, R_cap=None, pool=0, keep_G=False, grads=True):
+                 E_local=None, R_cap=None, pool=0, keep_G=False, grads=True, expert="ffn2", ln_eps=1e-5):
         self.d, self.M, self.k, self.D, self.H = d, M, k, D, H
         self.keep_G = keep_G  # also write the gate scores G (tests); the fused path otherwise never stores them
         self.sgd_lr = None    # default of backward(): a learning rate here makes every step an SGD step
@@ -37,13 +37,24 @@ class DMoELayer:
         El = self.P
         e = lambda *s, dt=dtype: torch.empty(*s, dtype=dt, device=dev)
         # parameters (filled by the caller / generator)
+        self.expert, self.ln_eps = expert, ln_eps
         self.Wg, self.bg = e(D, dM), e(dM, dt=f32)
-        self.W1, self.b1 = e(El, H, D), e(El, H, dt=f32)
-        self.W2, self.b2 = e(El, D, H), e(El, D, dt=f32)
+        if expert == "ffn3":  # the paper's block: D -> H -> H -> D with LayerNorm + ReLU
+            self.P3 = {"W1": e(El, H, D), "b1": e(El, H, dt=f32), "g1": e(El, H, dt=f32), "be1": e(El, H, dt=f32),
+                      "W2": e(El, H, H), "b2": e(El, H, dt=f32), "g2": e(El, H, dt=f32), "be2": e(El, H, dt=f32),
+                      "W3": e(El, D, H), "b3": e(El, D, dt=f32)}
+            self.Gr = {"d" + n: torch.empty_like(v) for n, v in self.P3.items()}
+            R0 = max(self.R_cap, 1)
+            self.z1, self.a1, self.z2, self.a2 = e(R0, H), e(R0, H), e(R0, H), e(R0, H)
+            self.stats = e(2, R0, 2, dt=f32)
+            self.W1, self.b1, self.W2, self.b2 = self.P3["W1"], self.P3["b1"], self.P3["W2"], self.P3["b2"]
+        else:
+            self.W1, self.b1 = e(El, H, D), e(El, H, dt=f32)
+            self.W2, self.b2 = e(El, D, H), e(El, D, dt=f32)
         # gradients
         self.dWg, self.dbg = e(D, dM, dt=f32), e(dM, dt=f32)
         # grads=False: the layer is only stepped with the fused SGD backward (no dW buffers)
-        gE = El if grads else 1
+        gE = El if (grads and expert == "ffn2") else 1   # the 2-linear expert's gradient buffers
         self.dW1, self.db1 = e(gE, H, D), e(gE, H, dt=f32)
         self.dW2, self.db2 = e(gE, D, H), e(gE, D, dt=f32)
         # activations / routing records (forward) and backward buffers
@@ -61,9 +72,10 @@ class DMoELayer:
         self.row_of_slot = e(T, k, dt=torch.int32)
         self.token_of_row = e(max(T * k, 1), dt=torch.int32)
         self.xd = e(max(R, 1), D)
-        self.h = e(max(R, 1), H)
+        R2 = max(R, 1) if expert == "ffn2" else 1
+        self.h = e(R2, H)
         # packed ReLU record [H/32, R_cap] (forward -> backward): 1/16 of h's bytes for dh's mask
-        self.hmask = e((H + 31) // 32, max(R, 1), dt=torch.int32)
+        self.hmask = e((H + 31) // 32, R2, dt=torch.int32)
         self.out = e(max(R, 1), D)
         self.y = e(T, D)
         self.dout = e(max(R, 1), D)
@@ -85,8 +97,12 @@ class DMoELayer:
                         self.xd, self.ws)
         if self.tie > 1:
             L.dmoe_segment_offsets(self.offsets, self.tie, self.seg)
-        L.dmoe_expert_ffn_fwd(self.xd, self.seg, self.W1, self.b1, self.W2, self.b2, self.h, self.out,
-                              self.ws, hmask=self.hmask)
+        if self.expert == "ffn3":
+            L.dmoe_expert_ffn3_fwd(self.xd, self.seg, self.P3, self.ln_eps, self.z1, self.a1, self.z2, self.a2,
+                                   self.stats, self.out, self.ws)
+        else:
+            L.dmoe_expert_ffn_fwd(self.xd, self.seg, self.W1, self.b1, self.W2, self.b2, self.h, self.out,
+                                  self.ws, hmask=self.hmask)
         L.dmoe_combine(self.out, self.row_of_slot[:T], self.w[:T], self.valid[:T], self.y[:T])
         return self.y[:T]
 
@@ -107,7 +123,11 @@ class DMoELayer:
                                         self.dout, self.dscore[:T])
         else:
             L.dmoe_combine_bwd(dy, self.out, self.row_of_slot[:T], self.w[:T], self.dout, self.dscore[:T])
-        if sgd_lr is not None:
+        if self.expert == "ffn3":
+            assert sgd_lr is None, "fused SGD is implemented for the 2-linear expert"
+            L.dmoe_expert_ffn3_bwd(self.xd, self.z1, self.a1, self.z2, self.a2, self.stats, self.dout, self.seg,
+                                   self.P3, self.dxd, self.Gr, self.ws)
+        elif sgd_lr is not None:
             L.dmoe_expert_ffn_bwd_sgd(self.xd, None if recompute else self.h, self.dout, self.seg, self.W1, self.b1,
                                       self.W2, self.b2, sgd_lr, self.dxd, self.ws,
                                       hmask=None if recompute else self.hmask)
