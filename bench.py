@@ -47,41 +47,49 @@ def load_peaks():
 
 # ------------------------------------------------------------------ algorithmic work
 def step_work(cfg, R):
-    """Algorithmic FLOPs and HBM bytes of one layer step, R = dispatched rows."""
-    T, D, H, k, dM, E = cfg.T, cfg.D, cfg.H, cfg.k, cfg.dM, cfg.E
+    """Algorithmic FLOPs and weight bytes of one layer step, R = dispatched rows."""
+    T, D, H, dM = cfg.T, cfg.D, cfg.H, cfg.dM
     es = 2 if cfg.dtype == "bf16" else 4
-    flops = 12.0 * R * D * H + 6.0 * T * D * dM
-    wbytes = E * 2 * D * H * es
+    mac = (2 * D * H + H * H) if cfg.expert == "ffn3" else 2 * D * H
+    flops = 6.0 * R * mac + 6.0 * T * D * dM
+    wbytes = cfg.P * mac * es
     return flops, wbytes
 
 
 def call_bytes(cfg, name, R, E_act):
-    """Algorithmic bytes moved by one ABI call (inputs read once + outputs written once)."""
+    """Algorithmic bytes moved by one ABI call (method I/O: inputs read once + outputs written
+    once; design intermediates such as G, dh or the LayerNorm gradients' scratch are not counted)."""
     T, D, H, k, dM, E = cfg.T, cfg.D, cfg.H, cfg.k, cfg.dM, cfg.E
     es = 2 if cfg.dtype == "bf16" else 4
-    W = cfg.P * D * H * es  # one weight matrix of all parameter slots (experts, or the tied pool)
-    E = cfg.P               # E_act counts slots with rows
+    E = cfg.P               # parameter slots; E_act counts the slots with rows
+    if cfg.expert == "ffn3":  # W1 [H,D], W2 [H,H], W3 [D,H]; saved z1, a1, z2, a2; LN + bias vectors
+        Wall = cfg.P * (2 * D * H + H * H) * es
+        vec = cfg.P * (6 * H + D) * 4
+        fwd = R * D * es + Wall * E_act / E + 4 * R * H * es + R * D * es
+        bwd = R * D * es * 2 + 4 * R * H * es + Wall * E_act / E + R * D * es + Wall + vec
+    else:
+        W2l = 2 * cfg.P * D * H * es  # both weight matrices of all slots
+        # read xd, W1, W2; write h, out (slots with no rows read no weights)
+        fwd = R * D * es + W2l * E_act / E + R * H * es + R * D * es
+        # read xd, h, dout, W1, W2 (slots with rows); write dxd, dW1, dW2 (all slots), db1, db2
+        bwd = R * D * es * 2 + R * H * es + W2l * E_act / E + R * D * es + W2l + E * (D + H) * 4
     return {
-        # read x, W_g; write sel, sel_score (G stays on chip in the fused call)
+        # read x, W_g; write sel, sel_score (G is an intermediate, L2-resident between the calls)
         "gate_topk": T * D * es + D * dM * es + T * k * 8,
         "dispatch": T * k * 8 + T * k * 9 + R * 4 + T * D * es + R * D * es,
-        # read xd, W1, W2; write h, out (experts with no rows read no weights)
-        "expert_ffn_fwd": R * D * es + 2 * W * E_act / E + R * H * es + R * D * es,
+        "expert_ffn_fwd": fwd,
         "combine": R * D * es + T * k * 8 + T + T * D * es,
         "combine_bwd": T * D * es + R * D * es + T * k * 8 + R * D * es + T * k * 4,
-        # method I/O: read xd, h, dout, W1, W2 (experts with rows); write dxd, dW1, dW2 (all
-        # experts), db1, db2.  The dh intermediate (written and re-read inside the call) is a
-        # design choice, not method I/O, and is not counted.
-        "expert_ffn_bwd": R * D * es * 2 + R * H * es + 2 * W * E_act / E + R * D * es + 2 * W
-        + E * (D + H) * 4,
+        "expert_ffn_bwd": bwd,
         "gate_bwd": T * D * es * 2 + R * D * es + T * k * 8 + T * D * es + D * dM * 4,
     }[name]
 
 
 def call_flops(cfg, name, R):
     T, D, H, dM = cfg.T, cfg.D, cfg.H, cfg.dM
-    return {"gate_topk": 2.0 * T * D * dM, "expert_ffn_fwd": 4.0 * R * D * H,
-            "expert_ffn_bwd": 8.0 * R * D * H, "gate_bwd": 4.0 * T * D * dM}.get(name, 0.0)
+    mac = (2 * D * H + H * H) if cfg.expert == "ffn3" else 2 * D * H   # multiply-adds per row, forward
+    return {"gate_topk": 2.0 * T * D * dM, "expert_ffn_fwd": 2.0 * R * mac,
+            "expert_ffn_bwd": 4.0 * R * mac, "gate_bwd": 4.0 * T * D * dM}.get(name, 0.0)
 
 
 # ------------------------------------------------------------------ clocks sampler
@@ -137,11 +145,18 @@ def build_layer(cfg, seed, device, T):
     from paper_2002_04013_b200 import DMoELayer
     dt = torch.bfloat16 if cfg.dtype == "bf16" else torch.float32
     lay = DMoELayer(cfg.d, cfg.M, cfg.k, cfg.D, cfg.H, dtype=dt, beam=cfg.beam, T_max=T, device=device,
-                    pool=cfg.pool, grads=not cfg.chunk)
+                    pool=cfg.pool, grads=not cfg.chunk, expert=cfg.expert)
     for t, tid in ((lay.Wg, gen.WG), (lay.bg, gen.BG), (lay.W1, gen.W1), (lay.b1, gen.B1), (lay.W2, gen.W2),
                    (lay.b2, gen.B2)):
         dist, scale = cfg.dist(tid)
         gen.dev_fill(t, seed, tid, dist, scale)
+    if cfg.expert == "ffn3":  # the block's middle / last linears and LayerNorm parameters
+        sH = float(np.float32(1.0 / math.sqrt(cfg.H)))
+        for name, tid, dist, scale in (("W2", gen.W2, gen.UNIFORM, sH), ("W3", gen.W3, gen.UNIFORM, sH),
+                                       ("b3", gen.B3, gen.UNIFORM, sH), ("g1", gen.LN1G, gen.UNIFORM, 1.5),
+                                       ("be1", gen.LN1B, gen.UNIFORM, 0.5), ("g2", gen.LN2G, gen.UNIFORM, 1.5),
+                                       ("be2", gen.LN2B, gen.UNIFORM, 0.5)):
+            gen.dev_fill(lay.P3[name], seed, tid, dist, scale)
     x = torch.empty(T, cfg.D, dtype=dt, device=device)
     dy = torch.empty(T, cfg.D, dtype=dt, device=device)
     gen.dev_fill(x, seed, gen.X, *cfg.dist(gen.X))
@@ -168,12 +183,16 @@ def run_calls(lay, x, dy, alive, resp, ev=None):
         lambda: L.dmoe_dispatch(x, g, lay.sel[:T], lay.sel_score[:T], resp, lay.w[:T], lay.valid[:T], lay.n_dropped,
                                 lay.counts, lay.offsets, lay.row_of_slot[:T], lay.token_of_row, lay.xd, lay.ws),
         lambda: (L.dmoe_segment_offsets(lay.offsets, lay.tie, lay.seg) if lay.tie > 1 else None,
+                 L.dmoe_expert_ffn3_fwd(lay.xd, lay.seg, lay.P3, lay.ln_eps, lay.z1, lay.a1, lay.z2, lay.a2,
+                                        lay.stats, lay.out, lay.ws) if lay.expert == "ffn3" else
                  L.dmoe_expert_ffn_fwd(lay.xd, lay.seg, lay.W1, lay.b1, lay.W2, lay.b2, lay.h, lay.out, lay.ws,
                                        hmask=lay.hmask)),
         lambda: L.dmoe_combine(lay.out, lay.row_of_slot[:T], lay.w[:T], lay.valid[:T], lay.y[:T]),
         lambda: L.dmoe_combine_bwd(dy, lay.out, lay.row_of_slot[:T], lay.w[:T], lay.dout, lay.dscore[:T]),
-        lambda: L.dmoe_expert_ffn_bwd(lay.xd, lay.h, lay.dout, lay.seg, lay.W1, lay.W2, lay.dxd, lay.dW1,
-                                      lay.db1, lay.dW2, lay.db2, lay.ws, hmask=lay.hmask),
+        lambda: L.dmoe_expert_ffn3_bwd(lay.xd, lay.z1, lay.a1, lay.z2, lay.a2, lay.stats, lay.dout, lay.seg, lay.P3,
+                                       lay.dxd, lay.Gr, lay.ws) if lay.expert == "ffn3" else
+        L.dmoe_expert_ffn_bwd(lay.xd, lay.h, lay.dout, lay.seg, lay.W1, lay.W2, lay.dxd, lay.dW1,
+                              lay.db1, lay.dW2, lay.db2, lay.ws, hmask=lay.hmask),
         lambda: L.dmoe_gate_bwd(x, lay.Wg, lay.sel[:T], lay.dscore[:T], lay.dxd, lay.row_of_slot[:T], g,
                                 lay.dx[:T], lay.dWg, lay.dbg, lay.ws),
     ]

@@ -27,6 +27,7 @@ class Config:
     beam: int = 0            # beam width B (0 -> k, the paper's Alg. 1)
     exact_grid: bool = False
     pool: int = 0            # parameter slots of the tied-weight pool (0 -> E, no tying; X20)
+    expert: str = "ffn2"     # "ffn2": D -> H -> D (X14); "ffn3": the paper's §4.1 block (X23)
     chunk: int = 0           # bench: tokens per layer call when the step does not fit one call
                              # (each chunk is a Backward request with the fused SGD update)
 
@@ -78,6 +79,13 @@ CONFIGS = {
     "mnist": Config("mnist", M=16, d=2, D=256, H=1024, k=4, T=4096, dtype="bf16", fail_frac=0.10),
     "transformer": Config("transformer", M=64, d=2, D=1024, H=4096, k=4, T=65536, dtype="bf16"),
     "grid3d": Config("grid3d", M=16, d=3, D=1024, H=4096, k=4, T=262144, dtype="bf16"),
+    # the paper's own expert block (§4.1: D -> H -> H -> D with LayerNorm + ReLU;
+    # NEXT-2) on the MNIST-style layer, and on the Transformer layer with a 1024-slot tied pool
+    # (4096 distinct blocks would need 206 GB of weights alone)
+    "mnist_block": Config("mnist_block", M=16, d=2, D=256, H=1024, k=4, T=4096, dtype="bf16", fail_frac=0.10,
+                          expert="ffn3"),
+    "transformer_block": Config("transformer_block", M=64, d=2, D=1024, H=4096, k=4, T=65536, dtype="bf16",
+                                expert="ffn3", pool=1024),
     # 1M tokens per GPU: 8 calls of 131,072 tokens, each a full fwd + bwd with the runtime's SGD
     # update; 512 parameter slots (the tied pool SURVEY §8(d) declares for G <= 2)
     "stress": Config("stress", M=64, d=2, D=2048, H=8192, k=8, T=1048576, dtype="bf16", fail_frac=0.30,
