@@ -219,6 +219,13 @@ static dmoe_status plans_for(GemmRows& a, GemmRows& b, const int32_t* offsets, i
     if (a.plan == plan_tc) a.plan = nullptr;
     if (b.plan == plan_tc) b.plan = nullptr;
   }
+  // both on the tensor-core engine with different row tiles (one CTA-pair GEMM, one not): the
+  // second gets its own plan in the SIMT plan's buffer (unused then)
+  if (a.plan == plan_tc && b.plan == plan_tc && tc_rows_tile(a) != tc_rows_tile(b)) {
+    DMOE_TRY(tile_plan(offsets, E, tc_rows_tile(a), plan_tc, s));
+    b.plan = plan_simt;
+    return tile_plan(offsets, E, tc_rows_tile(b), plan_simt, s);
+  }
   const bool need_tc = a.plan == plan_tc || b.plan == plan_tc;
   const bool need_simt = a.plan == plan_simt || b.plan == plan_simt;
   if (need_tc) DMOE_TRY(tile_plan(offsets, E, tc_rows_tile(a.plan == plan_tc ? a : b), plan_tc, s));
@@ -566,14 +573,22 @@ static dmoe_status ffn3_check(dmoe_dtype dt, int32_t D, int32_t H, int32_t E_loc
   return DMOE_OK;
 }
 
+// plans: [2][E+1] row-tile plans for 128-row tiles and for CTA-pair 256-row tiles (host-built only
+// when E exceeds the in-kernel plan's smem table)
 static GemmRows rows_for(const void* A, const void* B, void* C, const float* bias, const int32_t* offsets, int E,
-                         int N, int K, int64_t R_cap, bool b_mn, int epi, int32_t* plan) {
+                         int N, int K, int64_t R_cap, bool b_mn, int epi, int32_t* plans) {
   GemmRows g{};
   g.A = A; g.B = B; g.C = C; g.bias = bias; g.aux = nullptr; g.offsets = offsets;
   g.E = E; g.N = N; g.K = K; g.rows_cap = R_cap; g.b_mn = b_mn; g.epi = epi;
-  g.plan = E <= tc_plan_in_kernel_max() ? nullptr : plan;
-  g.max_tiles = ceil_div(R_cap, tc_rows_tile(g)) + E;
+  const int tile = tc_rows_tile(g);
+  g.plan = E <= tc_plan_in_kernel_max() ? nullptr : plans + (tile == TC_ROWS_TILE_DEFAULT ? 0 : E + 1);
+  g.max_tiles = ceil_div(R_cap, tile) + E;
   return g;
+}
+static dmoe_status ffn3_plans(const int32_t* offsets, int E, int32_t* plans, cudaStream_t s) {
+  if (E <= tc_plan_in_kernel_max()) return DMOE_OK;
+  DMOE_TRY(tile_plan(offsets, E, TC_ROWS_TILE_DEFAULT, plans, s));
+  return tile_plan(offsets, E, 2 * TC_ROWS_TILE_DEFAULT, plans + E + 1, s);
 }
 
 dmoe_status dmoe_expert_ffn3_fwd(const void* xd, const int32_t* offsets, int32_t E_local, int64_t R_cap,
@@ -587,9 +602,9 @@ dmoe_status dmoe_expert_ffn3_fwd(const void* xd, const int32_t* offsets, int32_t
   if (R_cap > 0) { NN(xd); NN(z1); NN(a1); NN(z2); NN(a2); NN(stats); NN(out); }
   cudaStream_t s = (cudaStream_t)stream;
   Carver cv(ws, ws_bytes);
-  int32_t* plan = cv.take<int32_t>(E_local + 1);
+  int32_t* plan = cv.take<int32_t>(2 * ((size_t)E_local + 1));
   DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "expert_ffn3_fwd: workspace too small");
-  if (E_local > tc_plan_in_kernel_max()) DMOE_TRY(tile_plan(offsets, E_local, TC_ROWS_TILE_DEFAULT, plan, s));
+  DMOE_TRY(ffn3_plans(offsets, E_local, plan, s));
   // z1 = W1 x + b1 -> a1 = relu(LN1(z1)) -> z2 = W2 a1 + b2 -> a2 = relu(LN2(z2)) -> out = W3 a2 + b3
   DMOE_TRY(tc_gemm_rows(rows_for(xd, W1, z1, b1, offsets, E_local, H, D, R_cap, false, EPI_BIAS, plan), s));
   DMOE_TRY(ln_relu_fwd(z1, offsets, E_local, R_cap, H, eps, g1, be1, a1, stats, s));
@@ -612,11 +627,11 @@ dmoe_status dmoe_expert_ffn3_bwd(const void* xd, const void* z1, const void* a1,
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t Rc = R_cap > 0 ? R_cap : 1;
   Carver cv(ws, ws_bytes);
-  int32_t* plan = cv.take<int32_t>(E_local + 1);
+  int32_t* plan = cv.take<int32_t>(2 * ((size_t)E_local + 1));
   void* da = cv.take<char>((size_t)Rc * H * 2);
   void* dz = cv.take<char>((size_t)Rc * H * 2);
   DMOE_REQUIRE(cv.ok(), DMOE_ERR_ARG, "expert_ffn3_bwd: workspace too small (%zu < %zu)", ws_bytes, cv.used);
-  if (E_local > tc_plan_in_kernel_max()) DMOE_TRY(tile_plan(offsets, E_local, TC_ROWS_TILE_DEFAULT, plan, s));
+  DMOE_TRY(ffn3_plans(offsets, E_local, plan, s));
   // out = W3 a2 + b3:  da2 = dout W3;  dW3 = dout^T a2, db3 = sum dout
   DMOE_TRY(tc_gemm_rows(rows_for(dout, W3, da, nullptr, offsets, E_local, H, D, R_cap, true, EPI_PLAIN, plan), s));
   GemmSegK g3{dout, a2, dW3, offsets, E_local, D, H, R_cap, db3};

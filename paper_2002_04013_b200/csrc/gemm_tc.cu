@@ -128,6 +128,59 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                : "memory");
 }
 
+// ---- CTA pair (cta_group::2): two SMs of a cluster run one M = 256 MMA, each CTA holding its
+// own 128 rows of A and half of B's N columns, each CTA's TMEM its own 128 accumulator rows
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// the same shared-memory offset in CTA 0 of the cluster (the pair's leader), as a cluster address
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+// TMA into this CTA's smem, completion counted on the leader's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t bar_c, int c0, int c1,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_c), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, uint32_t bar_c, int c0, int c1,
+                                                 int c2, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(bar_c), "r"(c0), "r"(c1), "r"(c2), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// MMA completion signalled on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   smem_u32(bar)), "h"((uint16_t)3)
+               : "memory");
+}
+
 #define TMEM_LD32(taddr, r)                                                                         \
   asm volatile(                                                                                     \
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14," \
@@ -154,14 +207,14 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // instruction descriptor: kind::f16, A/B bf16, D fp32, M=128, N=BN, majors
-__host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn) {
+__host__ __device__ constexpr uint32_t make_idesc(int bn, bool a_mn, bool b_mn, int m = TC_BM) {
   return (1u << 4)                       // D format f32
          | (1u << 7)                     // A format bf16
          | (1u << 10)                    // B format bf16
          | ((a_mn ? 1u : 0u) << 15)      // A major
          | ((b_mn ? 1u : 0u) << 16)      // B major
          | ((uint32_t)(bn >> 3) << 17)   // N >> 3
-         | ((uint32_t)(TC_BM >> 4) << 24);  // M >> 4
+         | ((uint32_t)(m >> 4) << 24);   // M >> 4 (256: the CTA pair's cta_group::2 MMA)
 }
 
 #define TMEM_LD16(taddr, r)                                                                     \
@@ -232,7 +285,7 @@ constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan 
 
 constexpr int TC_MAX_STAGES = 8;
 
-template <int BN, bool SEGK = false> struct TcCfg {
+template <int BN, bool SEGK = false, bool PAIR = false> struct TcCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
   // epilogue warps: 8 (two column halves) for tiles >= 128 wide.  4 warps on 256-wide tiles buy
   // a 4th ring stage but the epilogue then trails the mainloop (measured: mnist FFN fwd 78 -> 92 us)
@@ -243,7 +296,7 @@ template <int BN, bool SEGK = false> struct TcCfg {
   static constexpr int EPI_COLS = BN / (EPI_WARPS / 4);   // columns per epilogue warp
   static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int A_BYTES = TC_BM * TC_BK * 2;       // 16 KB
-  static constexpr int B_BYTES = BN * TC_BK * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * TC_BK * 2;   // a pair CTA holds half of B
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // multiple of 1 KB (BN % 8 == 0)
   // fixed smem without the per-expert tables (those are sized at launch: 2 x table_len ints)
   // weight-gradient tiles (~1 K block each): a 3rd accumulator (when TMEM has room) lets the
@@ -269,12 +322,14 @@ __device__ __forceinline__ float bf16hi(uint32_t w) { return __uint_as_float(w &
 // bf16 h > 0  <=>  sign bit clear and not +0
 __device__ __forceinline__ bool bf16_pos(uint32_t b) { return b != 0 && !(b & 0x8000u); }
 
-template <int BN, bool SEGK, bool B_MN, int EPI>
-__global__ void __launch_bounds__(TcCfg<BN, SEGK>::THREADS, 1)
+template <int BN, bool SEGK, bool B_MN, int EPI, bool PAIR = false>
+__global__ void __launch_bounds__(TcCfg<BN, SEGK, PAIR>::THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
           const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC2, const TcParams p) {
-  using Cfg = TcCfg<BN, SEGK>;
+  using Cfg = TcCfg<BN, SEGK, PAIR>;
+  static_assert(!PAIR || (!SEGK && BN == 256), "CTA pairs: 256-wide row GEMM tiles only");
+  constexpr int RT = PAIR ? 2 * TC_BM : TC_BM;   // rows per row tile (a pair: 128 per CTA)
   // Before waiting for the previous kernel (programmatic dependent launch: this CTA may already
   // sit on an SM the previous grid freed while its last CTAs finish): pull the expert weights of
   // this CTA's first tile into L2.  Weights are parameters no kernel of the step writes, and a
@@ -338,7 +393,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       int32_t carry = 0;
       for (int e0 = 0; e0 < p.E; e0 += blockDim.x) {
         const int e = e0 + threadIdx.x;
-        const int32_t v = e < p.E ? (off_s[e + 1] - off_s[e] + TC_BM - 1) / TC_BM : 0;
+        const int32_t v = e < p.E ? (off_s[e + 1] - off_s[e] + RT - 1) / RT : 0;
         int32_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -376,13 +431,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   int total;
   if (SEGK) total = total0 + (two ? p.E * MT2 * NT2 : 0);
   else if (p.offsets) total = plan[p.E] * NT;
-  else total = (int)((p.rows_single + TC_BM - 1) / TC_BM) * NT;
+  else total = (int)((p.rows_single + RT - 1) / RT) * NT;
 
   // tile walk: every role strides the grid.  (A contiguous chunk of SEGK tiles per CTA, which
   // would let consecutive tiles share the expert's operand rows, measured 45% slower on the
   // transformer dW2: the 148 CTAs then stream 148 experts' rows at once instead of sharing one
   // expert's rows through L2.)
-  const int t_begin = (int)blockIdx.x, t_end = total, t_step = (int)gridDim.x;
+  // a CTA pair (cluster of 2) walks one tile sequence; rank r takes rows [128 r, 128 r + 128) of it
+  const int prank = PAIR ? (int)cluster_rank() : 0;
+  const bool leader = prank == 0;
+  const int t_begin = PAIR ? (int)blockIdx.x >> 1 : (int)blockIdx.x, t_end = total;
+  const int t_step = PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x;
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -401,18 +460,28 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   if (warp == 1 && lane == 0) {
     // SEGK: a stage is released by the MMA commit and by the fix-up warp (column sums)
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], SEGK ? 2 : 1); mbar_init(&ready[i], 1); }
-    for (int i = 0; i < NACC; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], Cfg::EPI_WARPS); }
+    for (int i = 0; i < NACC; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], (PAIR ? 2 : 1) * Cfg::EPI_WARPS);  // a pair: both CTAs' epilogues drain
+    }
     for (int i = 0; i < 16; ++i) mbar_init(&wload[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const uint32_t tmem_cols = Cfg::TMEM_COLS;
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(tmem_cols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(tmem_cols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the peer's barriers exist before any remote arrival
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if ((DMOE_DBG(p) & 8) && blockIdx.x == 0 && threadIdx.x == 0) g_tc_probe[p.slot][8][3] = gtimer();
@@ -446,11 +515,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         int lo = 0, hi = p.E;
         while (hi - lo > 1) { int mid = (lo + hi) >> 1; if (plan[mid] <= rt) lo = mid; else hi = mid; }
         e = lo;
-        row0 = offs[e] + (int64_t)(rt - plan[e]) * TC_BM;
+        row0 = offs[e] + (int64_t)(rt - plan[e]) * RT + (int64_t)prank * TC_BM;
         row_end = offs[e + 1];
       } else {
         e = 0;
-        row0 = (int64_t)rt * TC_BM;
+        row0 = (int64_t)rt * RT + (int64_t)prank * TC_BM;
         row_end = p.rows_single;
       }
       nkb = p.K / TC_BK;
@@ -518,6 +587,22 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           prefetch_one();
           uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
+          if (PAIR) {
+            // both CTAs' loads complete on the leader's barrier, which expects the pair's bytes
+            if (leader) mbar_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+            const uint32_t fb = leader_addr(&full[stage]);
+            tma_load_2d_pair(sa, &tmA, fb, kb * TC_BK, (int)row0, pol_keep);
+            const int nh = n0 + prank * (BN / 2);  // this CTA's half of the N tile
+            if (B_MN) {
+#pragma unroll
+              for (int c = 0; c < BN / 128; ++c)
+                tma_load_3d_pair(sb + c * 8192, &tmB, fb, nh + 64 * c, kb * TC_BK, e, pol_stream);
+            } else {
+              tma_load_3d_pair(sb, &tmB, fb, kb * TC_BK, nh, e, pol_stream);
+            }
+            if (++stage == S) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           if (SEGK) {
             const int kr = (int)(row0 + kb * TC_BK);
@@ -548,9 +633,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         atomicAdd(&g_tc_wait[p.slot][11], 1ull);
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && (!PAIR || leader)) {
     // ======================= MMA issuer =======================
-    constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN);
+    // (a pair: the leader issues M = 256 MMAs over both CTAs' smem into both CTAs' TMEM)
+    constexpr uint32_t idesc = make_idesc(BN, A_MN, B_MN, PAIR ? 2 * TC_BM : TC_BM);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -593,11 +679,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if ((DMOE_DBG(p) & 4) || k >= nk16) break;
             const uint64_t ad = A_MN ? make_desc(a0 + k * 2048, 8192, 1024) : make_desc(a0 + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(b0 + k * 2048, 8192, 1024) : make_desc(b0 + k * 32, 16, 1024);
-            tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            if (PAIR) tc_mma_pair(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            else tc_mma(tmem_d, ad, bd, idesc, (kb | k) != 0);
           }
           WT_ADD(w_mmaonly, t_i);
-          tc_commit(&empty[stage]);
-          if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
+          if (PAIR) {
+            tc_commit_pair(&empty[stage]);
+            if (kb == nkb - 1) tc_commit_pair(&tfull[acc]);
+          } else {
+            tc_commit(&empty[stage]);
+            if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
+          }
         }
         __syncwarp();
         WT_ADD(w_issue, t_i);
@@ -844,7 +936,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             // before the staging and stores (the MMA of the tile after next needs it)
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+              if (PAIR) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+              else mbar_arrive(&tempty[acc]);
+            }
             released = true;
           }
         }
@@ -967,7 +1062,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (!released) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) {
+            if (PAIR) mbar_arrive_cluster(leader_addr(&tempty[acc]));
+            else mbar_arrive(&tempty[acc]);
+          }
         }
         if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
       }
@@ -985,9 +1083,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   tc_fence_before();
   __syncthreads();
   if ((DMOE_DBG(p) & 8) && blockIdx.x == 0 && threadIdx.x == 0) g_tc_probe[p.slot][8][5] = gtimer();
+  if (PAIR) cluster_sync_all();  // the peer is done with our barriers and our TMEM
   if (warp == 2) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tmem_cols));
   }
 }
 
@@ -1058,7 +1160,14 @@ int tc_plan_in_kernel_max() { return TC_TABLE_E; }
 bool tc_rows_mmajor() { return true; }
 
 // token rows per tile of the row GEMMs (the plan granularity)
-int tc_rows_tile(const GemmRows&) { return TC_BM; }
+// CTA pairs (cta_group::2, M = 256) for the grouped row GEMMs whose experts average >= 256 rows
+// of capacity (the tensor-bound side of the ridge): each CTA loads half of the weight tile, so
+// the L2 -> SM operand feed per MMA drops by a third
+static bool rows_pair(const GemmRows& g) {
+  static const bool off = dmoe_env("DMOE_TC_NOPAIR") != nullptr;  // A/B experiments
+  return !off && g.offsets && g.epi != EPI_F32_BIAS && g.N % 256 == 0 && g.rows_cap >= (int64_t)2 * TC_BM * g.E;
+}
+int tc_rows_tile(const GemmRows& g) { return rows_pair(g) ? 2 * TC_BM : TC_BM; }
 
 bool tc_rows_supported(const GemmRows& g) {
   if (g.K % TC_BK != 0 || g.K <= 0 || g.N % 16 != 0) return false;
@@ -1092,29 +1201,40 @@ static int debug_flags_segk() {
   return f;
 }
 
-template <int BN, bool SEGK, bool B_MN, int EPI>
-static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                               const CUtensorMap& a2, const CUtensorMap& b2, const CUtensorMap& c2,
-                               const TcParams& p, int64_t max_tiles, cudaStream_t s) {
-  auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI>;
+template <int BN, bool SEGK, bool B_MN, int EPI, bool PAIR>
+static dmoe_status launch_maps_p(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                                 const CUtensorMap& a2, const CUtensorMap& b2, const CUtensorMap& c2,
+                                 const TcParams& p, int64_t max_tiles, cudaStream_t s) {
+  using Cfg = TcCfg<BN, SEGK, PAIR>;
+  auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI, PAIR>;
   const int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
-  const int smem = TcCfg<BN, SEGK>::smem_for(table_len);
+  const int smem = Cfg::smem_for(table_len);
   static int attr = 0;
   if (smem > attr) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = smem;
   }
-  const int64_t ctas = (p.max_ctas > 0 && p.max_ctas < num_sms()) ? p.max_ctas : num_sms();
-  int64_t grid = max_tiles < ctas ? max_tiles : ctas;
-  if (grid < 1) grid = 1;
+  int64_t ctas = (p.max_ctas > 0 && p.max_ctas < num_sms()) ? p.max_ctas : num_sms();
+  int64_t grid = (PAIR ? 2 : 1) * max_tiles < ctas ? (PAIR ? 2 : 1) * max_tiles : ctas;
+  if (PAIR) grid &= ~(int64_t)1;  // whole pairs
+  if (grid < (PAIR ? 2 : 1)) grid = PAIR ? 2 : 1;
   TcParams pp = p;
   pp.dbg = debug_flags() | (SEGK ? debug_flags_segk() : 0);
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
-  pp.stages = TcCfg<BN, SEGK>::stages_for(table_len);
+  pp.stages = Cfg::stages_for(table_len);
   pp.table_len = table_len;
-  launch_pdl(kern, (unsigned)grid, TcCfg<BN, SEGK>::THREADS, smem, s, a, b, c, a2, b2, c2, pp);
+  if (PAIR)
+    launch_pdl_cluster(kern, (unsigned)grid, Cfg::THREADS, smem, s, 2u, a, b, c, a2, b2, c2, pp);
+  else
+    launch_pdl(kern, (unsigned)grid, Cfg::THREADS, smem, s, a, b, c, a2, b2, c2, pp);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
+}
+template <int BN, bool SEGK, bool B_MN, int EPI>
+static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                               const CUtensorMap& a2, const CUtensorMap& b2, const CUtensorMap& c2,
+                               const TcParams& p, int64_t max_tiles, cudaStream_t s) {
+  return launch_maps_p<BN, SEGK, B_MN, EPI, false>(a, b, c, a2, b2, c2, p, max_tiles, s);
 }
 template <int BN, bool SEGK, bool B_MN, int EPI>
 static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcParams& p,
@@ -1146,7 +1266,8 @@ static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
   if (g.max_tiles <= 0) return DMOE_OK;
   // expected row tiles ~ one per expert at <= 128 rows/expert, else rows/128
   const int64_t units = g.offsets ? (g.rows_cap / TC_BM > g.E ? g.rows_cap / TC_BM : g.E) : g.max_tiles;
-  const int BN = pick_bn_balanced(g.N, g.b_mn, units);
+  const bool pair = rows_pair(g);
+  const int BN = pair ? 256 : pick_bn_balanced(g.N, g.b_mn, units);
   // A: [rows_cap, K] K-major; rows past the extent are zero-filled by TMA, rows past a
   // segment produce accumulator rows the epilogue never stores.
   CUtensorMap ta, tb;
@@ -1157,7 +1278,7 @@ static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
     DMOE_TRY(make_map(&tb, g.B, 3, bdims, 64));
   } else {
     uint64_t bdims[3] = {(uint64_t)g.K, (uint64_t)g.N, (uint64_t)g.E};
-    DMOE_TRY(make_map(&tb, g.B, 3, bdims, (uint32_t)BN));
+    DMOE_TRY(make_map(&tb, g.B, 3, bdims, (uint32_t)(pair ? BN / 2 : BN)));   // a pair CTA: half the N rows
   }
   TcParams p{};
   p.offsets = g.offsets; p.plan = g.plan; p.bias = g.bias; p.aux = (const __nv_bfloat16*)g.aux;
@@ -1165,6 +1286,20 @@ static dmoe_status tc_gemm_rows_mk(const GemmRows& g, cudaStream_t s) {
   p.max_ctas = g.max_ctas;
   p.hmask = g.hmask; p.hmask_ld = g.hmask_ld;
   const int64_t tiles = g.max_tiles * ((g.N + BN - 1) / BN);
+  if (pair) {
+#define DMOE_TC_PAIR(BMN, E_) return launch_maps_p<256, false, BMN, E_, true>(ta, tb, ta, ta, tb, ta, p, tiles, s)
+#define DMOE_TC_PEPI(BMN)                                  \
+    switch (g.epi) {                                       \
+      case EPI_BIAS_RELU: DMOE_TC_PAIR(BMN, EPI_BIAS_RELU); \
+      case EPI_BIAS: DMOE_TC_PAIR(BMN, EPI_BIAS);           \
+      case EPI_RELU_MASK: DMOE_TC_PAIR(BMN, EPI_RELU_MASK); \
+      default: DMOE_TC_PAIR(BMN, EPI_PLAIN);                \
+    }
+    if (g.b_mn) { DMOE_TC_PEPI(true) }
+    DMOE_TC_PEPI(false)
+#undef DMOE_TC_PEPI
+#undef DMOE_TC_PAIR
+  }
   switch (BN) {
     case 256: return rows_bn<256>(g, ta, tb, p, tiles, s);
     case 128: return rows_bn<128>(g, ta, tb, p, tiles, s);

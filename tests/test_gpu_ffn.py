@@ -87,3 +87,15 @@ def test_bf16_wide_tiles():
 
 def test_bf16_single_expert_many_tiles():
     _run([1000], D=128, H=384, dtype="bf16", seed=4)
+
+
+def test_bf16_cta_pair_row_gemms():
+    """Experts averaging >= 256 rows of capacity run the row GEMMs on CTA pairs (cta_group::2,
+    M = 256; each CTA loads half of the weight tile): segments shorter than one CTA's 128 rows
+    (the peer's rows fall past the segment), exact 256-row pair tiles, odd tails, an empty expert."""
+    _run([300, 257, 0, 512, 1, 700, 256, 255], D=256, H=1024, dtype="bf16", seed=5)
+
+
+def test_bf16_cta_pair_many_experts():
+    rng = np.random.default_rng(6)
+    _run(list(rng.poisson(300, 24)), D=512, H=1024, dtype="bf16", seed=6)
