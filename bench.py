@@ -678,7 +678,12 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     if cfg.chunk:
+        # N > 1: independent replicas (each rank its own tokens and tied pool), max over ranks
         r = bench_chunked(args, cfg, rank, world, local_rank)
+        if world > 1:
+            t = torch.tensor([r["ms"], r["e2e_ms"]], device=torch.device("cuda", local_rank))
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            r["ms"], r["e2e_ms"] = float(t[0].item()), float(t[1].item())
     else:
         r = bench_ours(args, cfg, rank, world, local_rank) if world == 1 else bench_ep(args, cfg, rank, world, local_rank)
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
@@ -732,7 +737,8 @@ def main():
                       else {}),
                    **({"chunk_tokens": cfg.chunk, "update": "fused SGD per chunk (runtime Backward request, "
                        "PAPER.md:322)"} if cfg.chunk else {}),
-                   "parallelism": (f"ep{world} (experts sharded; " + ("NCCL all-to-all" if os.environ.get("DMOE_EP") == "nccl"
+                   "parallelism": (f"{world} replicas (chunked steps, no exchange)" if cfg.chunk else
+                                   f"ep{world} (experts sharded; " + ("NCCL all-to-all" if os.environ.get("DMOE_EP") == "nccl"
                                    else "NVLink peer-memory exchange") + ")") if world > 1 else "single",
                    "l2": "flushed before every timed step (256 MiB write, untimed)",
                    "graph": "eager (host split sizes per step)" if (world > 1 and os.environ.get("DMOE_EP") == "nccl")

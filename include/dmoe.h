@@ -112,6 +112,14 @@ dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_
                            int32_t* sel, float* sel_score, void* ws, size_t ws_bytes,
                            dmoe_stream_t stream);
 
+/* S3, exact form (NEXT-3): the best k ALIVE experts by the Eq. 2 score, under X4's order — the
+ * north star's "exact top-k ... restricted to a liveness mask".  Scores are the same level-order
+ * fp32 sums Alg. 1 forms, so with every expert alive this equals dmoe_beam_topk bit for bit;
+ * with dead experts Alg. 1 (beam B = k) may miss the true top-k, this does not (a per-token scan
+ * of every alive expert: E <= 2^20).  Arguments as dmoe_beam_topk (g.beam is ignored). */
+dmoe_status dmoe_topk_exact(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive_bits, int32_t* sel,
+                            float* sel_score, dmoe_stream_t stream);
+
 /* S1+S2+S3 in one call — gate scores (Eq. 2) then SelectExperts (Alg. 1 + FilterAlive):
  * exactly dmoe_gate_scores followed by dmoe_beam_topk (same definitions, same results bit for
  * bit).  G [T, d*M] fp32 is optional: NULL keeps it in `ws` (the search reads it back from L2).

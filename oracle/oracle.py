@@ -343,3 +343,25 @@ def layer_step_ffn3(X, Wg, bg, P, dY, alive, responded, d, M, k, B, sel_override
                 offsets=offsets, row_of_slot=ros, token_of_row=tor, z1=z1, a1=a1, z2=z2, a2=a2, y1=y1, y2=y2,
                 out=out, y=y,
                 g_rows=g, dscore=dscore, dx_rows=dx_rows, dX=dX, dWg=dWg, dbg=dbg, **grads)
+
+
+def topk_exact(G, d, M, k, alive):
+    """Exact top-k over the ALIVE experts by the Eq. 2 score (the north star's "exact top-k ...
+    restricted to a liveness mask"; NEXT-3): the plain definition, every expert scored with the
+    level-order sum of reading X1, ordered by (score desc, flat index asc) (reading X4), the first
+    k alive kept, -1 / -inf pad (X6).  Returns sel [T,k] int32 and sel_score [T,k]."""
+    G = np.asarray(G, np.float64)
+    T = G.shape[0]
+    E = M ** d
+    e = np.arange(E)
+    s = np.zeros((T, E))
+    for i in range(d):
+        s = s + G[:, i * M + (e // M ** (d - 1 - i)) % M]
+    live = np.nonzero(np.asarray(alive) == 1)[0]
+    sel = -np.ones((T, k), np.int32)
+    sc = np.full((T, k), -np.inf)
+    for t in range(T):
+        order = live[np.lexsort((live, -s[t, live]))][:k]
+        sel[t, :len(order)] = order
+        sc[t, :len(order)] = s[t, order]
+    return sel, sc

@@ -46,6 +46,7 @@ _SIGS = {
     "dmoe_launch_counters": ([_P, _I32], ctypes.c_int32),
     "dmoe_workspace_bytes": ([_I64, _I32, _I32, dmoe_grid, _I32, _I64], ctypes.c_size_t),
     "dmoe_gate_scores": ([_P, _I32, _I64, _I32, _P, _P, dmoe_grid, _P, _P, _SZ, _P], ctypes.c_int),
+    "dmoe_topk_exact": ([_P, _I64, dmoe_grid, _P, _P, _P, _P], ctypes.c_int),
     "dmoe_gate_topk": ([_P, _I32, _I64, _I32, _P, _P, dmoe_grid, _P, _P, _P, _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_beam_topk": ([_P, _I64, dmoe_grid, _P, _P, _P, _P, _SZ, _P], ctypes.c_int),
     "dmoe_dispatch": ([_P, _I32, _I64, _I32, dmoe_grid, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P,
@@ -137,6 +138,11 @@ def dmoe_gate_topk(x, Wg, bg, g, alive_bits, G, sel, sel_score, ws):
     _check("dmoe_gate_topk", _L.dmoe_gate_topk(_p(x), _dt(x), T, D, _p(Wg), _p(bg), g, _p(alive_bits), _p(G),
                                                _p(sel), _p(sel_score), _p(ws), ws.numel() * ws.element_size(),
                                                _stream()))
+
+
+def dmoe_topk_exact(G, g, alive_bits, sel, sel_score):
+    _check("dmoe_topk_exact", _L.dmoe_topk_exact(_p(G), G.shape[0], g, _p(alive_bits), _p(sel), _p(sel_score),
+                                                 _stream()))
 
 
 def dmoe_beam_topk(G, g, alive_bits, sel, sel_score, ws):

@@ -10,6 +10,8 @@
 #include <mutex>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -70,6 +72,8 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
                      size_t ws_bytes, cudaStream_t s);
 
 dmoe_status segment_offsets(const int32_t* offsets, int64_t E, int group, int32_t* seg, cudaStream_t s);
+dmoe_status topk_exact(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive, int32_t* sel, float* sel_score,
+                       cudaStream_t s);
 dmoe_status ln_relu_fwd(const void* z, const int32_t* offsets, int E, int64_t R_cap, int H, float eps,
                         const float* g, const float* be, void* a, float* stats, cudaStream_t s);
 dmoe_status ln_relu_bwd(const void* da, const void* z, const float* stats, const int32_t* offsets, int E, int H,
@@ -237,6 +241,15 @@ static dmoe_status plans_for(GemmRows& a, GemmRows& b, const int32_t* offsets, i
 
 using namespace dmoe;
 
+namespace {
+// one NVTX range per ABI call (SURVEY §5 tracing): free when no profiler is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
+#define DMOE_NVTX() NvtxRange dmoe_nvtx_range_(__func__)
+
 extern "C" {
 
 const char* dmoe_last_error(void) { return g_err; }
@@ -271,6 +284,7 @@ size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_
 dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg,
                              const float* bg, dmoe_grid g, float* G, void* ws, size_t ws_bytes,
                              dmoe_stream_t stream) {
+  DMOE_NVTX();
   int64_t E = 0;
   DMOE_TRY(check_grid(&g, &E));
   DMOE_TRY(check_dt(dt, D));
@@ -300,6 +314,7 @@ dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D,
 dmoe_status dmoe_gate_topk(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg, const float* bg,
                            dmoe_grid g, const uint32_t* alive_bits, float* G, int32_t* sel, float* sel_score,
                            void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_NVTX();
   int64_t E = 0;
   DMOE_TRY(check_grid(&g, &E));
   DMOE_TRY(check_dt(dt, D));
@@ -326,6 +341,7 @@ dmoe_status dmoe_gate_topk(const void* x, dmoe_dtype dt, int64_t T, int32_t D, c
 dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive_bits,
                            int32_t* sel, float* sel_score, void* ws, size_t ws_bytes,
                            dmoe_stream_t stream) {
+  DMOE_NVTX();
   int64_t E = 0;
   DMOE_TRY(check_grid(&g, &E));
   DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
@@ -335,12 +351,26 @@ dmoe_status dmoe_beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_
   return beam_topk(G, T, g, alive_bits, sel, sel_score, (uint32_t*)ws, (cudaStream_t)stream);
 }
 
+dmoe_status dmoe_topk_exact(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive_bits, int32_t* sel,
+                            float* sel_score, dmoe_stream_t stream) {
+  DMOE_NVTX();
+  int64_t E = 0;
+  DMOE_TRY(check_grid(&g, &E));
+  DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
+  DMOE_REQUIRE(E <= (1 << 20), DMOE_ERR_SHAPE, "topk_exact: E=%lld > 2^20 (a per-token scan of every expert)",
+               (long long)E);
+  NN(alive_bits);
+  if (T > 0) { NN(G); NN(sel); NN(sel_score); }
+  return topk_exact(G, T, g, alive_bits, sel, sel_score, (cudaStream_t)stream);
+}
+
 dmoe_status dmoe_dispatch(const void* x, dmoe_dtype dt, int64_t T, int32_t D, dmoe_grid g,
                           const int32_t* sel, const float* sel_score,
                           const uint32_t* responded_bits, float* w, uint8_t* valid,
                           int32_t* n_dropped, int32_t* counts, int32_t* offsets,
                           int32_t* row_of_slot, int32_t* token_of_row, void* xd, void* ws,
                           size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_NVTX();
   int64_t E = 0;
   DMOE_TRY(check_grid(&g, &E));
   DMOE_TRY(check_dt(dt, D));
@@ -357,6 +387,7 @@ dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t 
                                 const void* W1, const float* b1, const void* W2, const float* b2,
                                 void* h, uint32_t* hmask, void* out, void* ws, size_t ws_bytes,
                                 dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_dt(dt, D));
   DMOE_TRY(check_dt(dt, H));
   DMOE_REQUIRE(E_local >= 1 && R_cap >= 0, DMOE_ERR_SHAPE, "E_local=%d R_cap=%lld", E_local, (long long)R_cap);
@@ -387,6 +418,7 @@ dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t 
 dmoe_status dmoe_combine(const void* out, const int32_t* row_of_slot, const float* w,
                          const uint8_t* valid, int64_t T, int32_t D, int32_t k, dmoe_dtype dt,
                          void* y, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_dt(dt, D));
   DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
   if (T > 0) { NN(row_of_slot); NN(w); NN(valid); NN(y); }
@@ -396,6 +428,7 @@ dmoe_status dmoe_combine(const void* out, const int32_t* row_of_slot, const floa
 dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
                              const float* w, int64_t T, int32_t D, int32_t k, dmoe_dtype dt,
                              void* dout, float* dscore, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_dt(dt, D));
   DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
   if (T > 0) { NN(dy); NN(row_of_slot); NN(w); NN(dscore); }
@@ -406,6 +439,7 @@ dmoe_status dmoe_combine_bwd_failures(const void* dy, const void* out, const int
                                       const float* w, const int32_t* sel, const uint32_t* responded_bwd_bits,
                                       int64_t T, int32_t D, int32_t k, dmoe_dtype dt, void* dout, float* dscore,
                                       dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_dt(dt, D));
   DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
   NN(responded_bwd_bits);
@@ -419,6 +453,7 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
                                 int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
                                 const void* W2, void* dxd, void* dW1, float* db1, void* dW2,
                                 float* db2, void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_dt(dt, D));
   DMOE_TRY(check_dt(dt, H));
   DMOE_REQUIRE(E_local >= 1 && R_cap >= 0, DMOE_ERR_SHAPE, "E_local=%d R_cap=%lld", E_local, (long long)R_cap);
@@ -505,6 +540,7 @@ dmoe_status dmoe_expert_ffn_bwd_sgd(const void* xd, const void* h, const uint32_
                                     const int32_t* offsets, int32_t E_local, int64_t R_cap, int32_t D,
                                     int32_t H, dmoe_dtype dt, void* W1, float* b1, void* W2, float* b2,
                                     float lr, void* dxd, void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_dt(dt, D));
   DMOE_TRY(check_dt(dt, H));
   DMOE_REQUIRE(E_local >= 1 && R_cap >= 0, DMOE_ERR_SHAPE, "E_local=%d R_cap=%lld", E_local, (long long)R_cap);
@@ -597,6 +633,7 @@ dmoe_status dmoe_expert_ffn3_fwd(const void* xd, const int32_t* offsets, int32_t
                                  const float* g2, const float* be2, const void* W3, const float* b3, float eps,
                                  void* z1, void* a1, void* z2, void* a2, float* stats, void* out, void* ws,
                                  size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(ffn3_check(dt, D, H, E_local, R_cap));
   NN(offsets); NN(W1); NN(b1); NN(g1); NN(be1); NN(W2); NN(b2); NN(g2); NN(be2); NN(W3); NN(b3); NN(ws);
   if (R_cap > 0) { NN(xd); NN(z1); NN(a1); NN(z2); NN(a2); NN(stats); NN(out); }
@@ -620,6 +657,7 @@ dmoe_status dmoe_expert_ffn3_bwd(const void* xd, const void* z1, const void* a1,
                                  const float* be2, const void* W3, void* dxd, void* dW1, float* db1, float* dg1,
                                  float* dbe1, void* dW2, float* db2, float* dg2, float* dbe2, void* dW3,
                                  float* db3, void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(ffn3_check(dt, D, H, E_local, R_cap));
   NN(offsets); NN(W1); NN(g1); NN(be1); NN(W2); NN(g2); NN(be2); NN(W3); NN(dW1); NN(db1); NN(dg1); NN(dbe1);
   NN(dW2); NN(db2); NN(dg2); NN(dbe2); NN(dW3); NN(db3); NN(ws);
@@ -654,6 +692,7 @@ dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, con
                           const void* dxd, const int32_t* row_of_slot, int64_t T, int32_t D,
                           dmoe_grid g, dmoe_dtype dt, void* dx, float* dWg, float* dbg, void* ws,
                           size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_NVTX();
   int64_t E = 0;
   DMOE_TRY(check_grid(&g, &E));
   DMOE_TRY(check_dt(dt, D));
@@ -666,6 +705,7 @@ dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, con
 
 dmoe_status dmoe_segment_offsets(const int32_t* offsets, int32_t E, int32_t group, int32_t* seg,
                                  dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_REQUIRE(E >= 1 && group >= 1 && E % group == 0, DMOE_ERR_SHAPE, "segment_offsets: E=%d group=%d", E, group);
   NN(offsets); NN(seg);
   return segment_offsets(offsets, E, group, seg, (cudaStream_t)stream);
@@ -674,6 +714,7 @@ dmoe_status dmoe_segment_offsets(const int32_t* offsets, int32_t E, int32_t grou
 dmoe_status dmoe_exchange_layout(const int32_t* recv_counts, int32_t G, int32_t E_local, int64_t R_cap,
                                  int32_t* offsets, int32_t* src_of_dst, void* ws, size_t ws_bytes,
                                  dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_REQUIRE(G >= 1 && E_local >= 1 && R_cap >= 0, DMOE_ERR_SHAPE, "G=%d E_local=%d", G, E_local);
   NN(recv_counts); NN(offsets); NN(ws);
   if (R_cap > 0) NN(src_of_dst);
@@ -683,6 +724,7 @@ dmoe_status dmoe_exchange_layout(const int32_t* recv_counts, int32_t G, int32_t 
 
 dmoe_status dmoe_permute_rows(const void* src, dmoe_dtype dt, const int32_t* idx, const int32_t* n_rows,
                               int32_t D, int32_t inverse, void* dst, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_dt(dt, D));
   NN(src); NN(idx); NN(n_rows); NN(dst);
   DMOE_REQUIRE(inverse == 0 || inverse == 1, DMOE_ERR_ARG, "inverse must be 0 or 1");
@@ -702,11 +744,13 @@ static dmoe_status check_ep(const dmoe_ep* ep) {
 }
 
 dmoe_status dmoe_ep_begin(const dmoe_ep* ep, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_ep(ep));
   return ep_begin(ep->epoch, (cudaStream_t)stream);
 }
 
 dmoe_status dmoe_ep_exchange_counts(const dmoe_ep* ep, const int32_t* counts, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_ep(ep));
   NN(counts);
   cudaStream_t s = (cudaStream_t)stream;
@@ -720,6 +764,7 @@ dmoe_status dmoe_ep_exchange_counts(const dmoe_ep* ep, const int32_t* counts, dm
 dmoe_status dmoe_ep_push_rows(const dmoe_ep* ep, const void* src, dmoe_dtype dt, const int32_t* gather_idx,
                               const int32_t* offsets, int32_t D, void* const* peer_dst, int32_t phase,
                               dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_ep(ep));
   DMOE_TRY(check_dt(dt, D));
   NN(src); NN(offsets); NN(peer_dst);
@@ -732,6 +777,7 @@ dmoe_status dmoe_ep_push_rows(const dmoe_ep* ep, const void* src, dmoe_dtype dt,
 
 dmoe_status dmoe_ep_return_rows(const dmoe_ep* ep, const void* src, dmoe_dtype dt, int32_t D,
                                 void* const* peer_dst, int32_t phase, dmoe_stream_t stream) {
+  DMOE_NVTX();
   DMOE_TRY(check_ep(ep));
   DMOE_TRY(check_dt(dt, D));
   NN(src); NN(peer_dst);
@@ -744,6 +790,7 @@ dmoe_status dmoe_ep_return_rows(const dmoe_ep* ep, const void* src, dmoe_dtype d
 }
 
 dmoe_status dmoe_ipc_alloc(size_t bytes, void** ptr, void* handle) {
+  DMOE_NVTX();
   NN(ptr); NN(handle);
   cudaError_t e = cudaMalloc(ptr, bytes);
   if (e == cudaSuccess) e = cudaMemset(*ptr, 0, bytes);
@@ -753,6 +800,7 @@ dmoe_status dmoe_ipc_alloc(size_t bytes, void** ptr, void* handle) {
 }
 
 dmoe_status dmoe_ipc_open(const void* handle, void** ptr) {
+  DMOE_NVTX();
   NN(handle); NN(ptr);
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, sizeof(h));
@@ -762,12 +810,14 @@ dmoe_status dmoe_ipc_open(const void* handle, void** ptr) {
 }
 
 dmoe_status dmoe_ipc_close(void* ptr) {
+  DMOE_NVTX();
   cudaError_t e = cudaIpcCloseMemHandle(ptr);
   DMOE_REQUIRE(e == cudaSuccess, DMOE_ERR_CUDA, "ipc_close: %s", cudaGetErrorString(e));
   return DMOE_OK;
 }
 
 dmoe_status dmoe_ipc_free(void* ptr) {
+  DMOE_NVTX();
   cudaError_t e = cudaFree(ptr);
   DMOE_REQUIRE(e == cudaSuccess, DMOE_ERR_CUDA, "ipc_free: %s", cudaGetErrorString(e));
   return DMOE_OK;

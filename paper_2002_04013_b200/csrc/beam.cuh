@@ -222,6 +222,15 @@ struct TopSet {
   }
 };
 
+template <int N>
+__device__ __forceinline__ uint64_t beam_at_key(const TopSet<N>& ts, int q) {
+  uint64_t v = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (i == q) v = ts.key(i);
+  return v;
+}
+
 template <int WMAX>
 __device__ __forceinline__ void beam_dim_list(const float* gi, int gstride, int M, int n, uint64_t* out) {
   TopSet<WMAX + 1> L;

@@ -44,148 +44,169 @@ dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt
   return check_launch("transpose");
 }
 
-constexpr int kGbWarps = 16;                 // warps per CTA (one CTA per SM: W_g^T slice in smem)
-constexpr int kGbSmem = 128 * 1024;          // W_g^T column slice budget
 
-// dX (undispatch + gate path), the per-CTA partial bias gradient and the tokens' dG rows.
-// The gate path needs, per token, d*k rows of W_g^T; a CTA keeps the W_g^T columns of its D
-// slice [p0, p0 + Dp) resident in shared memory (grid = D slices x token blocks, one CTA per
-// SM), so the only HBM traffic is the gather of the k dispatched dxd rows (issued together:
-// k * Dp / (32 V) 16-byte vectors per lane in flight) and the dX write; 16 warps per CTA, a warp
-// per token.  CTAs of slice 0 also write the dG row (dense fp32 dG for the SIMT dW_g, bf16
-// hi | lo halves padded to ld2 columns for the tensor-core dW_g) and the bias partials
-// db_g = sum_t dG[t] of their tokens (lane owns columns lane + 32 m, warps combined in a fixed
-// order: deterministic).  Block (0, 0) writes the token chunk bounds of the split-K dW_g GEMM.
-template <typename T, int KMAX, int VPL>
-__global__ void __launch_bounds__(kGbWarps * 32, 1)
+// dX (undispatch + gate path), the per-CTA partial bias gradient and the tokens' dG rows, one
+// warp per token: every dxd row segment of the token's k dispatched rows is loaded before the
+// first add (UNR 16-byte vectors per lane per row), the d*k gate rows come from W_g^T
+// (transposed once, 2*d*M*D bytes: L2-resident), and the next token's routing record is fetched
+// while this token's rows are in flight.  The token's dG row is written as exact bf16 hi | lo
+// halves padded to ld2 columns (tensor-core dW_g) or as dense fp32 (SIMT dW_g), and the CTA's
+// bias partial db_g = sum_t dG[t] (lane owns columns lane + 32 m; warps combined in a fixed order:
+// deterministic).  Block 0 writes the token chunk bounds of the split-K dW_g GEMM.
+constexpr int kGbWarps = 4;
+
+template <int KMAX>
+struct GbRec {  // a token's routing record: dispatched rows, dscore, gate columns (one byte per level)
+  int32_t rows[KMAX];
+  uint32_t cols[KMAX];  // byte i = i*M + u_i(e) (< d*M <= 256); 0xffffffff: no expert
+  float ds[KMAX];
+  __device__ __forceinline__ void load(const int32_t* __restrict__ row_of_slot, const int32_t* __restrict__ sel,
+                                       const float* __restrict__ dscore, int64_t t, int64_t Tn, int d, int M,
+                                       int mshift, int k) {
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      const bool on = s < k && t < Tn;
+      rows[s] = on ? row_of_slot[t * k + s] : -1;
+      const int32_t e = on ? sel[t * k + s] : -1;
+      ds[s] = (on && e >= 0) ? dscore[t * k + s] : 0.0f;
+      uint32_t pk = 0xffffffffu;
+      if (e >= 0) {  // u_i(e) (reading X1): the last level is the lowest base-M digit
+        pk = 0u;
+        uint32_t ee = (uint32_t)e;
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {
+          if (i >= d) continue;
+          uint32_t q, r;
+          if (mshift >= 0) { q = ee >> mshift; r = ee & ((1u << mshift) - 1u); }
+          else { q = ee / (uint32_t)M; r = ee - q * (uint32_t)M; }
+          pk |= ((uint32_t)i * (uint32_t)M + r) << (8 * i);
+          ee = q;
+        }
+      }
+      cols[s] = pk;
+    }
+  }
+};
+
+template <typename T, int KMAX>
+__global__ void __launch_bounds__(kGbWarps * 32)
 k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
               const float* __restrict__ dscore, const T* __restrict__ dxd,
-              const int32_t* __restrict__ row_of_slot, int64_t Tn, int32_t D, int Dp, int d, int M, int k,
+              const int32_t* __restrict__ row_of_slot, int64_t Tn, int32_t D, int d, int M, int k,
               T* __restrict__ dx, float* __restrict__ pb, float* __restrict__ dG,
               __nv_bfloat16* __restrict__ dG2, int ld2, int32_t* __restrict__ chunk_off, int nchunk,
               int64_t tpc) {
   DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
-  constexpr int NB = 8;  // gate columns per lane (d*M <= 256)
-  extern __shared__ __align__(16) uint8_t gb_smem[];
-  T* wsl = reinterpret_cast<T*>(gb_smem);  // [dM][Dp]: W_g^T[:, p0 .. p0 + Dp)
+  constexpr int UNR = KMAX <= 4 ? 4 : (KMAX <= 8 ? 2 : 1);  // 16-byte vectors per lane per row in flight
+  constexpr int NB = 8;                                      // gate columns per lane (d*M <= 256)
   __shared__ float bsh[kGbWarps][NB * 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int dM = d * M;
-  const int part = blockIdx.x;
-  const int p0 = part * Dp;
-  const bool lead = part == 0;
-  if (chunk_off && blockIdx.x == 0 && blockIdx.y == 0)
-    for (int c = threadIdx.x; c <= nchunk; c += blockDim.x)
-      chunk_off[c] = (int32_t)((int64_t)c * tpc < Tn ? (int64_t)c * tpc : Tn);
-  {
-    const int vr = Dp / V;  // 16-byte vectors per slice row
-    for (int i = threadIdx.x; i < dM * vr; i += blockDim.x) {
-      const int r = i / vr, v = i - r * vr;
-      st_v4(wsl + (int64_t)r * Dp + v * V, ld_v4(WgT + (int64_t)r * D + p0 + v * V));
-    }
-  }
-  __syncthreads();
+  const int mshift = (M & (M - 1)) == 0 ? __ffs(M) - 1 : -1;
+  if (chunk_off && blockIdx.x == 0)
+    for (int i = threadIdx.x; i <= nchunk; i += blockDim.x)
+      chunk_off[i] = (int32_t)((int64_t)i * tpc < Tn ? (int64_t)i * tpc : Tn);
   float bpart[NB];
 #pragma unroll
   for (int m = 0; m < NB; ++m) bpart[m] = 0.0f;
-  const int64_t wstride = (int64_t)gridDim.y * kGbWarps;
-  for (int64_t t = (int64_t)blockIdx.y * kGbWarps + wib; t < Tn; t += wstride) {
-    int32_t rows[KMAX], cols[KMAX][4];
-    float ds[KMAX];
-#pragma unroll
-    for (int s = 0; s < KMAX; ++s) {
-      rows[s] = s < k ? row_of_slot[t * k + s] : -1;
-      const int32_t e = s < k ? sel[t * k + s] : -1;
-      ds[s] = (s < k && e >= 0) ? dscore[t * k + s] : 0.0f;
-      int ee = e < 0 ? 0 : e;
-#pragma unroll
-      for (int i = 3; i >= 0; --i) {   // u_i(e) (reading X1): column i*M + u_i
-        if (i < d) { cols[s][i] = i * M + (ee % M); ee /= M; } else cols[s][i] = -1;
-      }
-      if (e < 0) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) cols[s][i] = -1;
-      }
-    }
-    // the k dispatched rows of this slice: every load in flight before the first add
-    uint4 u[KMAX][VPL];
-#pragma unroll
-    for (int s = 0; s < KMAX; ++s)
-#pragma unroll
-      for (int q = 0; q < VPL; ++q) {
-        const int c = (lane + 32 * q) * V;
-        if (rows[s] >= 0 && c < Dp) u[s][q] = ld_nc_v4(dxd + (int64_t)rows[s] * D + p0 + c);
-      }
-    if (lead) {  // the token's dG row for the lane's columns (fixed slot, level order)
-      float g[NB];
-#pragma unroll
-      for (int m = 0; m < NB; ++m) g[m] = 0.0f;
+  const int64_t stride = (int64_t)gridDim.x * kGbWarps;
+  int64_t t = (int64_t)blockIdx.x * kGbWarps + wib;
+  GbRec<KMAX> cur, nxt;
+  cur.load(row_of_slot, sel, dscore, t, Tn, d, M, mshift, k);
+  for (; t < Tn; t += stride) {
+    nxt.load(row_of_slot, sel, dscore, t + stride, Tn, d, M, mshift, k);  // in flight with this token's rows
+    for (int c0 = lane * V; c0 < D; c0 += UNR * 32 * V) {
+      uint4 u[KMAX][UNR];
 #pragma unroll
       for (int s = 0; s < KMAX; ++s)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int col = cols[s][i];
-          if (col >= 0 && (col & 31) == lane) {
+        for (int q = 0; q < UNR; ++q) {
+          const int c = c0 + q * 32 * V;
+          u[s][q] = make_uint4(0u, 0u, 0u, 0u);  // a missing row reads as zeros
+          if (cur.rows[s] >= 0 && c < D) u[s][q] = ld_nc_v4(dxd + (int64_t)cur.rows[s] * D + c);
+        }
+      float acc[UNR][V];
 #pragma unroll
-            for (int m = 0; m < NB; ++m)
-              if (m == (col >> 5)) g[m] += ds[s];
+      for (int q = 0; q < UNR; ++q)
+#pragma unroll
+        for (int j = 0; j < V; ++j) acc[q][j] = 0.0f;
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (s >= k) break;
+#pragma unroll
+        for (int q = 0; q < UNR; ++q) {
+          float f[V];
+          unpack16(u[s][q], f, (const T*)nullptr);
+#pragma unroll
+          for (int j = 0; j < V; ++j) acc[q][j] += f[j];
+        }
+      }
+#pragma unroll
+      for (int s = 0; s < KMAX; ++s) {
+        if (cur.ds[s] == 0.0f) continue;
+#pragma unroll
+        for (int i = 3; i >= 0; --i) {  // last level first
+          if (i >= d) continue;
+          const int64_t col = (cur.cols[s] >> (8 * i)) & 0xffu;
+#pragma unroll
+          for (int q = 0; q < UNR; ++q) {
+            const int c = c0 + q * 32 * V;
+            if (c >= D) continue;
+            float f[V];
+            unpack16(ld_v4(WgT + col * D + c), f, (const T*)nullptr);
+#pragma unroll
+            for (int j = 0; j < V; ++j) acc[q][j] = fmaf(cur.ds[s], f[j], acc[q][j]);
           }
         }
-#pragma unroll
-      for (int m = 0; m < NB; ++m) {
-        bpart[m] += g[m];
-        const int col = lane + 32 * m;
-        if (dG && col < dM) dG[t * dM + col] = g[m];
-        if (dG2 && col < dM) {
-          const __nv_bfloat16 hi = __float2bfloat16_rn(g[m]);
-          dG2[t * ld2 + col] = hi;
-          dG2[t * ld2 + dM + col] = __float2bfloat16_rn(g[m] - __bfloat162float(hi));
-        }
       }
-      if (dG2)
-        for (int col = 2 * dM + lane; col < ld2; col += 32) dG2[t * ld2 + col] = __float2bfloat16_rn(0.0f);
+#pragma unroll
+      for (int q = 0; q < UNR; ++q) {
+        const int c = c0 + q * 32 * V;
+        if (c < D) st_v4(dx + t * D + c, pack16(acc[q], (const T*)nullptr));
+      }
+    }
+    // the token's dG row for the lane's columns lane + 32 m (fixed slot, level order; adding the
+    // zeros of the other lanes' entries changes nothing)
+    float g[NB];
+#pragma unroll
+    for (int m = 0; m < NB; ++m) g[m] = 0.0f;
+#pragma unroll
+    for (int s = 0; s < KMAX; ++s) {
+      if (cur.cols[s] == 0xffffffffu) continue;
+#pragma unroll
+      for (int i = 3; i >= 0; --i) {
+        if (i >= d) continue;
+        const int col = (int)((cur.cols[s] >> (8 * i)) & 0xffu);
+        const float add = (col & 31) == lane ? cur.ds[s] : 0.0f;
+#pragma unroll
+        for (int m = 0; m < NB; ++m) g[m] += m == (col >> 5) ? add : 0.0f;
+      }
     }
 #pragma unroll
-    for (int q = 0; q < VPL; ++q) {
-      const int c = (lane + 32 * q) * V;
-      if (c >= Dp) continue;
-      float acc[V];
-#pragma unroll
-      for (int j = 0; j < V; ++j) acc[j] = 0.0f;
-#pragma unroll
-      for (int s = 0; s < KMAX; ++s) {
-        if (rows[s] < 0) continue;
-        float f[V];
-        unpack16(u[s][q], f, (const T*)nullptr);
-#pragma unroll
-        for (int j = 0; j < V; ++j) acc[j] += f[j];
+    for (int m = 0; m < NB; ++m) {
+      const int col = lane + 32 * m;
+      if (col >= dM) break;
+      bpart[m] += g[m];
+      if (dG) dG[t * dM + col] = g[m];
+      if (dG2) {
+        const __nv_bfloat16 hi = __float2bfloat16_rn(g[m]);
+        dG2[t * ld2 + col] = hi;
+        dG2[t * ld2 + dM + col] = __float2bfloat16_rn(g[m] - __bfloat162float(hi));
       }
-#pragma unroll
-      for (int s = 0; s < KMAX; ++s) {
-        if (ds[s] == 0.0f) continue;
-#pragma unroll
-        for (int i = 3; i >= 0; --i) {   // last level first
-          if (cols[s][i] < 0) continue;
-          float f[V];
-          unpack16(ld_v4(wsl + (int64_t)cols[s][i] * Dp + c), f, (const T*)nullptr);
-#pragma unroll
-          for (int j = 0; j < V; ++j) acc[j] = fmaf(ds[s], f[j], acc[j]);
-        }
-      }
-      st_v4(dx + t * D + p0 + c, pack16(acc, (const T*)nullptr));
     }
+    if (dG2)
+      for (int col = 2 * dM + lane; col < ld2; col += 32) dG2[t * ld2 + col] = __float2bfloat16_rn(0.0f);
+    cur = nxt;
   }
-  if (lead) {
 #pragma unroll
-    for (int m = 0; m < NB; ++m) bsh[wib][lane + 32 * m] = bpart[m];
-    __syncthreads();
-    for (int col = threadIdx.x; col < dM; col += blockDim.x) {
-      float v = 0.0f;
+  for (int m = 0; m < NB; ++m) bsh[wib][lane + 32 * m] = bpart[m];
+  __syncthreads();
+  for (int col = threadIdx.x; col < dM; col += blockDim.x) {
+    float v = 0.0f;
 #pragma unroll
-      for (int w = 0; w < kGbWarps; ++w) v += bsh[w][col];
-      pb[(int64_t)blockIdx.y * dM + col] = v;
-    }
+    for (int w = 0; w < kGbWarps; ++w) v += bsh[w][col];
+    pb[(int64_t)blockIdx.x * dM + col] = v;
   }
 }
 
@@ -391,29 +412,9 @@ k_gate_reduce(const float* __restrict__ partial, int64_t nsplit, int ld, int hil
   if (lane == 0) dbg[col] = v;
 }
 
-// D slices of the dx kernel: the W_g^T slice [dM][Dp] must fit kGbSmem, Dp a multiple of 32
-// 16-byte vectors (one per lane per pass), at most 4 passes per lane
-struct GbdxShape { int parts, Dp, vpl; };
-// (k * vpl <= 8: 8 in-flight 16-byte vectors per lane, 64 KB per SM, within 128 registers)
-static GbdxShape gbdx_shape(int32_t D, int dM, size_t esz, int k) {
-  const int V = (int)(16 / esz);
-  const int kmax = k <= 4 ? 4 : (k <= 8 ? 8 : 16);
-  const int vmax = kmax >= 8 ? 1 : 8 / kmax;
-  for (int parts = 1; parts <= 64; ++parts) {
-    if (D % parts) continue;
-    const int Dp = D / parts;
-    if (Dp % (32 * V) && parts > 1) continue;
-    if ((size_t)dM * Dp * esz > (size_t)kGbSmem) continue;
-    const int vpl = (int)ceil_div(Dp, 32 * V);
-    if (vpl > vmax) continue;
-    return {parts, Dp, vpl};
-  }
-  return {0, 0, 0};
-}
-static int64_t gbdx_blocks(int64_t T, int parts) {
-  int64_t b = ceil_div((int64_t)num_sms(), parts);
-  const int64_t need = ceil_div(T > 0 ? T : 1, kGbWarps);
-  return b < need ? b : need;
+static int64_t gbdx_grid(int64_t T) {
+  const int64_t b = ceil_div(T > 0 ? T : 1, kGbWarps), cap = (int64_t)num_sms() * 16;
+  return b < cap ? b : cap;
 }
 // SIMT split-K over tokens (fp32 path): one 32-token pass per split where the partial sums
 // (capped at 8M floats) allow
@@ -444,7 +445,7 @@ size_t gate_bwd_ws_bytes(int64_t T, int32_t D, int dM) {
   const size_t simt = align_up(Tp * dM * 4, 256) + align_up((size_t)dwg_splits(T, D, dM) * D * dM * 4, 256);
   const size_t tc = align_up(Tp * tc_ld2(dM) * 2, 256) + align_up((size_t)tc_chunks(T, D) * D * tc_ld2(dM) * 4, 256) +
                     align_up((size_t)(tc_chunks(T, D) + 1) * 4, 256);
-  return align_up((size_t)D * dM * 4, 256) + (simt > tc ? simt : tc) + align_up((size_t)num_sms() * dM * 4, 256) +
+  return align_up((size_t)D * dM * 4, 256) + (simt > tc ? simt : tc) + align_up((size_t)gbdx_grid(T) * dM * 4, 256) +
          1024;
 }
 
@@ -456,9 +457,7 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
   DMOE_REQUIRE(dM <= 256, DMOE_ERR_SHAPE, "gate_bwd: d*M=%d > 256", dM);
   const bool tc = gate_bwd_tc(dt, D, dM) && T > 0;
   const size_t esz = dt == DMOE_BF16 ? 2 : 4;
-  const GbdxShape gs = gbdx_shape(D, dM, esz, k);
-  DMOE_REQUIRE(gs.parts > 0, DMOE_ERR_UNSUPPORTED, "gate_bwd: no D slicing for D=%d d*M=%d", D, dM);
-  const int64_t nb = gbdx_blocks(T, gs.parts);
+  const int64_t nb = gbdx_grid(T);
   Carver cv(ws, ws_bytes);
   void* WgT = cv.take<char>((size_t)D * dM * esz);
   float* pb = cv.take<float>((size_t)nb * dM);
@@ -487,27 +486,14 @@ dmoe_status gate_bwd(const void* x, const void* Wg, const int32_t* sel, const fl
   DMOE_TRY(check_launch("gate_bwd.transpose"));
   if (T > 0) {
     const int64_t tpc = tc ? ceil_div(T, nsplit) : 0;
-#define DMOE_GBDX3(TT, KM, VP)                                                                       \
-    {                                                                                                  \
-      static bool attr = false;                                                                        \
-      const size_t sm = (size_t)dM * gs.Dp * esz;                                                      \
-      if (!attr) { cudaFuncSetAttribute(k_gate_bwd_dx<TT, KM, VP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                        kGbSmem); attr = true; }                                       \
-      launch_pdl(k_gate_bwd_dx<TT, KM, VP>, dim3((unsigned)gs.parts, (unsigned)nb), kGbWarps * 32, sm, s,   \
-                 (const TT*)WgT, sel, dscore, (const TT*)dxd, row_of_slot, T, D, gs.Dp, d, M, k, (TT*)dx, pb, \
-                 dG, dG2, ld2, choff, (int)nsplit, tpc);                                               \
-    }
 #define DMOE_GBDX2(TT, KM)                                                                             \
-    switch (gs.vpl) {                                                                                  \
-      case 1: DMOE_GBDX3(TT, KM, 1) break;                                                             \
-      default: DMOE_GBDX3(TT, KM, 2) break;                                                            \
-    }
+    launch_pdl(k_gate_bwd_dx<TT, KM>, (unsigned)nb, kGbWarps * 32, 0, s, (const TT*)WgT, sel, dscore,   \
+               (const TT*)dxd, row_of_slot, T, D, d, M, k, (TT*)dx, pb, dG, dG2, ld2, choff, (int)nsplit, tpc);
 #define DMOE_GBDX(KM)                                                                                  \
     if (dt == DMOE_BF16) { DMOE_GBDX2(__nv_bfloat16, KM) } else { DMOE_GBDX2(float, KM) }
     if (k <= 4) { DMOE_GBDX(4) } else if (k <= 8) { DMOE_GBDX(8) } else { DMOE_GBDX(16) }
 #undef DMOE_GBDX
 #undef DMOE_GBDX2
-#undef DMOE_GBDX3
     DMOE_TRY(check_launch("gate_bwd.dx"));
     if (tc) {
       // dW_g partials on the tensor cores: chunk c's [D][hi | lo] = X[chunk]^T [dG_hi | dG_lo]

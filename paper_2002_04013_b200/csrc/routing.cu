@@ -178,4 +178,81 @@ dmoe_status beam_topk(const float* G, int64_t T, dmoe_grid g, const uint32_t* al
   return launch_beam<32>(G, T, g, PA_global, alive_bits, (int)words, sel, sel_score, s);
 }
 
+// Exact top-k over the alive experts (NEXT-3; the north star's "exact top-k ... restricted to a
+// liveness mask"): every alive expert e of the token is scored with the same level-order fp32
+// additions Alg. 1 uses, s = ((0 + g_0(u_0)) + g_1(u_1)) + ..., and the best k kept under X4's
+// order.  With every expert alive this equals Alg. 1 (SURVEY §8(c) X3 proof); with dead experts
+// Alg. 1 with B = k may miss the true top-k, this does not.  Thread per token over all E experts,
+// 128 tokens per CTA with their G rows staged in shared memory.
+template <int KMAX>
+__global__ void __launch_bounds__(kBeamTok)
+k_topk_exact(const float* __restrict__ G, int64_t T, int d, int M, int k, const uint32_t* __restrict__ alive,
+             int32_t* __restrict__ sel, float* __restrict__ sel_score) {
+  DMOE_PDL_ENTRY();
+  extern __shared__ float smem_f[];
+  const int dM = d * M, pitch = dM + 1;
+  float* gtile = smem_f;
+  int64_t E = 1;
+  for (int i = 0; i < d; ++i) E *= M;
+  for (int64_t t0 = (int64_t)blockIdx.x * kBeamTok; t0 < T; t0 += (int64_t)gridDim.x * kBeamTok) {
+    const int nt = (int)((T - t0) < kBeamTok ? (T - t0) : kBeamTok);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nt * dM; i += kBeamTok) {
+      const int r = i / dM;
+      gtile[r * pitch + (i - r * dM)] = __ldg(G + t0 * dM + i);
+    }
+    __syncthreads();
+    if ((int)threadIdx.x >= nt) continue;
+    const float* g = gtile + threadIdx.x * pitch;
+    TopSet<KMAX> top;
+    top.init(k);
+    for (int64_t w = 0; w < (E + 31) / 32; ++w) {
+      uint32_t bits = alive[w];
+      while (bits) {
+        const int b = __ffs(bits) - 1;
+        bits &= bits - 1;
+        const int64_t e = w * 32 + b;
+        if (e >= E) break;
+        float s = 0.0f;
+        int64_t rem = e, div = E / M;
+        for (int i = 0; i < d; ++i) {  // u_i = (e / M^(d-1-i)) mod M, levels in order (X1)
+          const int u = (int)(rem / div);
+          rem -= (int64_t)u * div;
+          div /= M;
+          s = s + g[i * M + u];
+        }
+        top.offer(s == 0.0f ? 0.0f : s, (uint32_t)e);
+      }
+    }
+    top.sort();
+    const int64_t t = t0 + threadIdx.x;
+    for (int q = 0; q < k; ++q) {
+      const uint64_t kq = beam_at_key(top, q);
+      sel[t * k + q] = kq ? (int32_t)(0xffffffffu - (uint32_t)kq) : -1;
+      sel_score[t * k + q] = kq ? beam_unord((uint32_t)(kq >> 32)) : -INFINITY;
+    }
+  }
+}
+
+dmoe_status topk_exact(const float* G, int64_t T, dmoe_grid g, const uint32_t* alive, int32_t* sel, float* sel_score,
+                       cudaStream_t s) {
+  if (T == 0) return DMOE_OK;
+  const size_t smem = (size_t)kBeamTok * (g.d * g.M + 1) * sizeof(float);
+  int64_t blocks = ceil_div(T, kBeamTok);
+  if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+#define DMOE_TKX(KM)                                                                                   \
+  {                                                                                                    \
+    static bool attr = false;                                                                          \
+    if (!attr && smem > 48 * 1024) {                                                                   \
+      cudaFuncSetAttribute(k_topk_exact<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+      attr = true;                                                                                     \
+    }                                                                                                  \
+    launch_pdl(k_topk_exact<KM>, (unsigned)blocks, kBeamTok, smem, s, G, T, g.d, g.M, g.k, alive, sel, sel_score); \
+  }
+  if (g.k <= 4) DMOE_TKX(4) else if (g.k <= 8) DMOE_TKX(8) else DMOE_TKX(16)
+#undef DMOE_TKX
+  return check_launch("topk_exact");
+}
+
 }  // namespace dmoe
+

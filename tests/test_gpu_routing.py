@@ -94,3 +94,31 @@ def test_gate_topk_equals_gate_then_beam(d, M, k, B, D, dead, T):
         assert torch.equal(s1, s2) and torch.equal(c1.view(torch.int32), c2.view(torch.int32))
         if keep:
             assert torch.equal(G1.view(torch.int32), G2.view(torch.int32))
+
+
+@pytest.mark.parametrize("d,M,k,dead,T", [(2, 64, 4, 0.3, 2000), (3, 16, 4, 0.1, 1500), (2, 16, 8, 0.5, 999),
+                                          (2, 64, 4, 0.0, 700)])
+def test_topk_exact_vs_oracle(d, M, k, dead, T):
+    """dmoe_topk_exact against the plain definition (oracle.topk_exact) on exact-grid scores
+    (every fp32 sum exact, ties everywhere): bit-exact on every token; with every expert alive it
+    also equals Alg. 1 (dmoe_beam_topk) bit for bit."""
+    rng = np.random.default_rng(T + d)
+    E = M ** d
+    G = (rng.integers(-8, 9, (T, d * M)) / 8).astype(np.float32)
+    alive = (rng.random(E) >= dead).astype(np.uint8)
+    g = L.grid(d, M, k, k)
+    Gt = torch.from_numpy(G).cuda()
+    sel = torch.empty(T, k, dtype=torch.int32, device="cuda")
+    sc = torch.empty(T, k, dtype=torch.float32, device="cuda")
+    L.dmoe_topk_exact(Gt, g, _alive_bits(alive), sel, sc)
+    torch.cuda.synchronize()
+    osel, osc = O.topk_exact(G.astype(np.float64), d, M, k, alive)
+    assert np.array_equal(np64(sel), osel)
+    assert np.array_equal(np64(sc), osc.astype(np.float32).astype(np.float64))
+    if dead == 0.0:
+        _, ws = _ws(T, 64, d, M, k, k)
+        s2 = torch.empty_like(sel)
+        c2 = torch.empty_like(sc)
+        L.dmoe_beam_topk(Gt, g, _alive_bits(alive), s2, c2, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(sel, s2) and torch.equal(sc.view(torch.int32), c2.view(torch.int32))

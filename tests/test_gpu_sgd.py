@@ -16,9 +16,11 @@ def _snap(lay):
 
 
 @pytest.mark.parametrize("recompute", [False, True])
-@pytest.mark.parametrize("name,T", [("mnist", 700), ("mnist", 1), ("stress_tied", 96)])
+@pytest.mark.parametrize("name,T", [("mnist", 700), ("mnist", 1), ("stress_tied", 96), ("mnist_pool8", 700)])
 def test_fused_sgd_step(name, T, recompute):
-    cfg = CONFIGS["stress"].with_(pool=8) if name == "stress_tied" else CONFIGS[name]
+    # mnist_pool8: 8 parameter slots of 32 tied experts, ~350 rows each -> CTA-pair GEMMs
+    cfg = {"stress_tied": CONFIGS["stress"].with_(pool=8), "mnist_pool8": CONFIGS["mnist"].with_(pool=8)}.get(
+        name, CONFIGS.get(name))
     inp = make_inputs(cfg, seed=40 + T, T=T)
     lay = gpu_layer(cfg, inp)            # one plain step: dW buffers, dxd
     dxd_ref = lay.dxd.clone()

@@ -192,3 +192,20 @@ def test_gap_definition():
     G2 = np.array([[0.0, -5.0, 3.0, 2.0, 0.5]])  # d=1, M=5
     _, _, gap2 = O.select_experts(G2, 1, 5, 2, 2, np.ones(5, np.uint8))
     assert gap2[0] == 1.0  # min(3-2, 2-0.5)
+
+
+@pytest.mark.parametrize("d,M,k,dead,seed", [(2, 4, 3, 0.4, 0), (3, 3, 4, 0.5, 1), (2, 6, 5, 0.2, 2), (1, 9, 4, 0.3, 3)])
+def test_topk_exact_equals_wide_beam(d, M, k, dead, seed):
+    """The exact alive top-k (the plain definition) equals Alg. 1 run with a beam at least as wide
+    as the number of prefixes at every level (reading X3: then no alive prefix is ever cut), with
+    integer-valued scores full of exact ties (X4 order), and on every all-dead / fully-alive case."""
+    rng = np.random.default_rng(seed)
+    E = M ** d
+    T = 300
+    G = rng.integers(-3, 4, (T, d * M)).astype(np.float64)
+    for alive in [(rng.random(E) >= dead).astype(np.uint8), np.ones(E, np.uint8), np.zeros(E, np.uint8)]:
+        sel_x, sc_x = O.topk_exact(G, d, M, k, alive)
+        B = max(k, M ** max(d - 1, 1))
+        sel_b, sc_b, _ = O.select_experts(G, d, M, k, B, alive)
+        assert np.array_equal(sel_x, sel_b)
+        np.testing.assert_array_equal(sc_x, sc_b)
