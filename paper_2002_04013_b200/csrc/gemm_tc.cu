@@ -35,6 +35,14 @@ constexpr int TC_BK = 64;  // one 128-byte swizzle atom of bf16
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void sts_v4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
@@ -45,15 +53,18 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// try_wait suspends the waiting warp until the phase completes (or this many ns pass): waiting
+// roles then stop spinning and leave the issue slots to the epilogue warps
+constexpr uint32_t kMbarSuspendNs = 1000000;
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
       "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(kMbarSuspendNs)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
@@ -239,7 +250,7 @@ __device__ unsigned long long g_tc_probe[8][TC_PROBE_ROLES][32];
 // 0 producer empty-wait, 1 producer loop, 2 mma tempty-wait, 3 mma full-wait, 4 mma zeroing,
 // 5 mma issue+commit, 6 mma loop, 7 epi tfull-wait (warp 4), 8 epi store-read wait, 9 epi loop,
 // 10 mma tiles, 11 CTAs, 12 mma issue without the commits
-__device__ unsigned long long g_tc_wait[8][16];
+__device__ unsigned long long g_tc_wait[8][20];
 #define WT_T0(v) const long long v = (DMOE_DBG(p) & 64) ? clock64() : 0
 #define WT_ADD(acc_, v) do { if (DMOE_DBG(p) & 64) acc_ += clock64() - v; } while (0)
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -249,6 +260,19 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #define PROBE(role, i) \
   do { if ((DMOE_DBG(p) & 8) && blockIdx.x == 0 && (i) < 32) g_tc_probe[p.slot][role][i] = gtimer(); } while (0)
+
+// n / d for a divisor fixed per launch (tile decode): multiply-high with a magic number
+// (round-up method, valid for n < 2^31, which tile indices are)
+struct FastDiv {
+  uint32_t d, m, s;
+  __device__ __forceinline__ void init(uint32_t d_) {
+    d = d_ > 0 ? d_ : 1;
+    s = 0;
+    while ((1u << s) < d) ++s;
+    m = (uint32_t)(((uint64_t)1 << 32) * (((uint64_t)1 << s) - d) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+};
 
 // ------------------------------------------------------------------------- kernel
 struct TcParams {
@@ -442,6 +466,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const bool leader = prank == 0;
   const int t_begin = PAIR ? (int)blockIdx.x >> 1 : (int)blockIdx.x, t_end = total;
   const int t_step = PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x;
+  FastDiv fd_e, fd_n, fd_e2, fd_n2;  // SEGK: tiles per expert, N tiles (both problems); ROWS: N tiles
+  fd_e.init(SEGK ? MT * NT : 1);
+  fd_n.init(NT);
+  fd_e2.init(SEGK ? MT2 * NT2 : 1);
+  fd_n2.init(NT2);
 
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -494,11 +523,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int prob = 0;
     if (SEGK) {
       int mt = MT, nt = NT;
-      if (tile >= total0) { prob = 1; tile -= total0; mt = MT2; nt = NT2; }
-      e = tile / (mt * nt);
+      const FastDiv* fe = &fd_e;
+      const FastDiv* fn = &fd_n;
+      if (tile >= total0) { prob = 1; tile -= total0; mt = MT2; nt = NT2; fe = &fd_e2; fn = &fd_n2; }
+      e = (int)fe->div((uint32_t)tile);
       const int rem = tile - e * mt * nt;
-      m0 = (rem / nt) * TC_BM;
-      n0 = (rem % nt) * BN;
+      const int mi = (int)fn->div((uint32_t)rem);
+      m0 = mi * TC_BM;
+      n0 = (rem - mi * nt) * BN;
       if (e != c_e) {
         c_e = e;
         c_r0 = offs[e];
@@ -508,7 +540,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       row_end = c_r1;
       nkb = (int)((row_end - row0 + TC_BK - 1) / TC_BK);
     } else {
-      const int rt = tile / NT;
+      const int rt = (int)fd_n.div((uint32_t)tile);
       n0 = (tile - rt * NT) * BN;
       m0 = 0;
       if (p.offsets) {
@@ -718,6 +750,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int stage = 0;
     uint32_t phase = 0;
     const int cchunk = lane >> 4, cunit = (lane & 15) >> 1, chalf = lane & 1;
+    long long w_fw = 0, w_fl = 0, w_fc = 0;
+    WT_T0(t_fl);
     for (int tile = t_begin; tile < t_end; tile += t_step) {
       int e, m0, n0, nkb;
       int64_t row0, row_end;
@@ -727,7 +761,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       const bool sums = colsum && n0 == 0;
       float cs[4] = {0.f, 0.f, 0.f, 0.f};
       for (int kb = 0; kb < nkb; ++kb) {
+        WT_T0(t_fw);
         mbar_wait(&full[stage], phase);
+        WT_ADD(w_fw, t_fw);
         uint8_t* sa = smem + stage * Cfg::STAGE_BYTES;
         uint8_t* sb = sa + Cfg::A_BYTES;
         const int64_t left = row_end - row0 - (int64_t)kb * TC_BK;
@@ -745,6 +781,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&ready[stage]);
+        WT_T0(t_fc);
         if (sums) {
           // 16 rows' loads in flight per batch (shared memory is busy with TMA / MMA / stores)
           const uint8_t* col = sa + cchunk * 8192 + chalf * 8;
@@ -765,6 +802,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
         }
         __syncwarp();
+        WT_ADD(w_fc, t_fc);
         if (lane == 0) mbar_arrive(&empty[stage]);
         if (++stage == S) { stage = 0; phase ^= 1; }
       }
@@ -779,6 +817,12 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           *dst = make_float4(cs[0], cs[1], cs[2], cs[3]);
         }
       }
+    }
+    WT_ADD(w_fl, t_fl);
+    if ((DMOE_DBG(p) & 64) && lane == 0) {
+      atomicAdd(&g_tc_wait[p.slot][13], (unsigned long long)w_fw);
+      atomicAdd(&g_tc_wait[p.slot][14], (unsigned long long)w_fl);
+      atomicAdd(&g_tc_wait[p.slot][15], (unsigned long long)w_fc);
     }
   } else if (warp >= 4) {
     // ======================= epilogue =======================
@@ -797,7 +841,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint32_t acc_phase = 0;
     int bias_buf = 0;
     int it = 0;
-    long long w_tf = 0, w_st = 0, w_loop = 0;
+    long long w_tf = 0, w_st = 0, w_loop = 0, w_ld = 0, w_pk = 0, w_is = 0;
     WT_T0(t_loop);
     for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
       int e, m0, n0, nkb;
@@ -883,13 +927,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int r = i * 4 + (lane >> 3), piece = lane & 7;
-            *reinterpret_cast<uint4*>(stg + r * TC_STAGE_ROW + piece * 16) = hreg[sb][i];
+            sts_v4(smem_u32(stg) + r * TC_STAGE_ROW + piece * 16, hreg[sb][i]);
           }
           __syncwarp();
           // this lane's row: one bit per column, 1 = h > 0
 #pragma unroll
           for (int piece = 0; piece < 8; ++piece) {
-            const uint4 hv = *reinterpret_cast<const uint4*>(stg + lane * TC_STAGE_ROW + piece * 16);
+            const uint4 hv = lds_v4(smem_u32(stg) + lane * TC_STAGE_ROW + piece * 16);
             const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -922,6 +966,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         (void)mw_lo;
         uint32_t racc[SUB];
         const bool tld = has_acc && !(DMOE_DBG(p) & 2);
+        WT_T0(t_ld);
         if (tld) {
 #pragma unroll
           for (int c16 = 0; c16 < SUB; c16 += 16) {
@@ -943,17 +988,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             released = true;
           }
         }
+        else {
+#pragma unroll
+          for (int j = 0; j < SUB; ++j) racc[j] = 0u;  // empty segment (or an experiment): zeros
+        }
+        WT_ADD(w_ld, t_ld);
+        WT_T0(t_pk);
 #pragma unroll
         for (int c16 = 0; c16 < SUB; c16 += 16) {
           if (c16 >= ncols) break;
           float v[16];
-          if (tld) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(racc[c16 + j]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = 0.0f;
-          }
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(racc[c16 + j]);
           if (HAS_BIAS) {
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] += bias_t[cs + c16 + j];
@@ -987,9 +1033,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
             for (int j = 0; j < 16; j += 8) {
               const int q = (c16 + j) >> 3;
-              uint4* slot = reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4));
+              const uint32_t slot = smem_u32(stg) + lane * 128 + ((q ^ (lane & 7)) << 4);
               if (sgd) {  // W <- W - lr * dW (fp32 arithmetic, one bf16 rounding: reading X21)
-                const uint4 wq = *slot;
+                const uint4 wq = lds_v4(slot);
                 const uint32_t ww[4] = {wq.x, wq.y, wq.z, wq.w};
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -997,8 +1043,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
                   v[j + 2 * i + 1] = bf16hi(ww[i]) - p.sgd_lr * v[j + 2 * i + 1];
                 }
               }
-              *slot = make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
-                                 pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+              sts_v4(slot, make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                                      pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7])));
             }
             continue;
           }
@@ -1008,22 +1054,24 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 #pragma unroll
             for (int j = 0; j < 16; j += 4) {
               const int pc = (c16 * 4 + j * 4) >> 4;
-              uint8_t* dst = STG_SWZ ? stg + lane * 128 + ((pc ^ (lane & 7)) << 4) : stg + lane * TC_STAGE_ROW + pc * 16;
-              *reinterpret_cast<float4*>(dst) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              const uint32_t dst = smem_u32(stg) + (STG_SWZ ? lane * 128 + ((pc ^ (lane & 7)) << 4) : lane * TC_STAGE_ROW + pc * 16);
+              sts_v4(dst, make_uint4(__float_as_uint(v[j]), __float_as_uint(v[j + 1]), __float_as_uint(v[j + 2]),
+                                     __float_as_uint(v[j + 3])));
             }
           } else {
 #pragma unroll
             for (int j = 0; j < 16; j += 8) {
               const int pc = (c16 * 2 + j * 2) >> 4;
-              uint8_t* dst = STG_SWZ ? stg + lane * 128 + ((pc ^ (lane & 7)) << 4) : stg + lane * TC_STAGE_ROW + pc * 16;
-              *reinterpret_cast<uint4*>(dst) =
-                  make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
-                             pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7]));
+              const uint32_t dst = smem_u32(stg) + (STG_SWZ ? lane * 128 + ((pc ^ (lane & 7)) << 4) : lane * TC_STAGE_ROW + pc * 16);
+              sts_v4(dst, make_uint4(pack_bf16x2(v[j], v[j + 1]), pack_bf16x2(v[j + 2], v[j + 3]),
+                                     pack_bf16x2(v[j + 4], v[j + 5]), pack_bf16x2(v[j + 6], v[j + 7])));
             }
           }
         }
+        WT_ADD(w_pk, t_pk);
         if (SEGK && !OUT_F32) {
           // full 32 x 64 box: one bulk tensor store (double-buffered box, see above)
+          WT_T0(t_is);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0 && !(DMOE_DBG(p) & 1)) {
@@ -1036,6 +1084,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           }
           stg_buf = (stg_buf + 1) % Cfg::NBOX;
           __syncwarp();
+          WT_ADD(w_is, t_is);
           continue;
         }
         __syncwarp();
@@ -1045,8 +1094,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         for (int i = 0; i < 8; ++i) {
           const int r = i * 4 + (lane >> 3), piece = lane & 7;
           if (r < live_rows && piece * 16 < row_bytes && !(DMOE_DBG(p) & 1)) {
-            const uint4 v = *reinterpret_cast<const uint4*>(
-                STG_SWZ ? stg + r * 128 + ((piece ^ (r & 7)) << 4) : stg + r * TC_STAGE_ROW + piece * 16);
+            const uint4 v = lds_v4(smem_u32(stg) + (STG_SWZ ? r * 128 + ((piece ^ (r & 7)) << 4) : r * TC_STAGE_ROW + piece * 16));
             uint8_t* gdst;
             if (SEGK)
               gdst = (uint8_t*)p.C + (((int64_t)e * p.Mdim + qrow0 + r) * p.N + n0 + cs) * OUT_ES + piece * 16;
@@ -1075,6 +1123,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       atomicAdd(&g_tc_wait[p.slot][7], (unsigned long long)w_tf);
       atomicAdd(&g_tc_wait[p.slot][8], (unsigned long long)w_st);
       atomicAdd(&g_tc_wait[p.slot][9], (unsigned long long)w_loop);
+      atomicAdd(&g_tc_wait[p.slot][16], (unsigned long long)w_ld);
+      atomicAdd(&g_tc_wait[p.slot][17], (unsigned long long)w_pk);
+      atomicAdd(&g_tc_wait[p.slot][18], (unsigned long long)w_is);
     }
   }
 
@@ -1384,7 +1435,7 @@ extern "C" int dmoe_debug_tc_wait(unsigned long long* host, int reset) {
   cudaDeviceSynchronize();
   int r = (int)cudaMemcpyFromSymbol(host, dmoe::g_tc_wait, sizeof(dmoe::g_tc_wait));
   if (reset) {
-    static unsigned long long zero[8 * 16] = {};
+    static unsigned long long zero[8 * 20] = {};
     r |= (int)cudaMemcpyToSymbol(dmoe::g_tc_wait, zero, sizeof(zero));
   }
   return r;

@@ -22,7 +22,7 @@ if len(sys.argv) > 2:  # overrides key=int, e.g. M=16 T=4096 (a transformer-shap
 lay, x, dy, alive, resp = bench.build_layer(cfg, 0, torch.device("cuda", 0), cfg.T)
 for _ in range(2):
     bench.run_calls(lay, x, dy, alive, resp)
-w = (ctypes.c_ulonglong * (8 * 16))()
+w = (ctypes.c_ulonglong * (8 * 20))()
 L._L.dmoe_debug_tc_wait(w, 1)
 c0 = L.dmoe_launch_counters()[1]
 bench.run_calls(lay, x, dy, alive, resp)
@@ -33,7 +33,7 @@ pb = (ctypes.c_ulonglong * (8 * R * 32))()
 L._L.dmoe_debug_tc_probe(pb, 8 * R * 32)
 for launch in range(c0, c1):
     s = launch % 8
-    v = [w[s * 16 + i] for i in range(16)]
+    v = [w[s * 20 + i] for i in range(20)]
     kid = pb[(s * R + 8) * 32]
     bn, segk, epi = kid >> 8, (kid >> 4) & 15, kid & 15
     ctas, tiles = max(v[11], 1), max(v[10], 1)
@@ -44,4 +44,7 @@ for launch in range(c0, c1):
     print(f"   mma     : tempty-wait {f(v[2], v[6])} full-wait {f(v[3], v[6])} zeroing {f(v[4], v[6])} "
           f"issue+commit {f(v[5], v[6])}  (per tile: tempty {v[2] / tiles:.0f} full {v[3] / tiles:.0f} "
           f"zero {v[4] / tiles:.0f} issue {v[5] / tiles:.0f} (mma only {v[12] / tiles:.0f}) cyc)")
-    print(f"   epilogue: tfull-wait {f(v[7], v[9])} store-read-wait {f(v[8], v[9])}")
+    if v[14]:
+        print(f"   fix-up  : full-wait {f(v[13], v[14])} colsum {f(v[15], v[14])}")
+    print(f"   epilogue: tfull-wait {f(v[7], v[9])} store-read-wait {f(v[8], v[9])} tmem-load {f(v[16], v[9])} "
+          f"pack+stage {f(v[17], v[9])} store-issue {f(v[18], v[9])}  (per tile: {v[9] / tiles:.0f} cyc)")
