@@ -56,6 +56,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // try_wait suspends the waiting warp until the phase completes (or this many ns pass): waiting
 // roles then stop spinning and leave the issue slots to the epilogue warps
 constexpr uint32_t kMbarSuspendNs = 1000000;
+#if defined(DMOE_EXPERIMENTS)
+__device__ uint32_t g_mbar_hint = kMbarSuspendNs;
+#define DMOE_MBAR_HINT g_mbar_hint
+#else
+#define DMOE_MBAR_HINT kMbarSuspendNs
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -64,7 +70,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(kMbarSuspendNs)
+      "r"(parity), "r"(DMOE_MBAR_HINT)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
@@ -578,10 +584,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (ptile >= t_end || !(DMOE_DBG(p) & 16)) return;  // opt-in (DMOE_TC_DEBUG=16): measured slower
         if (SEGK) {
           const int kr = (int)(prow0 + pkb * TC_BK);
-          tma_prefetch_2d(&tmA, pm0, kr);
-          tma_prefetch_2d(&tmA, pm0 + 64, kr);
-#pragma unroll
-          for (int c = 0; c < BN / 64; ++c) tma_prefetch_2d(&tmB, pn0 + 64 * c, kr);
+          tma_prefetch_3d(&tmA, 0, kr, pm0 / 64);
+          tma_prefetch_3d(&tmB, 0, kr, pn0 / 64);
         } else if (B_MN) {
 #pragma unroll
           for (int c = 0; c < BN / 64; ++c) tma_prefetch_3d(&tmB, pn0 + 64 * c, pkb * TC_BK, pe);
@@ -635,16 +639,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if (++stage == S) { stage = 0; phase ^= 1; }
             continue;
           }
+          if (SEGK && (DMOE_DBG(p) & 512)) {  // experiments: no operand loads (pipeline skeleton)
+            mbar_expect_tx(&full[stage], 0);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+            continue;
+          }
           mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           if (SEGK) {
             const int kr = (int)(row0 + kb * TC_BK);
             const CUtensorMap* mA = prob ? &tmA2 : &tmA;
             const CUtensorMap* mB = prob ? &tmB2 : &tmB;
-            tma_load_2d_h(sa, mA, &full[stage], m0, kr, pol_keep);
-            tma_load_2d_h(sa + 8192, mA, &full[stage], m0 + 64, kr, pol_keep);
-#pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              tma_load_2d_h(sb + c * 8192, mB, &full[stage], n0 + 64 * c, kr, pol_keep);
+            tma_load_3d_h(sa, mA, &full[stage], 0, kr, m0 / 64, pol_keep);  // 2 chunks of 64 columns
+            tma_load_3d_h(sb, mB, &full[stage], 0, kr, n0 / 64, pol_keep);  // BN / 64 chunks
           } else {
             tma_load_2d_h(sa, &tmA, &full[stage], kb * TC_BK, (int)row0, pol_keep);
             if (B_MN) {
@@ -718,6 +724,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
           if (PAIR) {
             tc_commit_pair(&empty[stage]);
             if (kb == nkb - 1) tc_commit_pair(&tfull[acc]);
+          } else if (DMOE_DBG(p) & 4096) {  // experiments (with MMAs skipped): plain arrivals
+            mbar_arrive(&empty[stage]);
+            if (kb == nkb - 1) mbar_arrive(&tfull[acc]);
           } else {
             tc_commit(&empty[stage]);
             if (kb == nkb - 1) { tc_commit(&tfull[acc]); PROBE(3, it); }
@@ -770,13 +779,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         const int valid = left < TC_BK ? (int)left : TC_BK;
         const int lines = ((valid + 15) & ~15) - valid;
         if (lines > 0) {
-          constexpr int nchunk = 2 + BN / 64;  // 128-byte lines per K row across A and B chunks
-          for (int i = lane; i < lines * nchunk * 8; i += 32) {
-            const int piece = i & 7, rest = i >> 3;
-            const int c = rest % nchunk, r = valid + rest / nchunk;
-            uint8_t* base = c < 2 ? sa + c * 8192 : sb + (c - 2) * 8192;
-            *reinterpret_cast<uint4*>(base + r * 128 + piece * 16) = make_uint4(0, 0, 0, 0);
-          }
+          // 128-byte lines per K row: A's 2 chunks then B's BN / 64, 8 KB apart from sa on (a line
+          // is zeroed whole, so the 128-byte swizzle inside it does not matter); lane = (row % 4,
+          // 16-byte piece)
+          constexpr int nchunk = 2 + BN / 64;
+          const uint32_t z0 = smem_u32(sa) + (uint32_t)valid * 128 + (lane & 7) * 16;
+#pragma unroll
+          for (int c = 0; c < nchunk; ++c)
+            for (int r = lane >> 3; r < lines; r += 4) sts_v4(z0 + c * 8192 + r * 128, make_uint4(0, 0, 0, 0));
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncwarp();
@@ -1072,7 +1082,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         if (SEGK && !OUT_F32) {
           // full 32 x 64 box: one bulk tensor store (double-buffered box, see above)
           WT_T0(t_is);
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (!(DMOE_DBG(p) & 1024)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0 && !(DMOE_DBG(p) & 1)) {
             asm volatile(
@@ -1178,6 +1188,23 @@ static dmoe_status make_map(CUtensorMap* m, const void* ptr, int rank, const uin
   return DMOE_OK;
 }
 
+// weight-gradient operands ([rows][cols] row-major, MN-major for the MMA) as a 3D view
+// {64 cols, rows, cols / 64 chunks} so that one box {64, 64, chunks} brings a whole 64-row K
+// block of a 128- or 256-column tile in one TMA command (chunk c lands 8 KB after chunk c-1:
+// the layout of one 2D box per 64 columns)
+static dmoe_status make_map_chunked(CUtensorMap* m, const void* ptr, uint64_t cols, uint64_t rows,
+                                    uint32_t chunks) {
+  EncodeTiledFn fn = encode_fn();
+  DMOE_REQUIRE(fn != nullptr, DMOE_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t gdim[3] = {64, rows, cols / 64}, gstride[2] = {cols * 2, 128};
+  cuuint32_t box[3] = {64, 64, chunks}, estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), gdim, gstride, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DMOE_REQUIRE(r == CUDA_SUCCESS, DMOE_ERR_CUDA, "cuTensorMapEncodeTiled (chunked) failed (%d)", (int)r);
+  return DMOE_OK;
+}
+
 // N tile: 256 when it divides N, else 128; K-major B also takes any N = 16..256 in one tile
 // (the gate, N = d*M) and MN-major B any multiple of 64 up to 256.
 static int pick_bn(int N, bool b_mn) {
@@ -1271,6 +1298,16 @@ static dmoe_status launch_maps_p(const CUtensorMap& a, const CUtensorMap& b, con
   if (grid < (PAIR ? 2 : 1)) grid = PAIR ? 2 : 1;
   TcParams pp = p;
   pp.dbg = debug_flags() | (SEGK ? debug_flags_segk() : 0);
+#if defined(DMOE_EXPERIMENTS)
+  static bool hint_set = false;
+  if (!hint_set) {  // DMOE_MBAR_HINT=<ns>: the mbarrier try_wait suspend-time hint
+    hint_set = true;
+    if (const char* e = dmoe_env("DMOE_MBAR_HINT")) {
+      const uint32_t v = (uint32_t)atoi(e);
+      cudaMemcpyToSymbol(g_mbar_hint, &v, sizeof(v));
+    }
+  }
+#endif
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
   pp.stages = Cfg::stages_for(table_len);
   pp.table_len = table_len;
@@ -1377,10 +1414,8 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   // K rows past a segment end (other experts' rows, or capacity rows past R) are zeroed
   // in smem before the MMA; rows past R_cap are zero-filled by TMA.
   const uint64_t rc = (uint64_t)(g.R_cap > 0 ? g.R_cap : 1);
-  uint64_t adims[2] = {(uint64_t)g.Mdim, rc};
-  uint64_t bdims[2] = {(uint64_t)g.N, rc};
-  DMOE_TRY(make_map(&ta, g.A, 2, adims, 64));
-  DMOE_TRY(make_map(&tb, g.B, 2, bdims, 64));
+  DMOE_TRY(make_map_chunked(&ta, g.A, (uint64_t)g.Mdim, rc, TC_BM / 64));
+  DMOE_TRY(make_map_chunked(&tb, g.B, (uint64_t)g.N, rc, (uint32_t)(BN / 64)));
   // output dW [E][Mdim][N] as a 2D [E*Mdim, N] map, 64 x 32 boxes (bulk tensor stores)
   CUtensorMap tc;
   if (!g.out_f32) {
@@ -1413,11 +1448,9 @@ dmoe_status tc_gemm_segk2(const GemmSegK& g, const GemmSegK& h, cudaStream_t s) 
   for (int i = 0; i < 2; ++i) {
     const GemmSegK& x = *gs[i];
     const uint64_t rc = (uint64_t)(x.R_cap > 0 ? x.R_cap : 1);
-    uint64_t adims[2] = {(uint64_t)x.Mdim, rc};
-    uint64_t bdims[2] = {(uint64_t)x.N, rc};
     uint64_t cdims[2] = {(uint64_t)x.N, (uint64_t)x.E * x.Mdim};
-    DMOE_TRY(make_map(&m[3 * i + 0], x.A, 2, adims, 64));
-    DMOE_TRY(make_map(&m[3 * i + 1], x.B, 2, bdims, 64));
+    DMOE_TRY(make_map_chunked(&m[3 * i + 0], x.A, (uint64_t)x.Mdim, rc, TC_BM / 64));
+    DMOE_TRY(make_map_chunked(&m[3 * i + 1], x.B, (uint64_t)x.N, rc, 256 / 64));
     DMOE_TRY(make_map(&m[3 * i + 2], x.C, 2, cdims, 32));
   }
   TcParams p{};

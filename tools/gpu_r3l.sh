@@ -1,0 +1,19 @@
+# full-size weight-gradient GEMM with parts switched off (EXPERIMENTS build): data-movement bound?
+mkdir -p gpurun_out/r3l
+make -s clean && make -s -j8 all EXPERIMENTS=1 2>&1 | tail -2
+lst() {
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_tc_gemm -c 14 --csv --log-file gpurun_out/r3l/l_$1.csv python tools/profile_step.py --config transformer --steps 2 --set $2 > /dev/null 2>&1
+python - $1 <<'PY'
+import csv, sys
+rows = list(csv.reader(open(f"gpurun_out/r3l/l_{sys.argv[1]}.csv")))
+hdr = [r for r in rows if "Kernel Name" in r][0]
+out = [dict(zip(hdr, r)) for r in rows if len(r) == len(hdr) and r != hdr]
+for d in out[-7:]: print(sys.argv[1], d["Kernel Name"].split("(")[0][:40], round(float(d["Metric Value"]) / 1000, 1), "us")
+PY
+}
+DMOE_TC_DEBUG_SEGK=519 lst skeleton_full "M=64"
+DMOE_TC_DEBUG_SEGK=4615 lst skel_nocommit_full "M=64"
+DMOE_TC_DEBUG_SEGK=4615 lst skel_nocommit_k64 "M=16 T=4096"
+DMOE_TC_DEBUG_SEGK=519 lst skeleton_k64 "M=16 T=4096"
+lst base_full "M=64"
+make -s clean && make -s -j8 all 2>&1 | tail -2
