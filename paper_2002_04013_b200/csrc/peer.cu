@@ -145,29 +145,57 @@ k_ep_plan(const int32_t* __restrict__ cnt, int G, int rank, int E, int El, int64
   }
 }
 
-// dispatch-order rows -> owners' expert-major buffers.  Row r of expert e (offsets[e] <= r <
-// offsets[e+1]) goes to peer_dst[owner(e)][base[e] + r - offsets[e]].  Source row = src[gidx[r]]
-// when gidx is given (x gathered by token_of_row: the dispatch gather fused with the send),
-// else src[r].  err != 0 (plan overflow) skips all writes.
+// Both row movers (err != 0, a plan overflow, skips all writes) run a warp per row over contiguous row chunks (rows are expert-major, so the
+// row's expert advances linearly from one binary search per warp); a row is D/V 16-byte vectors,
+// loaded 4 per lane before the first (NVLink peer) store.
 template <typename T>
-__global__ void k_ep_push_rows(const T* __restrict__ src, const int32_t* __restrict__ gidx,
-                               const int32_t* __restrict__ offsets, const int32_t* __restrict__ base, int E, int El,
-                               int32_t D, T* const* peer_dst, const int32_t* __restrict__ err) {
+__device__ __forceinline__ void copy_row_warp(T* __restrict__ dst, const T* __restrict__ src, int vecs, int lane) {
+  constexpr int V = Vec16<T>::N;
+  for (int v = lane; v < vecs; v += 32 * 4) {
+    uint4 a[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v + 32 * u < vecs) a[u] = ld_nc_v4(src + (int64_t)(v + 32 * u) * V);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v + 32 * u < vecs) st_v4(dst + (int64_t)(v + 32 * u) * V, a[u]);
+  }
+}
+
+__device__ __forceinline__ int seg_of(const int32_t* __restrict__ offsets, int n, int64_t r) {
+  int lo = 0, hi = n;  // offsets[lo] <= r < offsets[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (offsets[mid] <= r) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// dispatch-order rows (expert-major over all E experts) -> owners' receive buffers: row r of
+// expert e (owner e / El) goes to peer_dst[owner][base[e] + r - offsets[e]]; its source row is
+// gidx[r] (the fused dispatch gather) or r.
+template <typename T>
+__global__ void __launch_bounds__(256)
+k_ep_push_rows(const T* __restrict__ src, const int32_t* __restrict__ gidx, const int32_t* __restrict__ offsets,
+               const int32_t* __restrict__ base, int E, int El, int32_t D, T* const* peer_dst,
+               const int32_t* __restrict__ err) {
   DMOE_PDL_ENTRY();
   if (*err) return;
   constexpr int V = Vec16<T>::N;
   const int64_t R = offsets[E];
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t per = (R + nw - 1) / nw;
+  const int64_t r0 = w * per, r1 = r0 + per < R ? r0 + per : R;
+  if (r0 >= r1) return;
+  int e = seg_of(offsets, E, r0);
+  int64_t e_beg = offsets[e], e_end = offsets[e + 1];
   const int vecs = D / V;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R * vecs;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / vecs;
-    const int v = (int)(i - r * vecs);
-    int lo = 0, hi = E;
-    while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (offsets[mid] <= r) lo = mid; else hi = mid; }
-    const int e = lo;
+  for (int64_t r = r0; r < r1; ++r) {
+    while (r >= e_end) { ++e; e_beg = e_end; e_end = offsets[e + 1]; }
     const int64_t srow = gidx ? (int64_t)gidx[r] : r;
-    T* dst = peer_dst[e / El] + ((int64_t)base[e] + (r - offsets[e])) * D + (int64_t)v * V;
-    st_v4(dst, ld_nc_v4(src + srow * D + (int64_t)v * V));
+    copy_row_warp(peer_dst[e / El] + ((int64_t)base[e] + (r - e_beg)) * D, src + srow * D, vecs, lane);
   }
 }
 
@@ -175,27 +203,30 @@ __global__ void k_ep_push_rows(const T* __restrict__ src, const int32_t* __restr
 // el from source s (dst_off[s][el] <= q < dst_off[s][el] + cnt[s][e]) goes to
 // peer_dst[s][src_off[s][el] + q - dst_off[s][el]].
 template <typename T>
-__global__ void k_ep_return_rows(const T* __restrict__ src, const int32_t* __restrict__ cnt,
-                                 const int32_t* __restrict__ off_loc, const int32_t* __restrict__ src_off,
-                                 const int32_t* __restrict__ dst_off, int G, int rank, int E, int El, int32_t D,
-                                 T* const* peer_dst, const int32_t* __restrict__ err) {
+__global__ void __launch_bounds__(256)
+k_ep_return_rows(const T* __restrict__ src, const int32_t* __restrict__ cnt, const int32_t* __restrict__ off_loc,
+                 const int32_t* __restrict__ src_off, const int32_t* __restrict__ dst_off, int G, int rank, int E,
+                 int El, int32_t D, T* const* peer_dst, const int32_t* __restrict__ err) {
   DMOE_PDL_ENTRY();
   if (*err) return;
   constexpr int V = Vec16<T>::N;
   const int64_t R = off_loc[El];
+  const int lane = threadIdx.x & 31;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t per = (R + nw - 1) / nw;
+  const int64_t q0 = w * per, q1 = q0 + per < R ? q0 + per : R;
+  if (q0 >= q1) return;
+  int el = seg_of(off_loc, El, q0);
+  int64_t el_end = off_loc[el + 1];
   const int vecs = D / V;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R * vecs;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = i / vecs;
-    const int v = (int)(i - q * vecs);
-    int lo = 0, hi = El;
-    while (hi - lo > 1) { const int mid = (lo + hi) >> 1; if (off_loc[mid] <= q) lo = mid; else hi = mid; }
-    const int el = lo;
+  for (int64_t q = q0; q < q1; ++q) {
+    while (q >= el_end) { ++el; el_end = off_loc[el + 1]; }
     const int e = rank * El + el;
-    int s = 0;
-    while (s + 1 < G && q >= dst_off[s * El + el] + cnt[(int64_t)s * E + e]) ++s;
-    const int64_t drow = (int64_t)src_off[s * El + el] + (q - dst_off[s * El + el]);
-    st_v4(peer_dst[s] + drow * D + (int64_t)v * V, ld_nc_v4(src + q * D + (int64_t)v * V));
+    int sidx = 0;
+    while (sidx + 1 < G && q >= dst_off[sidx * El + el] + cnt[(int64_t)sidx * E + e]) ++sidx;
+    const int64_t drow = (int64_t)src_off[sidx * El + el] + (q - dst_off[sidx * El + el]);
+    copy_row_warp(peer_dst[sidx] + drow * D, src + q * D, vecs, lane);
   }
 }
 

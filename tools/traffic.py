@@ -3,7 +3,7 @@
 the kernels each call launches, for one step; written to profiles/<name>.json for bench.py's
 roofline `traffic` field.
 
-  python tools/traffic.py gpurun_out/launches_tf.csv transformer profiles/r01_traffic_transformer.json
+  python tools/traffic.py gpurun_out/launches_tf.csv transformer profiles/r02_traffic_transformer.json
 """
 import csv
 import json
@@ -11,17 +11,18 @@ import sys
 
 # kernel-name prefixes launched by each ABI call, in step order
 CALLS = [
-    ("gate_topk", ["k_transpose", "k_tc_gemm<32, 0, 0, 5>", "k_tc_gemm<48, 0, 0, 5>", "k_tc_gemm<128, 0, 0, 5>",
-                   "k_tc_gemm<32, 0, 0, 0>", "k_tc_gemm<48, 0, 0, 0>", "k_tc_gemm<128, 0, 0, 0>", "k_simt_rows",
-                   "k_prefix_alive", "k_beam_topk"]),
+    ("gate_topk", ["k_transpose", "k_tc_gemm<32, 0, 0, 0", "k_tc_gemm<48, 0, 0, 0", "k_tc_gemm<64, 0, 0, 0",
+                   "k_tc_gemm<128, 0, 0, 0", "k_tc_gemm<256, 0, 0, 0", "k_simt_rows", "k_prefix_alive", "k_beam_topk",
+                   "k_topk_exact"]),
     ("dispatch", ["k_weights_hist", "k_scan_chunks", "k_scan_experts", "k_rank", "k_scatter", "k_gather"]),
-    ("expert_ffn_fwd", ["k_tile_plan", "k_tc_gemm<256, 0, 0, 1>", "k_tc_gemm<256, 0, 0, 2>", "k_tc_gemm<128, 0, 0, 1>",
-                        "k_tc_gemm<128, 0, 0, 2>"]),
+    ("expert_ffn_fwd", ["k_tile_plan", "k_tc_gemm<256, 0, 0, 1", "k_tc_gemm<256, 0, 0, 2", "k_tc_gemm<128, 0, 0, 1",
+                        "k_tc_gemm<128, 0, 0, 2"]),
     ("combine", ["k_combine<"]),
     ("combine_bwd", ["k_combine_bwd"]),
-    ("expert_ffn_bwd", ["k_tile_plan", "k_tc_gemm<256, 0, 1", "k_tc_gemm<128, 0, 1", "k_tc_gemm<128, 1, 1",
-                        "k_tc_gemm<256, 1, 1", "k_seg_colsum"]),
-    ("gate_bwd", ["k_transpose", "k_gate_bwd_dx", "k_dwg_sparse", "k_dwg_partial", "k_dwg_reduce"]),
+    ("expert_ffn_bwd", ["k_tile_plan", "k_tc_gemm<256, 0, 1", "k_tc_gemm<128, 0, 1", "k_tc_gemm<128, 1, 1, 4",
+                        "k_tc_gemm<256, 1, 1, 4", "k_seg_colsum"]),
+    ("gate_bwd", ["k_transpose", "k_gate_bwd_dx", "k_tc_gemm<128, 1, 1, 6", "k_tc_gemm<256, 1, 1, 6",
+                  "k_gate_reduce", "k_dwg_partial", "k_dwg_reduce"]),
 ]
 
 
@@ -41,7 +42,8 @@ def main(path, name, out):
                 order.append(key)
             kern[key][d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
     allk = [kern[k] for k in order]
-    gate = ("k_tc_gemm<32", "k_tc_gemm<48", "k_tc_gemm<128, 0, 0, 0>", "k_tc_gemm<256, 0, 0, 0>", "k_simt_rows")
+    gate = ("k_tc_gemm<32, 0, 0, 0", "k_tc_gemm<48, 0, 0, 0", "k_tc_gemm<64, 0, 0, 0", "k_tc_gemm<128, 0, 0, 0",
+            "k_tc_gemm<256, 0, 0, 0", "k_simt_rows")
     starts = [j for j in range(len(allk) - 1)
               if allk[j]["name"].startswith("k_transpose") and allk[j + 1]["name"].startswith(gate)]
     seq = allk[starts[-1]:]  # the last full step (gate transpose .. gate backward)
