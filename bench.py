@@ -427,7 +427,23 @@ def bench_ours(args, cfg, rank, world, local_rank):
         pipe.submit(hx, hdy, hy, hdx)
     b.record(pipe.d2h)
     b.synchronize()
-    e2e = a.elapsed_time(b) / args.steps
+    e2e_pipe = a.elapsed_time(b) / args.steps
+    e2e, e2e_api = e2e_pipe, "HostPipeline.submit (copies of neighbouring steps overlapped, no L2 flush: weights > L2)"
+    # the C ABI's own host-buffer step (dmoe_layer_step_host: H2D of x, dy, all of S1-S10, D2H of
+    # y, dX inside one call), K calls back to back on the stream: the e2e headline when the layer
+    # has the 2-linear experts
+    if cfg.expert == "ffn2" and lay.dW1.shape[0] == lay.P:
+        desc = lay.host_desc(alive, resp)
+        for _ in range(args.warmup):
+            lay.step_host_c(desc, hx, hdy, hy, hdx)
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(args.steps):
+            lay.step_host_c(desc, hx, hdy, hy, hdx)
+        b.record()
+        b.synchronize()
+        e2e = a.elapsed_time(b) / args.steps
+        e2e_api = "dmoe_layer_step_host (C ABI; pinned host x, dy in and y, dX out inside each call; no L2 flush)"
     if world > 1:
         t = torch.tensor([e2e], device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -436,6 +452,7 @@ def bench_ours(args, cfg, rank, world, local_rank):
     E_act = int((lay.seg[1:] - lay.seg[:-1] > 0).sum().item())
     n_dropped = int(lay.n_dropped.item())
     return dict(ms=ms, step_ms=step_ms, per_call_ms=per_call_ms, e2e_ms=e2e, R=R, E_act=E_act,
+                e2e_api=e2e_api, e2e_pipelined_ms=e2e_pipe,
                 n_dropped=n_dropped, launches=launches_per_step, tc_launches=tc_per_step, clocks=clk.summary(),
                 h2d=2 * T * cfg.D * x.element_size(), d2h=2 * T * cfg.D * x.element_size())
 
@@ -744,8 +761,12 @@ def main():
                    "graph": "eager (host split sizes per step)" if (world > 1 and os.environ.get("DMOE_EP") == "nccl")
                    else "cuda graph replay"},
         "e2e": {"value": e2e_v, "unit": "tokens/s", "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"],
-                "api": "HostPipeline.submit (copies of neighbouring steps overlapped, no L2 flush: weights > L2)"
-                if (world == 1 or os.environ.get("DMOE_EP", "peer") != "nccl") else "step_host (per step)"},
+                "api": r.get("e2e_api") or ("HostPipeline.submit (copies of neighbouring steps overlapped, no L2 flush: "
+                                            "weights > L2)" if (world == 1 or os.environ.get("DMOE_EP", "peer") != "nccl")
+                                            else "step_host (per step)"),
+                **({"pipelined_value": tokens / (r["e2e_pipelined_ms"] / 1e3),
+                    "pipelined_api": "HostPipeline.submit (Python: double-buffered device staging, copies of "
+                                     "neighbouring steps overlapped)"} if r.get("e2e_pipelined_ms") else {})},
         "gpu_launches": r["launches"] * args.steps,
         "roofline": roof,
         "clocks": r["clocks"],

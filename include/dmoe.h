@@ -340,6 +340,40 @@ dmoe_status dmoe_ipc_open(const void* handle, void** ptr);
 dmoe_status dmoe_ipc_close(void* ptr);
 dmoe_status dmoe_ipc_free(void* ptr);
 
+/* One whole layer step from HOST buffers (the end-to-end unit): x and dy
+ * are copied host -> device, S1-S10 run (forward: gate + beam search, dispatch, expert FFN,
+ * combine; backward: combine backward, expert backward with dW written, gate backward), and y
+ * and dX are copied device -> host, all on `stream` (dy's upload overlaps the forward and y's
+ * download overlaps the backward on a library copy stream joined back into `stream` before the
+ * call's work completes).  Every pointer in dmoe_layer is caller-owned DEVICE memory sized for
+ * T_max tokens (the ones the per-call entry points above take); x_host, dy_host, y_host,
+ * dx_host are host memory of [T, D] dt (pinned for asynchronous copies; pageable memory works
+ * but the copies then synchronise).  tie > 1: the tied-weight pool (reading X20) with E / tie
+ * parameter slots and seg [E/tie + 1]; tie == 1: seg is unused.  G, h and hmask may be NULL
+ * (no scores kept / no saved-activation mask).  Errors: any entry point's status. */
+typedef struct {
+  dmoe_grid g;
+  int32_t D, H, tie;
+  dmoe_dtype dt;
+  int64_t T_max, R_cap;                       /* R_cap = T_max * k capacity rows            */
+  const void* Wg; const float* bg;            /* gate [D, d*M], [d*M]                        */
+  const void* W1; const float* b1;            /* experts [E/tie, H, D], [E/tie, H]           */
+  const void* W2; const float* b2;            /*         [E/tie, D, H], [E/tie, D]           */
+  const uint32_t* alive_bits; const uint32_t* responded_bits;
+  void* x; void* dy;                          /* [T_max, D] device staging                   */
+  float* G;                                   /* [T_max, d*M] or NULL                        */
+  int32_t* sel; float* sel_score; float* w; uint8_t* valid; int32_t* n_dropped;
+  int32_t* counts; int32_t* offsets; int32_t* seg;
+  int32_t* row_of_slot; int32_t* token_of_row;
+  void* xd; void* h; uint32_t* hmask; void* out; void* y;
+  void* dout; float* dscore; void* dxd;
+  void* dW1; float* db1; void* dW2; float* db2;
+  void* dx; float* dWg; float* dbg;
+  void* ws; size_t ws_bytes;
+} dmoe_layer;
+dmoe_status dmoe_layer_step_host(const dmoe_layer* layer, int64_t T, const void* x_host, const void* dy_host,
+                                 void* y_host, void* dx_host, dmoe_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

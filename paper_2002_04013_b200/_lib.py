@@ -32,6 +32,17 @@ class dmoe_ep(ctypes.Structure):
                                        "src_off", "dst_off")]
 
 
+class dmoe_layer(ctypes.Structure):
+    """include/dmoe.h dmoe_layer: device pointers of one layer for dmoe_layer_step_host."""
+    _fields_ = [("g", dmoe_grid), ("D", ctypes.c_int32), ("H", ctypes.c_int32), ("tie", ctypes.c_int32),
+                ("dt", ctypes.c_int32), ("T_max", ctypes.c_int64), ("R_cap", ctypes.c_int64)] + [
+        (n, ctypes.c_void_p) for n in (
+            "Wg", "bg", "W1", "b1", "W2", "b2", "alive_bits", "responded_bits", "x", "dy", "G",
+            "sel", "sel_score", "w", "valid", "n_dropped", "counts", "offsets", "seg", "row_of_slot",
+            "token_of_row", "xd", "h", "hmask", "out", "y", "dout", "dscore", "dxd", "dW1", "db1", "dW2",
+            "db2", "dx", "dWg", "dbg", "ws")] + [("ws_bytes", ctypes.c_size_t)]
+
+
 class DMoEError(RuntimeError):
     def __init__(self, fn, status):
         msg = _L.dmoe_last_error().decode()
@@ -76,6 +87,7 @@ _SIGS = {
     "dmoe_ipc_close": ([_P], ctypes.c_int),
     "dmoe_ipc_free": ([_P], ctypes.c_int),
     "dmoe_permute_rows": ([_P, _I32, _P, _P, _I32, _I32, _P, _P], ctypes.c_int),
+    "dmoe_layer_step_host": ([_P, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_L, _name)
@@ -83,7 +95,7 @@ for _name, (_args, _res) in _SIGS.items():
     _f.restype = _res
 
 EXPORTED = tuple(_SIGS)
-__all__ = [n for n in _SIGS if n != "dmoe_last_error"] + ["grid", "DMoEError", "dmoe_ep", "dmoe_grid"]
+__all__ = [n for n in _SIGS if n != "dmoe_last_error"] + ["grid", "DMoEError", "dmoe_ep", "dmoe_grid", "dmoe_layer"]
 
 
 def _check(fn, st):
@@ -282,3 +294,11 @@ def dmoe_ipc_close(ptr):
 
 def dmoe_ipc_free(ptr):
     _check("dmoe_ipc_free", _L.dmoe_ipc_free(ptr))
+
+
+def dmoe_layer_step_host(layer, T, x_host, dy_host, y_host, dx_host):
+    """One layer step from host buffers (pinned torch CPU tensors [T, D]); layer: dmoe_layer."""
+    for t in (x_host, dy_host, y_host, dx_host):
+        assert not t.is_cuda and t.is_contiguous()
+    _check("dmoe_layer_step_host", _L.dmoe_layer_step_host(ctypes.byref(layer), T, _p(x_host), _p(dy_host),
+                                                           _p(y_host), _p(dx_host), _stream()))

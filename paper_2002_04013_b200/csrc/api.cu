@@ -824,3 +824,83 @@ dmoe_status dmoe_ipc_free(void* ptr) {
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ host-buffer layer step
+namespace {
+struct CopyStream {  // per (device, caller stream): the host step's copy stream and its events
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+std::mutex g_copy_mu;
+std::map<std::pair<int, cudaStream_t>, CopyStream> g_copy;
+CopyStream* copy_for(cudaStream_t s) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_copy_mu);
+  CopyStream& cs = g_copy[{dev, s}];
+  if (!cs.st) {
+    if (cudaStreamCreateWithFlags(&cs.st, cudaStreamNonBlocking) != cudaSuccess) { cs.st = nullptr; return nullptr; }
+    for (auto& e : cs.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  return &cs;
+}
+}  // namespace
+
+extern "C" dmoe_status dmoe_layer_step_host(const dmoe_layer* L, int64_t T, const void* x_host,
+                                            const void* dy_host, void* y_host, void* dx_host,
+                                            dmoe_stream_t stream) {
+  DMOE_NVTX();
+  DMOE_REQUIRE(L && x_host && dy_host && y_host && dx_host, DMOE_ERR_ARG, "layer_step_host: null argument");
+  DMOE_REQUIRE(T >= 0 && T <= L->T_max, DMOE_ERR_SHAPE, "layer_step_host: T=%lld outside [0, T_max=%lld]",
+               (long long)T, (long long)L->T_max);
+  DMOE_REQUIRE(L->tie >= 1, DMOE_ERR_ARG, "layer_step_host: tie=%d < 1", L->tie);
+  cudaStream_t s = (cudaStream_t)stream;
+  const dmoe_grid g = L->g;
+  int64_t E = 1;
+  for (int i = 0; i < g.d; ++i) E *= g.M;
+  DMOE_REQUIRE(E % L->tie == 0, DMOE_ERR_SHAPE, "layer_step_host: tie=%d does not divide E=%lld", L->tie,
+               (long long)E);
+  const int32_t El = (int32_t)(E / L->tie);
+  const int32_t* seg = L->tie > 1 ? L->seg : L->offsets;
+  const size_t nbytes = (size_t)T * L->D * (L->dt == DMOE_BF16 ? 2 : 4);
+  CopyStream* cs = copy_for(s);
+  DMOE_REQUIRE(cs != nullptr, DMOE_ERR_CUDA, "layer_step_host: copy stream: %s",
+               cudaGetErrorString(cudaGetLastError()));
+#define DMOE_CU(x_)                                                                                 \
+  do {                                                                                              \
+    cudaError_t e_ = (x_);                                                                          \
+    if (e_ != cudaSuccess) return set_error(DMOE_ERR_CUDA, "layer_step_host: %s", cudaGetErrorString(e_)); \
+  } while (0)
+  // dy: uploaded on the copy stream once the stream's earlier work (the previous step) is done
+  DMOE_CU(cudaEventRecord(cs->ev[0], s));
+  DMOE_CU(cudaStreamWaitEvent(cs->st, cs->ev[0], 0));
+  DMOE_CU(cudaMemcpyAsync(L->dy, dy_host, nbytes, cudaMemcpyHostToDevice, cs->st));
+  DMOE_CU(cudaEventRecord(cs->ev[1], cs->st));
+  DMOE_CU(cudaMemcpyAsync(L->x, x_host, nbytes, cudaMemcpyHostToDevice, s));
+  // forward (S1-S7)
+  DMOE_TRY(dmoe_gate_topk(L->x, L->dt, T, L->D, L->Wg, L->bg, g, L->alive_bits, L->G, L->sel, L->sel_score, L->ws,
+                          L->ws_bytes, stream));
+  DMOE_TRY(dmoe_dispatch(L->x, L->dt, T, L->D, g, L->sel, L->sel_score, L->responded_bits, L->w, L->valid,
+                         L->n_dropped, L->counts, L->offsets, L->row_of_slot, L->token_of_row, L->xd, L->ws,
+                         L->ws_bytes, stream));
+  if (L->tie > 1) DMOE_TRY(dmoe_segment_offsets(L->offsets, (int32_t)E, L->tie, L->seg, stream));
+  DMOE_TRY(dmoe_expert_ffn_fwd(L->xd, seg, El, L->R_cap, L->D, L->H, L->dt, L->W1, L->b1, L->W2, L->b2, L->h,
+                               L->hmask, L->out, L->ws, L->ws_bytes, stream));
+  DMOE_TRY(dmoe_combine(L->out, L->row_of_slot, L->w, L->valid, T, L->D, g.k, L->dt, L->y, stream));
+  // y: downloaded on the copy stream while the backward runs
+  DMOE_CU(cudaEventRecord(cs->ev[2], s));
+  DMOE_CU(cudaStreamWaitEvent(cs->st, cs->ev[2], 0));
+  DMOE_CU(cudaMemcpyAsync(y_host, L->y, nbytes, cudaMemcpyDeviceToHost, cs->st));
+  // backward (S8-S10)
+  DMOE_CU(cudaStreamWaitEvent(s, cs->ev[1], 0));
+  DMOE_TRY(dmoe_combine_bwd(L->dy, L->out, L->row_of_slot, L->w, T, L->D, g.k, L->dt, L->dout, L->dscore, stream));
+  DMOE_TRY(dmoe_expert_ffn_bwd(L->xd, L->h, L->hmask, L->dout, seg, El, L->R_cap, L->D, L->H, L->dt, L->W1, L->W2,
+                               L->dxd, L->dW1, L->db1, L->dW2, L->db2, L->ws, L->ws_bytes, stream));
+  DMOE_TRY(dmoe_gate_bwd(L->x, L->Wg, L->sel, L->dscore, L->dxd, L->row_of_slot, T, L->D, g, L->dt, L->dx, L->dWg,
+                         L->dbg, L->ws, L->ws_bytes, stream));
+  DMOE_CU(cudaMemcpyAsync(dx_host, L->dx, nbytes, cudaMemcpyDeviceToHost, s));
+  DMOE_CU(cudaEventRecord(cs->ev[3], cs->st));
+  DMOE_CU(cudaStreamWaitEvent(s, cs->ev[3], 0));  // the y download is part of this call's work
+#undef DMOE_CU
+  return DMOE_OK;
+}

@@ -143,6 +143,30 @@ class DMoELayer:
         self.forward(x, alive_bits, responded_bits)
         return self.backward(dy)
 
+    def host_desc(self, alive_bits, responded_bits):
+        """The include/dmoe.h dmoe_layer of this layer (device pointers; 2-linear experts, one GPU)
+        for dmoe_layer_step_host, with its own [T_max, D] device staging for x and dy."""
+        assert self.expert == "ffn2" and self.E_local == self.E and self.dW1.shape[0] == self.P
+        if not hasattr(self, "_stage_x"):
+            self._stage_x = torch.empty(self.T_max, self.D, dtype=self.dtype, device=self.y.device)
+            self._stage_dy = torch.empty_like(self._stage_x)
+        p = L._p
+        return L.dmoe_layer(
+            self.g, self.D, self.H, self.tie, L._dt(self.y), self.T_max, self.R_cap,
+            p(self.Wg), p(self.bg), p(self.W1), p(self.b1), p(self.W2), p(self.b2), p(alive_bits),
+            p(responded_bits), p(self._stage_x), p(self._stage_dy), p(self.G) if self.keep_G else None,
+            p(self.sel), p(self.sel_score), p(self.w), p(self.valid), p(self.n_dropped), p(self.counts),
+            p(self.offsets), p(self.seg), p(self.row_of_slot), p(self.token_of_row), p(self.xd), p(self.h),
+            p(self.hmask), p(self.out), p(self.y), p(self.dout), p(self.dscore), p(self.dxd), p(self.dW1),
+            p(self.db1), p(self.dW2), p(self.db2), p(self.dx), p(self.dWg), p(self.dbg), p(self.ws),
+            self.ws.numel())
+
+    def step_host_c(self, desc, hx, hdy, hy, hdx):
+        """One step through the C ABI's host-buffer entry point (dmoe_layer_step_host): x, dy in
+        and y, dX out as pinned host tensors, copies inside the call."""
+        L.dmoe_layer_step_host(desc, hx.shape[0], hx, hdy, hy, hdx)
+        return hdx
+
     def step_host(self, hx, hdy, hy, hdx, alive_bits, responded_bits):
         """One step from pinned host buffers: x in, y and dX out.  The dy upload overlaps the
         forward pass and the y download overlaps the backward pass (copy stream + events);
