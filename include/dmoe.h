@@ -68,7 +68,8 @@ typedef enum {
   DMOE_ERR_ARG = -1,         /* null pointer, negative size, bad enum */
   DMOE_ERR_SHAPE = -2,       /* dimension outside the supported envelope or inconsistent */
   DMOE_ERR_UNSUPPORTED = -3, /* valid request the library does not implement */
-  DMOE_ERR_CUDA = -4         /* a CUDA launch / driver call failed */
+  DMOE_ERR_CUDA = -4,        /* a CUDA launch / driver call failed */
+  DMOE_ERR_NONFINITE = -5    /* debug switch on (dmoe_set_check_finite): a NaN / Inf output */
 } dmoe_status;
 
 typedef enum { DMOE_F32 = 0, DMOE_BF16 = 1 } dmoe_dtype;
@@ -340,12 +341,20 @@ dmoe_status dmoe_ipc_open(const void* handle, void** ptr);
 dmoe_status dmoe_ipc_close(void* ptr);
 dmoe_status dmoe_ipc_free(void* ptr);
 
+/* Debug switch (off by default; the hot path never checks finiteness): with on != 0, the calls
+ * dmoe_gate_scores (G), dmoe_gate_topk (G), dmoe_expert_ffn_fwd (out rows [0, offsets[E_local])),
+ * dmoe_combine (y), dmoe_combine_bwd (dscore), dmoe_expert_ffn_bwd (dW1, dW2, db1, db2, dxd rows)
+ * and dmoe_gate_bwd (dWg, dbg, dx) scan their floating-point outputs after the launch,
+ * SYNCHRONISE the stream and return DMOE_ERR_NONFINITE (message: call and output) on a NaN or
+ * Inf — SPEC.md:40's "numeric error".  Process-wide; not for use inside graph capture. */
+void dmoe_set_check_finite(int on);
+
 /* One whole layer step from HOST buffers (the end-to-end unit): x and dy
  * are copied host -> device, S1-S10 run (forward: gate + beam search, dispatch, expert FFN,
  * combine; backward: combine backward, expert backward with dW written, gate backward), and y
- * and dX are copied device -> host, all on `stream` (dy's upload overlaps the forward and y's
- * download overlaps the backward on a library copy stream joined back into `stream` before the
- * call's work completes).  Every pointer in dmoe_layer is caller-owned DEVICE memory sized for
+ * and dX are copied device -> host, all on `stream` (x first; dy's upload then overlaps the
+ * forward and y's download overlaps the backward on a library copy stream joined back into
+ * `stream` before the call's work completes).  Every pointer in dmoe_layer is caller-owned DEVICE memory sized for
  * T_max tokens (the ones the per-call entry points above take); x_host, dy_host, y_host,
  * dx_host are host memory of [T, D] dt (pinned for asynchronous copies; pageable memory works
  * but the copies then synchronise).  tie > 1: the tied-weight pool (reading X20) with E / tie

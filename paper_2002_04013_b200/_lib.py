@@ -18,7 +18,8 @@ if not os.path.exists(LIB_PATH):
 _L = ctypes.CDLL(LIB_PATH)
 
 DMOE_F32, DMOE_BF16 = 0, 1
-_STATUS = {0: "DMOE_OK", -1: "DMOE_ERR_ARG", -2: "DMOE_ERR_SHAPE", -3: "DMOE_ERR_UNSUPPORTED", -4: "DMOE_ERR_CUDA"}
+_STATUS = {0: "DMOE_OK", -1: "DMOE_ERR_ARG", -2: "DMOE_ERR_SHAPE", -3: "DMOE_ERR_UNSUPPORTED", -4: "DMOE_ERR_CUDA",
+           -5: "DMOE_ERR_NONFINITE"}
 
 
 class dmoe_grid(ctypes.Structure):
@@ -88,6 +89,7 @@ _SIGS = {
     "dmoe_ipc_free": ([_P], ctypes.c_int),
     "dmoe_permute_rows": ([_P, _I32, _P, _P, _I32, _I32, _P, _P], ctypes.c_int),
     "dmoe_layer_step_host": ([_P, _I64, _P, _P, _P, _P, _P], ctypes.c_int),
+    "dmoe_set_check_finite": ([ctypes.c_int], None),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_L, _name)
@@ -302,3 +304,8 @@ def dmoe_layer_step_host(layer, T, x_host, dy_host, y_host, dx_host):
         assert not t.is_cuda and t.is_contiguous()
     _check("dmoe_layer_step_host", _L.dmoe_layer_step_host(ctypes.byref(layer), T, _p(x_host), _p(dy_host),
                                                            _p(y_host), _p(dx_host), _stream()))
+
+
+def dmoe_set_check_finite(on):
+    """Debug switch: calls scan their outputs, synchronise and raise DMOE_ERR_NONFINITE on NaN / Inf."""
+    _L.dmoe_set_check_finite(1 if on else 0)

@@ -281,6 +281,52 @@ size_t dmoe_workspace_bytes(int64_t T, int32_t D, int32_t H, dmoe_grid g, int32_
   return align_up(m, 4096);
 }
 
+// ------------------------------------------------------- finiteness check (debug switch)
+// Off by default (the hot path does not check finiteness); dmoe_set_check_finite(1)
+// (or DMOE_CHECK_FINITE in experiments builds) makes the calls below scan their floating-point
+// outputs after the launch, synchronise the stream and return DMOE_ERR_NONFINITE on a NaN / Inf.
+static int g_check_finite = -1;
+static bool finite_on() {
+  if (g_check_finite < 0) g_check_finite = dmoe_env("DMOE_CHECK_FINITE") ? 1 : 0;
+  return g_check_finite == 1;
+}
+__global__ void k_nonfinite(const void* p, int bf16, int64_t n, int* flag) {
+  int bad = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = bf16 ? __bfloat162float(((const __nv_bfloat16*)p)[i]) : ((const float*)p)[i];
+    bad |= !isfinite(v);
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+static dmoe_status finite_check(const char* call, const char* what, const void* p, dmoe_dtype dt, int64_t n,
+                                cudaStream_t s) {
+  if (!finite_on() || p == nullptr || n <= 0) return DMOE_OK;
+  static int* dflag[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) return set_error(DMOE_ERR_CUDA, "%s: finite check", call);
+  if (!dflag[dev] && cudaMalloc(&dflag[dev], sizeof(int)) != cudaSuccess)
+    return set_error(DMOE_ERR_CUDA, "%s: finite check flag", call);
+  int h = 0;
+  if (cudaMemsetAsync(dflag[dev], 0, sizeof(int), s) != cudaSuccess) return set_error(DMOE_ERR_CUDA, "%s", call);
+  const int64_t blocks = ceil_div(n, (int64_t)256) < 4096 ? ceil_div(n, (int64_t)256) : 4096;
+  k_nonfinite<<<(unsigned)blocks, 256, 0, s>>>(p, dt == DMOE_BF16, n, dflag[dev]);
+  if (cudaMemcpyAsync(&h, dflag[dev], sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return set_error(DMOE_ERR_CUDA, "%s: finite check: %s", call, cudaGetErrorString(cudaGetLastError()));
+  if (h) return set_error(DMOE_ERR_NONFINITE, "%s: non-finite value in %s", call, what);
+  return DMOE_OK;
+}
+// rows [0, offsets[E]) of a capacity buffer (reads offsets[E] back: the check synchronises anyway)
+static int64_t rows_used(const int32_t* offsets, int32_t E, cudaStream_t s) {
+  if (!finite_on()) return 0;
+  int32_t r = 0;
+  if (cudaMemcpyAsync(&r, offsets + E, sizeof(r), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return 0;
+  return r;
+}
+extern "C" void dmoe_set_check_finite(int on) { g_check_finite = on ? 1 : 0; }
+
 dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg,
                              const float* bg, dmoe_grid g, float* G, void* ws, size_t ws_bytes,
                              dmoe_stream_t stream) {
@@ -304,11 +350,13 @@ dmoe_status dmoe_gate_scores(const void* x, dmoe_dtype dt, int64_t T, int32_t D,
     DMOE_TRY(transpose(Wg, D, dM, dt, ws, s));
     r.B = ws;
     r.max_tiles = ceil_div(T, tc_rows_tile(r));
-    return tc_gemm_rows(r, s);
+    DMOE_TRY(tc_gemm_rows(r, s));
+  } else {
+    r.b_mn = true;
+    r.max_tiles = ceil_div(T, kPlanBM_SIMT);
+    DMOE_TRY(simt_gemm_rows(r, dt, s));
   }
-  r.b_mn = true;
-  r.max_tiles = ceil_div(T, kPlanBM_SIMT);
-  return simt_gemm_rows(r, dt, s);
+  return finite_check("gate_scores", "G", G, DMOE_F32, T * dM, s);
 }
 
 dmoe_status dmoe_gate_topk(const void* x, dmoe_dtype dt, int64_t T, int32_t D, const void* Wg, const float* bg,
@@ -412,7 +460,8 @@ dmoe_status dmoe_expert_ffn_fwd(const void* xd, const int32_t* offsets, int32_t 
   }
   DMOE_TRY(plans_for(g1, g2, offsets, E_local, plan_tc, plan_simt, s));
   DMOE_TRY(rows_gemm(g1, dt, s));
-  return rows_gemm(g2, dt, s);
+  DMOE_TRY(rows_gemm(g2, dt, s));
+  return finite_check("expert_ffn_fwd", "out", out, dt, rows_used(offsets, E_local, s) * D, s);
 }
 
 dmoe_status dmoe_combine(const void* out, const int32_t* row_of_slot, const float* w,
@@ -422,7 +471,8 @@ dmoe_status dmoe_combine(const void* out, const int32_t* row_of_slot, const floa
   DMOE_TRY(check_dt(dt, D));
   DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
   if (T > 0) { NN(row_of_slot); NN(w); NN(valid); NN(y); }
-  return combine(out, row_of_slot, w, valid, T, D, k, dt, y, (cudaStream_t)stream);
+  DMOE_TRY(combine(out, row_of_slot, w, valid, T, D, k, dt, y, (cudaStream_t)stream));
+  return finite_check("combine", "y", y, dt, T * D, (cudaStream_t)stream);
 }
 
 dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row_of_slot,
@@ -432,7 +482,8 @@ dmoe_status dmoe_combine_bwd(const void* dy, const void* out, const int32_t* row
   DMOE_TRY(check_dt(dt, D));
   DMOE_REQUIRE(T >= 0 && k >= 1 && k <= 16, DMOE_ERR_SHAPE, "T=%lld k=%d", (long long)T, k);
   if (T > 0) { NN(dy); NN(row_of_slot); NN(w); NN(dscore); }
-  return combine_bwd(dy, out, row_of_slot, w, T, D, k, dt, dout, dscore, nullptr, nullptr, (cudaStream_t)stream);
+  DMOE_TRY(combine_bwd(dy, out, row_of_slot, w, T, D, k, dt, dout, dscore, nullptr, nullptr, (cudaStream_t)stream));
+  return finite_check("combine_bwd", "dscore", dscore, DMOE_F32, T * k, (cudaStream_t)stream);
 }
 
 dmoe_status dmoe_combine_bwd_failures(const void* dy, const void* out, const int32_t* row_of_slot,
@@ -448,7 +499,7 @@ dmoe_status dmoe_combine_bwd_failures(const void* dy, const void* out, const int
                      (cudaStream_t)stream);
 }
 
-dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
+static dmoe_status expert_ffn_bwd_impl(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
                                 const int32_t* offsets, int32_t E_local, int64_t R_cap,
                                 int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
                                 const void* W2, void* dxd, void* dW1, float* db1, void* dW2,
@@ -534,6 +585,21 @@ dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* h
   if (fused) return DMOE_OK;
   DMOE_TRY(seg_colsum(dout, dt, offsets, E_local, D, db2, s));
   return seg_colsum(dh, dt, offsets, E_local, H, db1, s);
+}
+
+dmoe_status dmoe_expert_ffn_bwd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
+                                const int32_t* offsets, int32_t E_local, int64_t R_cap,
+                                int32_t D, int32_t H, dmoe_dtype dt, const void* W1,
+                                const void* W2, void* dxd, void* dW1, float* db1, void* dW2,
+                                float* db2, void* ws, size_t ws_bytes, dmoe_stream_t stream) {
+  DMOE_TRY(expert_ffn_bwd_impl(xd, h, hmask, dout, offsets, E_local, R_cap, D, H, dt, W1, W2, dxd, dW1, db1, dW2,
+                               db2, ws, ws_bytes, stream));
+  cudaStream_t s = (cudaStream_t)stream;
+  DMOE_TRY(finite_check("expert_ffn_bwd", "dW1", dW1, dt, (int64_t)E_local * H * D, s));
+  DMOE_TRY(finite_check("expert_ffn_bwd", "dW2", dW2, dt, (int64_t)E_local * D * H, s));
+  DMOE_TRY(finite_check("expert_ffn_bwd", "db1", db1, DMOE_F32, (int64_t)E_local * H, s));
+  DMOE_TRY(finite_check("expert_ffn_bwd", "db2", db2, DMOE_F32, (int64_t)E_local * D, s));
+  return finite_check("expert_ffn_bwd", "dxd", dxd, dt, rows_used(offsets, E_local, s) * D, s);
 }
 
 dmoe_status dmoe_expert_ffn_bwd_sgd(const void* xd, const void* h, const uint32_t* hmask, const void* dout,
@@ -699,8 +765,11 @@ dmoe_status dmoe_gate_bwd(const void* x, const void* Wg, const int32_t* sel, con
   DMOE_REQUIRE(T >= 0, DMOE_ERR_SHAPE, "T < 0");
   NN(Wg); NN(dWg); NN(dbg); NN(ws);
   if (T > 0) { NN(x); NN(sel); NN(dscore); NN(row_of_slot); NN(dx); }
-  return gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, T, D, g.d, g.M, g.k, dt, dx, dWg, dbg, ws,
-                  ws_bytes, (cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  DMOE_TRY(gate_bwd(x, Wg, sel, dscore, dxd, row_of_slot, T, D, g.d, g.M, g.k, dt, dx, dWg, dbg, ws, ws_bytes, s));
+  DMOE_TRY(finite_check("gate_bwd", "dWg", dWg, DMOE_F32, (int64_t)D * g.d * g.M, s));
+  DMOE_TRY(finite_check("gate_bwd", "dbg", dbg, DMOE_F32, (int64_t)g.d * g.M, s));
+  return finite_check("gate_bwd", "dx", dx, dt, T * D, s);
 }
 
 dmoe_status dmoe_segment_offsets(const int32_t* offsets, int32_t E, int32_t group, int32_t* seg,
@@ -871,12 +940,13 @@ extern "C" dmoe_status dmoe_layer_step_host(const dmoe_layer* L, int64_t T, cons
     cudaError_t e_ = (x_);                                                                          \
     if (e_ != cudaSuccess) return set_error(DMOE_ERR_CUDA, "layer_step_host: %s", cudaGetErrorString(e_)); \
   } while (0)
-  // dy: uploaded on the copy stream once the stream's earlier work (the previous step) is done
+  // x first (the forward waits for it), then dy on the copy stream while the forward runs (it
+  // would otherwise share the host link with x)
+  DMOE_CU(cudaMemcpyAsync(L->x, x_host, nbytes, cudaMemcpyHostToDevice, s));
   DMOE_CU(cudaEventRecord(cs->ev[0], s));
   DMOE_CU(cudaStreamWaitEvent(cs->st, cs->ev[0], 0));
   DMOE_CU(cudaMemcpyAsync(L->dy, dy_host, nbytes, cudaMemcpyHostToDevice, cs->st));
   DMOE_CU(cudaEventRecord(cs->ev[1], cs->st));
-  DMOE_CU(cudaMemcpyAsync(L->x, x_host, nbytes, cudaMemcpyHostToDevice, s));
   // forward (S1-S7)
   DMOE_TRY(dmoe_gate_topk(L->x, L->dt, T, L->D, L->Wg, L->bg, g, L->alive_bits, L->G, L->sel, L->sel_score, L->ws,
                           L->ws_bytes, stream));

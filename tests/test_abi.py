@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "dmoe.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int32_t|size_t|dmoe_status)\s+(dmoe_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int32_t|size_t|dmoe_status|void)\s+(dmoe_\w+)\s*\(", src, re.M)))
 
 
 def test_header_declares_the_north_star_calls():

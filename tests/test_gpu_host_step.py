@@ -39,3 +39,25 @@ def test_host_step_equals_per_call_path(name, T, T_run):
         if n in ("y", "dx"):
             got, want = got[:T_run], want[:T_run]
         assert torch.equal(got, want), n
+
+
+def test_check_finite_switch():
+    """dmoe_set_check_finite(1): a NaN reaching an output is reported as DMOE_ERR_NONFINITE (the
+    gate scores of a token with a NaN input); finite steps pass; off by default."""
+    from paper_2002_04013_b200 import _lib as L
+    cfg = CONFIGS["mnist"]
+    inp = make_inputs(cfg, seed=77, T=300)
+    lay = gpu_layer(cfg, inp)
+    x, dy, alive, resp = lay._inputs
+    L.dmoe_set_check_finite(True)
+    try:
+        lay.step(x, dy, alive, resp)          # finite: every checked output passes
+        bad = x.clone()
+        bad[5, 3] = float("nan")
+        with pytest.raises(L.DMoEError) as ei:
+            lay.forward(bad, alive, resp)
+        assert ei.value.status == -5 and "non-finite" in str(ei.value)
+    finally:
+        L.dmoe_set_check_finite(False)
+    lay.forward(bad, alive, resp)             # switch off: no check, no error
+    torch.cuda.synchronize()
