@@ -676,10 +676,17 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dead-frac", type=float, default=None,
+                    help="override the config's P(expert dead before selection) (alive-mask sweeps)")
+    ap.add_argument("--fail-frac", type=float, default=None, help="override the config's P(expert does not respond)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     os.environ.setdefault("OMP_NUM_THREADS", str(len(os.sched_getaffinity(0))))  # oracle baseline threads
     cfg = CONFIGS[args.config]
+    if args.dead_frac is not None:
+        cfg = cfg.with_(dead_frac=args.dead_frac)
+    if args.fail_frac is not None:
+        cfg = cfg.with_(fail_frac=args.fail_frac)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
@@ -749,7 +756,7 @@ def main():
         "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (counter-based generator, seeded)",
         "config": {"workload": cfg.name, "tokens_per_gpu": cfg.T, "grid": f"{cfg.M}^{cfg.d}", "E": cfg.E, "D": cfg.D,
-                   "H": cfg.H, "k": cfg.k, "beam": cfg.B, "fail_frac": cfg.fail_frac,
+                   "H": cfg.H, "k": cfg.k, "beam": cfg.B, "fail_frac": cfg.fail_frac, "dead_frac": cfg.dead_frac,
                    **({"param_slots": cfg.P, "tied": f"expert e -> slot e // {cfg.tie} (reading X20)"} if cfg.tie > 1
                       else {}),
                    **({"chunk_tokens": cfg.chunk, "update": "fused SGD per chunk (runtime Backward request, "

@@ -162,6 +162,28 @@ __device__ __forceinline__ void copy_row_warp(T* __restrict__ dst, const T* __re
   }
 }
 
+// two rows at once (8 loads per lane in flight before the first store)
+template <typename T>
+__device__ __forceinline__ void copy_rows2_warp(T* __restrict__ d0, const T* __restrict__ s0, T* __restrict__ d1,
+                                                const T* __restrict__ s1, int vecs, int lane) {
+  constexpr int V = Vec16<T>::N;
+  for (int v = lane; v < vecs; v += 32 * 4) {
+    uint4 a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v + 32 * u < vecs) {
+        a[u] = ld_nc_v4(s0 + (int64_t)(v + 32 * u) * V);
+        b[u] = ld_nc_v4(s1 + (int64_t)(v + 32 * u) * V);
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v + 32 * u < vecs) {
+        st_v4(d0 + (int64_t)(v + 32 * u) * V, a[u]);
+        st_v4(d1 + (int64_t)(v + 32 * u) * V, b[u]);
+      }
+  }
+}
+
 __device__ __forceinline__ int seg_of(const int32_t* __restrict__ offsets, int n, int64_t r) {
   int lo = 0, hi = n;  // offsets[lo] <= r < offsets[hi]
   while (hi - lo > 1) {
@@ -192,7 +214,16 @@ k_ep_push_rows(const T* __restrict__ src, const int32_t* __restrict__ gidx, cons
   int e = seg_of(offsets, E, r0);
   int64_t e_beg = offsets[e], e_end = offsets[e + 1];
   const int vecs = D / V;
-  for (int64_t r = r0; r < r1; ++r) {
+  int64_t r = r0;
+  for (; r + 1 < r1; r += 2) {
+    while (r >= e_end) { ++e; e_beg = e_end; e_end = offsets[e + 1]; }
+    T* d0 = peer_dst[e / El] + ((int64_t)base[e] + (r - e_beg)) * D;
+    while (r + 1 >= e_end) { ++e; e_beg = e_end; e_end = offsets[e + 1]; }
+    T* d1 = peer_dst[e / El] + ((int64_t)base[e] + (r + 1 - e_beg)) * D;
+    const int64_t s0 = gidx ? (int64_t)gidx[r] : r, s1 = gidx ? (int64_t)gidx[r + 1] : r + 1;
+    copy_rows2_warp(d0, src + s0 * D, d1, src + s1 * D, vecs, lane);
+  }
+  if (r < r1) {
     while (r >= e_end) { ++e; e_beg = e_end; e_end = offsets[e + 1]; }
     const int64_t srow = gidx ? (int64_t)gidx[r] : r;
     copy_row_warp(peer_dst[e / El] + ((int64_t)base[e] + (r - e_beg)) * D, src + srow * D, vecs, lane);
@@ -220,14 +251,20 @@ k_ep_return_rows(const T* __restrict__ src, const int32_t* __restrict__ cnt, con
   int el = seg_of(off_loc, El, q0);
   int64_t el_end = off_loc[el + 1];
   const int vecs = D / V;
-  for (int64_t q = q0; q < q1; ++q) {
+  auto dst_of = [&](int64_t q) -> T* {
     while (q >= el_end) { ++el; el_end = off_loc[el + 1]; }
     const int e = rank * El + el;
     int sidx = 0;
     while (sidx + 1 < G && q >= dst_off[sidx * El + el] + cnt[(int64_t)sidx * E + e]) ++sidx;
-    const int64_t drow = (int64_t)src_off[sidx * El + el] + (q - dst_off[sidx * El + el]);
-    copy_row_warp(peer_dst[sidx] + drow * D, src + q * D, vecs, lane);
+    return peer_dst[sidx] + ((int64_t)src_off[sidx * El + el] + (q - dst_off[sidx * El + el])) * D;
+  };
+  int64_t q = q0;
+  for (; q + 1 < q1; q += 2) {
+    T* d0 = dst_of(q);
+    T* d1 = dst_of(q + 1);
+    copy_rows2_warp(d0, src + q * D, d1, src + (q + 1) * D, vecs, lane);
   }
+  if (q < q1) copy_row_warp(dst_of(q), src + q * D, vecs, lane);
 }
 
 // ------------------------------------------------------------------ host entry points
