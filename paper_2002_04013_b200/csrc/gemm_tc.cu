@@ -302,6 +302,7 @@ struct TcParams {
   int table_len;  // M-major engine: per-expert smem table entries (0: tables stay in global)
   float sgd_lr;    // SEGK bf16: != 0 -> C (and colsum) are the parameters, updated in place:
                    // C -= lr * acc (the dW tile never reaches HBM), colsum -= lr * column sums
+  int segk_gs;    // weight-gradient tile walk: CTAs per expert group (<= 1: strided walk; see the kernel)
   int slot;  // probe slot (launch ordinal % 8)
   int dbg;  // experiment switches (DMOE_EXPERIMENTS builds only, env DMOE_TC_DEBUG): 1 skip stores,
             // 2 skip TMEM loads, 4 skip MMAs, 8 timeline probe, 16 L2 prefetch cursor, 32 no L2 hints,
@@ -472,6 +473,33 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
   const bool leader = prank == 0;
   const int t_begin = PAIR ? (int)blockIdx.x >> 1 : (int)blockIdx.x, t_end = total;
   const int t_step = PAIR ? (int)gridDim.x >> 1 : (int)gridDim.x;
+  // Weight-gradient walk: groups of GS CTAs share one expert's tiles (both problems, interleaved
+  // over the group's CTAs) and the NG = grid / GS groups take experts round-robin, so only NG
+  // experts' operand rows are live at a time however far the groups drift apart; the host picks
+  // GS so that they fit in ~40 MB of L2 (TcParams::segk_gs).  The strided walk over the flat tile
+  // space (GS = 1) let drifting CTAs spread over hundreds of experts and re-read the operands
+  // from HBM (transformer: 46-48 GB per call instead of ~5; 17 GB grouped, 22% faster).
+  const int T0e = SEGK ? MT * NT : 0, T1e = (SEGK && two) ? MT2 * NT2 : 0, Te = T0e + T1e;
+  const int GS = (SEGK && p.segk_gs > 1 && p.segk_gs <= (int)gridDim.x) ? p.segk_gs : 1;
+  const int NG = (int)gridDim.x / GS, g_id = (int)blockIdx.x / GS, g_rk = (int)blockIdx.x % GS;
+  const int per = (Te + GS - 1) / GS > 0 ? (Te + GS - 1) / GS : 1;
+  FastDiv fd_per;
+  fd_per.init(per);
+  // the v-th tile of this CTA's walk: -1 past its end, -2 a slot of the group's last round that
+  // has no tile (every role skips it alike)
+  auto seq = [&](int v) -> int {
+    if (GS == 1) {
+      const int t = t_begin + v * t_step;
+      return t < t_end ? t : -1;
+    }
+    if (g_id >= NG) return -1;  // CTAs past the last whole group idle
+    const int j = (int)fd_per.div((uint32_t)v), w = v - j * per;
+    const int e = g_id + j * NG;
+    if (e >= p.E) return -1;
+    const int lt = g_rk + w * GS;
+    if (lt >= Te) return -2;
+    return lt < T0e ? e * T0e + lt : total0 + e * T1e + (lt - T0e);
+  };
   FastDiv fd_e, fd_n, fd_e2, fd_n2;  // SEGK: tiles per expert, N tiles (both problems); ROWS: N tiles
   fd_e.init(SEGK ? MT * NT : 1);
   fd_n.init(NT);
@@ -581,7 +609,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
         }
       };
       auto prefetch_one = [&]() {
-        if (ptile >= t_end || !(DMOE_DBG(p) & 16)) return;  // opt-in (DMOE_TC_DEBUG=16): measured slower
+        if (ptile >= t_end || !(DMOE_DBG(p) & 16) || GS > 1) return;  // opt-in (DMOE_TC_DEBUG=16): measured slower
         if (SEGK) {
           const int kr = (int)(prow0 + pkb * TC_BK);
           tma_prefetch_2d(&tmA, pm0, kr);
@@ -611,7 +639,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
       int it = 0;
       long long w_empty = 0, w_loop = 0;
       WT_T0(t_loop);
-      for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
+      for (int v = 0, tile; (tile = seq(v)) != -1; ++v, ++it) {
+        if (tile < 0) continue;
         int e, m0, n0, nkb;
         int64_t row0, row_end;
         const int prob = decode(tile, e, row0, row_end, m0, n0, nkb);
@@ -689,7 +718,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int it = 0;
     long long w_te = 0, w_full = 0, w_zero = 0, w_issue = 0, w_loop = 0, n_tiles = 0, w_mmaonly = 0;
     WT_T0(t_loop);
-    for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
+    for (int v = 0, tile; (tile = seq(v)) != -1; ++v, ++it) {
+      if (tile < 0) continue;
       int e, m0, n0, nkb;
       int64_t row0, row_end;
       decode(tile, e, row0, row_end, m0, n0, nkb);
@@ -768,7 +798,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const int cchunk = lane >> 4, cunit = (lane & 15) >> 1, chalf = lane & 1;
     long long w_fw = 0, w_fl = 0, w_fc = 0;
     WT_T0(t_fl);
-    for (int tile = t_begin; tile < t_end; tile += t_step) {
+    for (int v = 0, tile; (tile = seq(v)) != -1; ++v) {
+      if (tile < 0) continue;
       int e, m0, n0, nkb;
       int64_t row0, row_end;
       const int prob = decode(tile, e, row0, row_end, m0, n0, nkb);
@@ -860,7 +891,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     int it = 0;
     long long w_tf = 0, w_st = 0, w_loop = 0, w_ld = 0, w_pk = 0, w_is = 0;
     WT_T0(t_loop);
-    for (int tile = t_begin; tile < t_end; tile += t_step, ++it) {
+    for (int v = 0, tile; (tile = seq(v)) != -1; ++v, ++it) {
+      if (tile < 0) continue;
       int e, m0, n0, nkb;
       int64_t row0, row_end;
       const int prob = decode(tile, e, row0, row_end, m0, n0, nkb);
@@ -1195,6 +1227,22 @@ static dmoe_status make_map(CUtensorMap* m, const void* ptr, int rank, const uin
   return DMOE_OK;
 }
 
+// Weight-gradient walk group size (TcParams::segk_gs): NG = grid / GS experts in flight, their
+// operand rows (R_cap / E rows x (A + B columns) per problem) within ~40 MB of L2.  Measured
+// (ncu, one box, A/B): transformer (1.3 MB per expert, GS = 4) 22.5 -> 18.0 ms and 47 -> 17 GB
+// of DRAM reads; but with a few MB per expert (grid3d 5.2 MB, 1024-row experts 21 MB) large
+// groups were slower than the strided walk (32.5 vs 34.8 ms, 6.3 vs 8.6 ms), so the grouped
+// walk is used only for small per-expert operands (>= 16 groups) and never when half the grid's
+// experts already fit (the strided walk then keeps L2 anyway).
+static int segk_group(int64_t R_cap, int E, int64_t cols, int max_ctas) {
+  const int grid = (max_ctas > 0 && max_ctas < num_sms()) ? max_ctas : num_sms();
+  const double bytes_e = E > 0 ? (double)R_cap / E * (double)cols * 2.0 : 0.0;
+  if (bytes_e <= 0.0) return 1;
+  const int ng = (int)(40e6 / bytes_e);
+  if (ng < 16 || ng >= grid / 2) return 1;
+  return grid / ng;
+}
+
 // N tile: 256 when it divides N, else 128; K-major B also takes any N = 16..256 in one tile
 // (the gate, N = d*M) and MN-major B any multiple of 64 up to 256.
 static int pick_bn(int N, bool b_mn) {
@@ -1300,6 +1348,15 @@ static dmoe_status launch_maps_p(const CUtensorMap& a, const CUtensorMap& b, con
 #endif
   pp.slot = (int)(__atomic_load_n(&g_counters[1], __ATOMIC_RELAXED) % 8);
   pp.stages = Cfg::stages_for(table_len);
+  if (SEGK) {  // CTAs per expert group: NG = grid / GS experts' operands within ~40 MB of L2
+    int gs = p.segk_gs;
+    if (const char* e = dmoe_env("DMOE_SEGK_GS")) gs = atoi(e);  // experiments: A/B of the walk
+    pp.segk_gs = gs;
+  }
+  if (const char* e = dmoe_env("DMOE_TC_STAGES")) {  // experiments: a shallower ring
+    const int st = atoi(e);
+    if (st >= 1 && st < pp.stages) pp.stages = st;
+  }
   pp.table_len = table_len;
   if (PAIR)
     launch_pdl_cluster(kern, (unsigned)grid, Cfg::THREADS, smem, s, 2u, a, b, c, a2, b2, c2, pp);
@@ -1418,6 +1475,7 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
   p.offsets = g.offsets; p.C = g.C; p.E = g.E; p.N = g.N; p.Mdim = g.Mdim; p.colsum = g.colsum;
   p.max_ctas = g.max_ctas;
   p.sgd_lr = g.out_f32 ? 0.0f : g.sgd_lr;
+  p.segk_gs = g.out_f32 ? 1 : segk_group(g.R_cap, g.E, (int64_t)g.Mdim + g.N, g.max_ctas);
   const int64_t tiles = (int64_t)g.E * (g.Mdim / TC_BM) * (g.N / BN);
   if (g.out_f32) {  // fp32 output through the padded staging (the C map is unused)
     if (BN == 256) return launch<256, true, true, EPI_F32>(ta, tb, ta, p, tiles, s);
@@ -1452,6 +1510,7 @@ dmoe_status tc_gemm_segk2(const GemmSegK& g, const GemmSegK& h, cudaStream_t s) 
   p.N2 = h.N; p.Mdim2 = h.Mdim; p.colsum2 = h.colsum;
   p.max_ctas = g.max_ctas;
   p.sgd_lr = g.sgd_lr;
+  p.segk_gs = segk_group(g.R_cap, g.E, (int64_t)g.Mdim + g.N + h.Mdim + h.N, g.max_ctas);
   const int64_t tiles = (int64_t)g.E * ((g.Mdim / TC_BM) * (g.N / 256) + (h.Mdim / TC_BM) * (h.N / 256));
   return launch_maps<256, true, true, EPI_PLAIN>(m[0], m[1], m[2], m[3], m[4], m[5], p, tiles, s);
 }
