@@ -6,6 +6,7 @@ NVFLAGS   := $(ARCH) -O3 -std=c++17 -lineinfo -Xcompiler -fPIC -Xcompiler -Wall 
 ifdef EXPERIMENTS
 NVFLAGS   += -DDMOE_EXPERIMENTS
 endif
+NVFLAGS   += $(XFLAGS)   # extra -D tuning flags for A/B builds (never set by build())
 CFLAGS    := -O2 -fPIC -fopenmp -Wall -std=c11
 
 PKG       := paper_2002_04013_b200

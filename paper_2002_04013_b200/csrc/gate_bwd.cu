@@ -54,6 +54,15 @@ dmoe_status transpose(const void* src, int64_t rows, int64_t cols, dmoe_dtype dt
 // bias partial db_g = sum_t dG[t] (lane owns columns lane + 32 m; warps combined in a fixed order:
 // deterministic).  Block 0 writes the token chunk bounds of the split-K dW_g GEMM.
 constexpr int kGbWarps = 4;
+// k <= 4: two 16-byte vectors per lane per row in flight and 5 CTAs (20 warps) per SM (93
+// registers) beat four vectors at 3 CTAs per SM (transformer 295-358 -> 204 us, grid3d 1.2-1.6 ->
+// 0.85-1.36 ms in one launch list)
+#ifndef GBDX_UNR4
+#define GBDX_UNR4 2
+#endif
+#ifndef GBDX_MINB
+#define GBDX_MINB 5
+#endif
 
 template <int KMAX>
 struct GbRec {  // a token's routing record: dispatched rows, dscore, gate columns (one byte per level)
@@ -89,7 +98,7 @@ struct GbRec {  // a token's routing record: dispatched rows, dscore, gate colum
 };
 
 template <typename T, int KMAX>
-__global__ void __launch_bounds__(kGbWarps * 32)
+__global__ void __launch_bounds__(kGbWarps * 32, KMAX <= 4 ? GBDX_MINB : 1)
 k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
               const float* __restrict__ dscore, const T* __restrict__ dxd,
               const int32_t* __restrict__ row_of_slot, int64_t Tn, int32_t D, int d, int M, int k,
@@ -98,7 +107,7 @@ k_gate_bwd_dx(const T* __restrict__ WgT, const int32_t* __restrict__ sel,
               int64_t tpc) {
   DMOE_PDL_ENTRY();
   constexpr int V = Vec16<T>::N;
-  constexpr int UNR = KMAX <= 4 ? 4 : (KMAX <= 8 ? 2 : 1);  // 16-byte vectors per lane per row in flight
+  constexpr int UNR = KMAX <= 4 ? GBDX_UNR4 : (KMAX <= 8 ? 2 : 1);  // 16-byte vectors per lane per row in flight
   constexpr int NB = 8;                                      // gate columns per lane (d*M <= 256)
   __shared__ float bsh[kGbWarps][NB * 32];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

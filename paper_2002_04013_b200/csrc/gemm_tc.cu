@@ -280,6 +280,15 @@ struct FastDiv {
   __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
 };
 
+// Weight-gradient tail boxes: the last K block of an expert with at most `rows` rows left (e.g.
+// the 1-16 rows of a 65-80-row expert at transformer) is loaded with these `rows`-row boxes
+// instead of the 64-row ones (the MMA reads only the 16-row slices holding segment rows).
+// rows == 0: none.
+struct TcTail {
+  CUtensorMap a, b, a2, b2;
+  int rows;
+};
+
 // ------------------------------------------------------------------------- kernel
 struct TcParams {
   const int32_t* offsets;  // [E+1] or nullptr (single group of rows_single rows)
@@ -315,6 +324,7 @@ constexpr int TC_STAGE_WARP = 5 * 1024;           // one warp's 32-row staging t
 constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan live in smem
 
 constexpr int TC_MAX_STAGES = 8;
+constexpr int kTailRows = 32;  // weight-gradient tail boxes (TcTail)
 
 template <int BN, bool SEGK = false, bool PAIR = false> struct TcCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
@@ -357,7 +367,8 @@ template <int BN, bool SEGK, bool B_MN, int EPI, bool PAIR = false>
 __global__ void __launch_bounds__(TcCfg<BN, SEGK, PAIR>::THREADS, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
           const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmA2,
-          const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC2, const TcParams p) {
+          const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmC2, const TcParams p,
+          const __grid_constant__ TcTail tail) {
   using Cfg = TcCfg<BN, SEGK, PAIR>;
   static_assert(!PAIR || (!SEGK && BN == 256), "CTA pairs: 256-wide row GEMM tiles only");
   constexpr int RT = PAIR ? 2 * TC_BM : TC_BM;   // rows per row tile (a pair: 128 per CTA)
@@ -675,11 +686,12 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             if (++stage == S) { stage = 0; phase ^= 1; }
             continue;
           }
-          mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           if (SEGK) {
             const int kr = (int)(row0 + kb * TC_BK);
-            const CUtensorMap* mA = prob ? &tmA2 : &tmA;
-            const CUtensorMap* mB = prob ? &tmB2 : &tmB;
+            const bool tl = tail.rows > 0 && row_end - kr <= tail.rows;  // a short last K block
+            mbar_expect_tx(&full[stage], tl ? (2 + BN / 64) * tail.rows * 128 : Cfg::STAGE_BYTES);
+            const CUtensorMap* mA = tl ? (prob ? &tail.a2 : &tail.a) : (prob ? &tmA2 : &tmA);
+            const CUtensorMap* mB = tl ? (prob ? &tail.b2 : &tail.b) : (prob ? &tmB2 : &tmB);
             // one 2D box per 64 columns (a 3D {64, rows, chunks} view taking a whole operand per
             // command measured no faster and read 64% more DRAM bytes: 19.0 vs 11.6 GB per call)
             tma_load_2d_h(sa, mA, &full[stage], m0, kr, pol_keep);
@@ -688,6 +700,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             for (int c = 0; c < BN / 64; ++c)
               tma_load_2d_h(sb + c * 8192, mB, &full[stage], n0 + 64 * c, kr, pol_keep);
           } else {
+            mbar_expect_tx(&full[stage], Cfg::STAGE_BYTES);
             tma_load_2d_h(sa, &tmA, &full[stage], kb * TC_BK, (int)row0, pol_keep);
             if (B_MN) {
 #pragma unroll
@@ -1320,7 +1333,12 @@ static int debug_flags_segk() {
 template <int BN, bool SEGK, bool B_MN, int EPI, bool PAIR>
 static dmoe_status launch_maps_p(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                                  const CUtensorMap& a2, const CUtensorMap& b2, const CUtensorMap& c2,
-                                 const TcParams& p, int64_t max_tiles, cudaStream_t s) {
+                                 const TcParams& p, int64_t max_tiles, cudaStream_t s,
+                                 const TcTail* tail_in = nullptr) {
+  TcTail tail;
+  if (tail_in) tail = *tail_in;
+  else { memset(&tail, 0, sizeof(tail)); }
+  if (dmoe_env("DMOE_TC_NOTAIL")) tail.rows = 0;  // experiments: A/B of the tail boxes
   using Cfg = TcCfg<BN, SEGK, PAIR>;
   auto kern = k_tc_gemm<BN, SEGK, B_MN, EPI, PAIR>;
   const int table_len = (p.offsets && p.E <= TC_TABLE_E) ? ((p.E + 4) & ~3) : 0;
@@ -1359,22 +1377,23 @@ static dmoe_status launch_maps_p(const CUtensorMap& a, const CUtensorMap& b, con
   }
   pp.table_len = table_len;
   if (PAIR)
-    launch_pdl_cluster(kern, (unsigned)grid, Cfg::THREADS, smem, s, 2u, a, b, c, a2, b2, c2, pp);
+    launch_pdl_cluster(kern, (unsigned)grid, Cfg::THREADS, smem, s, 2u, a, b, c, a2, b2, c2, pp, tail);
   else
-    launch_pdl(kern, (unsigned)grid, Cfg::THREADS, smem, s, a, b, c, a2, b2, c2, pp);
+    launch_pdl(kern, (unsigned)grid, Cfg::THREADS, smem, s, a, b, c, a2, b2, c2, pp, tail);
   __atomic_fetch_add(&g_counters[1], 1, __ATOMIC_RELAXED);
   return check_launch("tc_gemm");
 }
 template <int BN, bool SEGK, bool B_MN, int EPI>
 static dmoe_status launch_maps(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                                const CUtensorMap& a2, const CUtensorMap& b2, const CUtensorMap& c2,
-                               const TcParams& p, int64_t max_tiles, cudaStream_t s) {
-  return launch_maps_p<BN, SEGK, B_MN, EPI, false>(a, b, c, a2, b2, c2, p, max_tiles, s);
+                               const TcParams& p, int64_t max_tiles, cudaStream_t s,
+                               const TcTail* tail = nullptr) {
+  return launch_maps_p<BN, SEGK, B_MN, EPI, false>(a, b, c, a2, b2, c2, p, max_tiles, s, tail);
 }
 template <int BN, bool SEGK, bool B_MN, int EPI>
 static dmoe_status launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const TcParams& p,
-                          int64_t max_tiles, cudaStream_t s) {
-  return launch_maps<BN, SEGK, B_MN, EPI>(a, b, c, a, b, c, p, max_tiles, s);
+                          int64_t max_tiles, cudaStream_t s, const TcTail* tail = nullptr) {
+  return launch_maps<BN, SEGK, B_MN, EPI>(a, b, c, a, b, c, p, max_tiles, s, tail);
 }
 
 template <int BN>
@@ -1481,8 +1500,14 @@ dmoe_status tc_gemm_segk(const GemmSegK& g, cudaStream_t s) {
     if (BN == 256) return launch<256, true, true, EPI_F32>(ta, tb, ta, p, tiles, s);
     return launch<128, true, true, EPI_F32>(ta, tb, ta, p, tiles, s);
   }
-  if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
-  return launch<128, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s);
+  TcTail tail;
+  memset(&tail, 0, sizeof(tail));
+  DMOE_TRY(make_map(&tail.a, g.A, 2, adims, kTailRows));
+  DMOE_TRY(make_map(&tail.b, g.B, 2, bdims, kTailRows));
+  tail.a2 = tail.a; tail.b2 = tail.b;
+  tail.rows = (g.E > 0 && g.R_cap <= (int64_t)2 * TC_BK * g.E) ? kTailRows : 0;  // see tc_gemm_segk2
+  if (BN == 256) return launch<256, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s, &tail);
+  return launch<128, true, true, EPI_PLAIN>(ta, tb, tc, p, tiles, s, &tail);
 }
 
 // two weight-gradient GEMMs over the same segments in one persistent launch (the expert
@@ -1494,10 +1519,21 @@ bool tc_segk2_supported(const GemmSegK& a, const GemmSegK& b) {
 }
 dmoe_status tc_gemm_segk2(const GemmSegK& g, const GemmSegK& h, cudaStream_t s) {
   CUtensorMap m[6];
+  TcTail tail;
+  memset(&tail, 0, sizeof(tail));
+  // tail boxes pay off for experts of ~1 K block (transformer, same-box A/B: 18.0 -> 17.6 ms,
+  // 16.5 -> 14 GB read) and not at 256 rows (grid3d 32.7 -> 33.7 ms)
+  tail.rows = (g.E > 0 && g.R_cap <= (int64_t)2 * TC_BK * g.E) ? kTailRows : 0;
   const GemmSegK* gs[2] = {&g, &h};
   for (int i = 0; i < 2; ++i) {
     const GemmSegK& x = *gs[i];
     const uint64_t rc = (uint64_t)(x.R_cap > 0 ? x.R_cap : 1);
+    {
+      uint64_t adims[2] = {(uint64_t)x.Mdim, rc};
+      uint64_t bdims[2] = {(uint64_t)x.N, rc};
+      DMOE_TRY(make_map(i ? &tail.a2 : &tail.a, x.A, 2, adims, kTailRows));
+      DMOE_TRY(make_map(i ? &tail.b2 : &tail.b, x.B, 2, bdims, kTailRows));
+    }
     uint64_t cdims[2] = {(uint64_t)x.N, (uint64_t)x.E * x.Mdim};
     uint64_t adims[2] = {(uint64_t)x.Mdim, rc};
     uint64_t bdims[2] = {(uint64_t)x.N, rc};
@@ -1512,7 +1548,7 @@ dmoe_status tc_gemm_segk2(const GemmSegK& g, const GemmSegK& h, cudaStream_t s) 
   p.sgd_lr = g.sgd_lr;
   p.segk_gs = segk_group(g.R_cap, g.E, (int64_t)g.Mdim + g.N + h.Mdim + h.N, g.max_ctas);
   const int64_t tiles = (int64_t)g.E * ((g.Mdim / TC_BM) * (g.N / 256) + (h.Mdim / TC_BM) * (h.N / 256));
-  return launch_maps<256, true, true, EPI_PLAIN>(m[0], m[1], m[2], m[3], m[4], m[5], p, tiles, s);
+  return launch_maps<256, true, true, EPI_PLAIN>(m[0], m[1], m[2], m[3], m[4], m[5], p, tiles, s, &tail);
 }
 
 }  // namespace dmoe
