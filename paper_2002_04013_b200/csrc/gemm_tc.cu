@@ -324,7 +324,10 @@ constexpr int TC_STAGE_WARP = 5 * 1024;           // one warp's 32-row staging t
 constexpr int TC_TABLE_E = 2048;                  // experts whose offsets/plan live in smem
 
 constexpr int TC_MAX_STAGES = 8;
-constexpr int kTailRows = 32;  // weight-gradient tail boxes (TcTail)
+#ifndef DMOE_TAIL_ROWS
+#define DMOE_TAIL_ROWS 32
+#endif
+constexpr int kTailRows = DMOE_TAIL_ROWS;  // weight-gradient tail boxes (TcTail)
 
 template <int BN, bool SEGK = false, bool PAIR = false> struct TcCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
