@@ -48,15 +48,21 @@ __global__ void k_prefix_alive(const uint32_t* __restrict__ alive, int d, int M,
 }
 
 constexpr int kSmemPAWords = 2048;  // prefix bitmaps up to 64K bits live in smem
-constexpr int kBeamTok = 128;       // tokens per CTA tile
-constexpr int kBeamThreads = 256;   // threads per CTA: (token, level) list tasks, then a merge per token
+#ifndef DMOE_BEAM_TOK
+#define DMOE_BEAM_TOK 128
+#endif
+#ifndef DMOE_BEAM_MINB
+#define DMOE_BEAM_MINB 2
+#endif
+constexpr int kBeamTok = DMOE_BEAM_TOK;        // tokens per CTA tile
+constexpr int kBeamThreads = 2 * kBeamTok;     // threads per CTA: (token, level) list tasks, then a merge per token
 
 // Thread per token (beam.cuh): the CTA stages its 128 tokens' G rows in shared memory with
 // coalesced 16-byte loads (row pitch d*M + 1 floats: the threads' column reads hit 32 distinct
 // banks), builds the prefix-alive bitmaps in shared memory (small grids) and notes whether every
 // expert is alive (then FilterAlive is a no-op and the unmasked search runs).
 template <int WMAX>
-__global__ void __launch_bounds__(kBeamThreads, 2)
+__global__ void __launch_bounds__(kBeamThreads, DMOE_BEAM_MINB)
 k_beam_topk(const float* __restrict__ G, int64_t T, int d, int M, int k, int B,
             const uint32_t* __restrict__ PA_global, const uint32_t* __restrict__ alive, int pa_words,
             int32_t* __restrict__ sel, float* __restrict__ sel_score) {
